@@ -1,0 +1,196 @@
+/*
+ * ssfm.h -- C-ABI of the B200-native sparse Levenberg-Marquardt core
+ * (bundle adjustment + global positioning) of InstantSfM (arXiv 2510.13310).
+ *
+ * This is the drop-in boundary that replaces the reference package's
+ * native layer and the numpy/scipy hot path under `lm_solve`:
+ *
+ *   reference (sparsesfm, /root/reference/pkg/src/sparsesfm)      -> here
+ *   ----------------------------------------------------------------------
+ *   BAProblem.__init__            ba.py:35-64                      ssfm_create_ba
+ *   GPProblem.__init__/fix_gauge  gp.py:33-67, gp.py:193-201       ssfm_create_gp
+ *   problem.cost(theta)           ba.py:133-138, gp.py:103-107     ssfm_cost
+ *   problem.linearize(theta)      ba.py:140-194, gp.py:109-128     ssfm_linearize
+ *   jtj_fill_cy / jtr_fill_cy     _kernels/_core.pyx:18-97         (inside ssfm_linearize)
+ *   apply_damping                 sparse_block.py:406-426          (inside ssfm_solve_normal)
+ *   solve_normal -> _solve_schur  lm.py:537-720                    ssfm_solve_normal
+ *   schur_fill_cy + dense S@p     _core.pyx:100-160, lm.py:656     (implicit S*p, inside the PCG)
+ *   problem.post_step / renormalize  ba.py:196-197, lm.py:104-117,
+ *                                 gp.py:130-147                    ssfm_post_step
+ *   lm_solve                      lm.py:727-800                    ssfm_lm_solve
+ *   JtJPattern.off_keys           sparse_block.py:219-323          ssfm_export_pattern
+ *
+ * Conventions
+ *   - Plain pointers and sizes only. Array pointers are DEVICE pointers on the
+ *     handle's device unless a parameter says "host". Streams are passed as
+ *     `void*` (a cudaStream_t; NULL = legacy default stream).
+ *   - theta is the reference parameter vector, same layout (lm.py, ba.py:68-81,
+ *     gp.py:71-80): BA [C x (q4,t3)] ++ [P x 3] ++ [C focal | 1 shared | none];
+ *     GP [C x 3] ++ [P x 3] ++ [N scales | none in depth mode].
+ *   - All arithmetic is IEEE fp64.
+ *   - Every entry point returns an ssfm_status; ssfm_last_error() gives the
+ *     message of the last failure on the calling thread.
+ *   - A handle is not thread-safe; separate handles may run concurrently.
+ */
+#ifndef SSFM_H
+#define SSFM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes, 1:1 with the reference exception taxonomy (errors.py:4-77). */
+typedef enum {
+  SSFM_OK = 0,
+  SSFM_SINGULAR_BLOCK = 1,      /* errors.SingularBlock      (errors.py:20)  */
+  SSFM_CG_STALL = 2,            /* errors.CGStall            (errors.py:24)  */
+  SSFM_SOLVER_FAILURE = 3,      /* errors.SolverFailure      (errors.py:28)  */
+  SSFM_ZERO_QUATERNION = 4,     /* errors.ZeroQuaternion     (errors.py:39)  */
+  SSFM_EMPTY_PROBLEM = 5,       /* errors.EmptyProblem       (errors.py:43)  */
+  SSFM_MISSING_DEPTH = 6,       /* errors.MissingDepth       (errors.py:47)  */
+  SSFM_LAYOUT_MISMATCH = 7,     /* errors.LayoutMismatch     (errors.py:12)  */
+  SSFM_DIMENSION_MISMATCH = 8,  /* errors.DimensionMismatch  (errors.py:16)  */
+  SSFM_INVALID_ARGUMENT = 9,    /* ValueError / IndexError                    */
+  SSFM_CUDA_ERROR = 10,
+  SSFM_NCCL_ERROR = 11
+} ssfm_status;
+
+/* Termination reasons of SolveReport.termination (lm.py:61-83). */
+typedef enum {
+  SSFM_TERM_MAX_ITER = 0,
+  SSFM_TERM_CONVERGED_COST = 1,
+  SSFM_TERM_CONVERGED_GRAD = 2,
+  SSFM_TERM_SOLVER_FAILURE = 3
+} ssfm_termination;
+
+enum { SSFM_PINHOLE = 0, SSFM_BAL_RADIAL = 1 };   /* scene.py:19-20 */
+enum { SSFM_LOSS_TRIVIAL = 0, SSFM_LOSS_HUBER = 1 }; /* scene.py:233-242 */
+
+/* LMConfig (lm.py:36-58). solver: 0 = schur_pcg (the only device solver). */
+typedef struct {
+  int32_t max_iterations;
+  double lambda0, lambda_up, lambda_down, lambda_min, lambda_max;
+  double rel_cost_tol, grad_tol;
+  int32_t cg_max_iters;
+  double cg_tol;
+} ssfm_lm_config;
+
+/* IterationRecord (lm.py:61-69). */
+typedef struct {
+  int32_t iteration;
+  int32_t step_accepted;
+  int32_t cg_iters;
+  int32_t status;          /* in-step failure that caused a rejection, else 0 */
+  double cost_before, cost_after, lam;
+  int64_t wall_time_ns;    /* host clock around the iteration, like lm.py:755 */
+  double device_ms;        /* CUDA-event time of the iteration on the stream */
+} ssfm_iter_record;
+
+/* BAProblem(scene, loss, optimize_focal, shared_focal), ba.py:35-64.
+ * Observation arrays are in the scene's observation order (residual order). */
+typedef struct {
+  int32_t num_cameras;
+  int32_t num_points;
+  int64_t num_obs;
+  int32_t model;           /* SSFM_PINHOLE | SSFM_BAL_RADIAL */
+  int32_t optimize_focal;
+  int32_t shared_focal;
+  int32_t loss_kind;
+  double loss_delta;
+  const int32_t* cam_idx;  /* [N] device */
+  const int32_t* pt_idx;   /* [N] device */
+  const double* pixels;    /* [N,2] device */
+  const double* pps;       /* [C,2] device, principal points */
+  const double* dists;     /* [C,2] device, bal radial (k1,k2) */
+  const double* focals;    /* [C] device, used when optimize_focal == 0 */
+} ssfm_ba_desc;
+
+/* GPProblem(rays, fixed_rotations, cam_idx, pt_idx, num_points, loss,
+ * depth_mode, depths) + fix_gauge, gp.py:33-67 / gp.py:193-201. */
+typedef struct {
+  int32_t num_cameras;
+  int32_t num_points;
+  int64_t num_obs;
+  int32_t depth_mode;
+  int32_t gauge_fixed;
+  int32_t loss_kind;
+  double loss_delta;
+  const int32_t* cam_idx;  /* [N] device */
+  const int32_t* pt_idx;   /* [N] device */
+  const double* rays;      /* [N,3] device, unit world rays (make_rays) */
+  const double* depths;    /* [N] device ray distances, depth mode only (else NULL) */
+} ssfm_gp_desc;
+
+typedef struct ssfm_handle ssfm_handle;
+
+const char* ssfm_last_error(void);
+const char* ssfm_version(void);
+
+/* Build a problem: copies the inputs into the handle's device arena and builds
+ * the point-major / camera-major orderings, segments and work tiles on the
+ * device (replaces JtJPattern / JtrPattern / _SchurPlan construction,
+ * sparse_block.py:219-363, lm.py:236-483). */
+int ssfm_create_ba(const ssfm_ba_desc* desc, void* stream, ssfm_handle** out);
+int ssfm_create_gp(const ssfm_gp_desc* desc, void* stream, ssfm_handle** out);
+int ssfm_destroy(ssfm_handle* h);
+
+int64_t ssfm_num_params(const ssfm_handle* h);
+int64_t ssfm_num_residuals(const ssfm_handle* h);
+int64_t ssfm_device_bytes(const ssfm_handle* h);
+
+/* cost(theta) -> *cost_host (blocking). ba.py:133-138 / gp.py:103-107. */
+int ssfm_cost(ssfm_handle* h, const double* theta, double* cost_host, void* stream);
+
+/* linearize(theta): fills the handle's compact Jacobian and the block
+ * normal-equation pieces. Optional exports in the reference layout
+ * (ba.py:185-193, gp.py:118-128): r [total_residuals], J [N x 22 | 21 | 18]
+ * row-major per entry, grad = J^T r [total_params] (jtr, sparse_block.py:388).
+ * *grad_max_host (may be NULL) = max |J^T r| (lm.py:762). */
+int ssfm_linearize(ssfm_handle* h, const double* theta, double* r_out,
+                   double* J_out, double* grad_out, double* grad_max_host,
+                   void* stream);
+
+/* solve_normal(apply_damping(jtj, lambda), ...) (lm.py:537-720) on the state of
+ * the last ssfm_linearize; delta [total_params] device. Returns SSFM_OK,
+ * SSFM_SINGULAR_BLOCK or SSFM_CG_STALL (a rejection inside lm_solve). */
+int ssfm_solve_normal(ssfm_handle* h, double lambda, const ssfm_lm_config* cfg,
+                      double* delta, int32_t* cg_iters_host, void* stream);
+
+/* post_step in place (renormalize lm.py:104-117 / GP gauge gp.py:130-147). */
+int ssfm_post_step(ssfm_handle* h, double* theta, void* stream);
+
+/* lm_solve (lm.py:727-800). theta in/out (device). recs: host array of cap
+ * records; *n_recs = records written; *termination = ssfm_termination.
+ * Returns SSFM_SOLVER_FAILURE (records still valid) when the linear solve
+ * fails with lambda at lambda_max. */
+int ssfm_lm_solve(ssfm_handle* h, double* theta, const ssfm_lm_config* cfg,
+                  ssfm_iter_record* recs, int32_t cap, int32_t* n_recs,
+                  int32_t* termination, void* stream);
+
+/* Reference-equivalent integer structures, bit-exact with the reference:
+ *  - obs_pt_order [N] int32: stable point-major permutation of observations
+ *  - obs_cam_order [N] int32: stable camera-major permutation
+ *  - off_keys: JtJPattern.off_keys (sparse_block.py:263-266), int32 [K,2]
+ *    sorted (a<b), written when off_keys != NULL and cap >= K; *n_off = K.
+ *  - slots: _SchurPlan retained slots (lm.py:338-384), int32 [S,2] sorted by
+ *    retained pair code, written when slots != NULL and cap >= S; *n_slots = S.
+ * All outputs are device pointers (any may be NULL). */
+int ssfm_export_pattern(ssfm_handle* h, int32_t* obs_pt_order,
+                        int32_t* obs_cam_order, int32_t* off_keys,
+                        int64_t off_cap, int64_t* n_off, int32_t* slots,
+                        int64_t slot_cap, int64_t* n_slots, void* stream);
+
+/* Timing hooks for bench.py: per-kernel-class accumulated device time of the
+ * last lm_solve (ms) and launch counts. kind: 0 = PCG operator (S*p), 1 =
+ * linearize, 2 = all. */
+int ssfm_profile_get(const ssfm_handle* h, int32_t kind, double* ms,
+                     int64_t* launches, double* bytes);
+int ssfm_profile_enable(ssfm_handle* h, int32_t on);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SSFM_H */

@@ -1,0 +1,563 @@
+// ba_kernels.cuh -- bundle-adjustment kernels: camera prep, cost, linearize
+// (+ Jt r, J^T J blocks), damped elimination blocks, preconditioner, back
+// substitution and the candidate update.
+//
+// Data layout in HBM (N observations, P points, C cameras):
+//   Jpm[16][N]  compact Jacobian, SoA, point-major   (read by point passes)
+//   Jcm[16][N]  same records, SoA, camera-major       (read by camera passes)
+//   rcm[2][N]   weighted residual, camera-major
+//   per point (AoS): Cpt[6] (Jp^T Jp), gpt[3] (Jp^T r), Cinv[6], y0[3], yv[3]
+//   per camera (AoS): Bc[64] (Jc^T Jc, 8x8 full), gcam[8], Minv[64], bred[8]
+// The compact record is 16 fp64 per observation instead of the reference's
+// 22 (ba.py:63): the pose-center block equals -(point block) (ba.py:187-188).
+#pragma once
+#include "ba.cuh"
+#include "topo.cuh"
+
+struct BADev {
+  BAParams bp;
+  Topo topo;
+  const double* pix_pm;   // [2N] interleaved, point-major
+  const double* pps;      // [2C]
+  const double* dists;    // [2C]
+  const double* focals;   // [C] fixed focals (focal_mode 0)
+  BACam* cams;            // [C]
+  double* Jpm;            // [16 * Npad]
+  double* Jcm;            // [16 * Npad]
+  double* rcm;            // [2 * Npad]
+  long long Npad;
+  double* Cpt;            // [6P]
+  double* gpt;            // [3P]
+  double* Bc;             // [64C]
+  double* gcam;           // [8C]
+  double* tilebuf;        // [44 * nt]
+  double* Cinv;           // [6P]
+  double* y0;             // [3P]
+  double* yv;             // [3P]
+  double* Minv;           // [64C]
+  double* bred;           // [8C]
+  unsigned char* pinned;  // [C] bitmask of pinned retained slots
+  double* scal;           // scalars: [0] gmax bits, [1] gnorm2, [2] cost, ...
+  double* partials;       // [max(nb, blocks)] reduction scratch
+  int* status;
+};
+
+enum { SC_GMAX = 0, SC_GNORM2 = 1, SC_COST = 2, SC_LAMBDA = 3 };
+
+// ---------------------------------------------------------------------------
+// camera cache from theta (quat_to_matrix_many per camera, ba.py:111-116)
+// ---------------------------------------------------------------------------
+__global__ void ba_k_prep(BADev d, const double* __restrict__ theta) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= d.bp.C) return;
+  const double* pose = theta + 7ll * c;
+  double f;
+  if (d.bp.focal_mode == 1) f = theta[d.bp.off_foc + c];
+  else if (d.bp.focal_mode == 2) f = theta[d.bp.off_foc];
+  else f = d.focals[c];
+  BACam cc;
+  ba_make_cam(pose, pose + 4, f, d.pps + 2 * c, d.dists + 2 * c, cc);
+  d.cams[c] = cc;
+}
+
+// ---------------------------------------------------------------------------
+// cost (ba.py:133-138): one thread per observation (point-major), fixed-tree
+// block sums, then a single-block sum of the block partials in block order.
+// ---------------------------------------------------------------------------
+__global__ void ba_k_cost(BADev d, const double* __restrict__ theta, double* partials) {
+  __shared__ double sm[32];
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  double v[1] = {0.0};
+  if (i < d.topo.N) {
+    const int c = d.topo.pm_cam[i], j = d.topo.pm_pt[i];
+    const BACam cc = d.cams[c];
+    const double* X = theta + d.bp.off_pts + 3ll * j;
+    BAProj pr;
+    double r[2], sw, ct;
+    ba_residual(d.bp, cc, X, d.pix_pm + 2 * i, pr, r, sw, ct);
+    v[0] = ct;
+  }
+  block_reduce<1>(v, sm);
+  if (threadIdx.x == 0) partials[blockIdx.x] = v[0];
+}
+
+// Sum n partials in fixed order with one block (deterministic).
+__global__ void k_sum_partials(const double* __restrict__ partials, int n, double* out) {
+  __shared__ double sm[32];
+  double v[1] = {0.0};
+  // contiguous chunk per thread, chunks in thread order
+  int per = (n + blockDim.x - 1) / blockDim.x;
+  int a = threadIdx.x * per, b = min(n, a + per);
+  for (int k = a; k < b; ++k) v[0] += partials[k];
+  block_reduce<1>(v, sm);
+  if (threadIdx.x == 0) *out = v[0];
+}
+
+__device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
+  // order-preserving for non-negative doubles (and NaN sorts above +inf)
+  atomicMax(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)__double_as_longlong(v));
+}
+
+// ---------------------------------------------------------------------------
+// linearize (ba.py:140-194) fused with the point side of jtj/jtr
+// (_core.pyx:18-97 for point keys): one warp per point batch.
+// Writes Jpm (coalesced), Jcm/rcm (camera-major scatter), Cpt, gpt, and the
+// optional reference-layout exports (r_out [2N], J_out [22N] in observation order).
+// ---------------------------------------------------------------------------
+#define LIN_V 9
+__global__ void __launch_bounds__(256) ba_k_linearize(BADev d, const double* __restrict__ theta,
+                                                      double* r_out, double* J_out, double* gpt_norm_part) {
+  __shared__ double sm[8][SSFM_BATCH][LIN_V];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long Np = d.Npad;
+  double gn2 = 0.0;   // sum of squares of owned point gradients (lane-local)
+  double gmax = 0.0;
+  for (int b = gw; b < d.topo.nb; b += warps) {
+    const int ob0 = d.topo.bat_obs[b], ob1 = d.topo.bat_obs[b + 1];
+    const int pb0 = d.topo.bat_pt[b], pb1 = d.topo.bat_pt[b + 1];
+    const int my_pt = pb0 + lane;
+    int ps = 0, pe = 0;
+    if (my_pt < pb1) { ps = d.topo.pt_seg[my_pt]; pe = d.topo.pt_seg[my_pt + 1]; }
+    double acc[LIN_V];
+#pragma unroll
+    for (int k = 0; k < LIN_V; ++k) acc[k] = 0.0;
+    for (int base = ob0; base < ob1; base += SSFM_BATCH) {
+      const int i = base + lane;
+      double val[LIN_V];
+#pragma unroll
+      for (int k = 0; k < LIN_V; ++k) val[k] = 0.0;
+      if (i < ob1) {
+        const int c = d.topo.pm_cam[i], j = d.topo.pm_pt[i];
+        const BACam cc = d.cams[c];
+        const double* X = theta + d.bp.off_pts + 3ll * j;
+        BAProj pr;
+        double r[2], sw, ct;
+        ba_residual(d.bp, cc, X, d.pix_pm + 2ll * i, pr, r, sw, ct);
+        double J[BA_JREC];
+        ba_jacobian(d.bp, cc, pr, sw, J);
+        const int ic = d.topo.pm_to_cm[i];
+#pragma unroll
+        for (int k = 0; k < BA_JREC; ++k) {
+          d.Jpm[k * Np + i] = J[k];
+          d.Jcm[k * Np + ic] = J[k];
+        }
+        d.rcm[ic] = r[0];
+        d.rcm[Np + ic] = r[1];
+        // point-side products: Jp^T Jp (upper 6) and Jp^T r
+        const double* jp = J + 8;
+        val[0] = jp[0] * jp[0] + jp[3] * jp[3];
+        val[1] = jp[0] * jp[1] + jp[3] * jp[4];
+        val[2] = jp[0] * jp[2] + jp[3] * jp[5];
+        val[3] = jp[1] * jp[1] + jp[4] * jp[4];
+        val[4] = jp[1] * jp[2] + jp[4] * jp[5];
+        val[5] = jp[2] * jp[2] + jp[5] * jp[5];
+        val[6] = jp[0] * r[0] + jp[3] * r[1];
+        val[7] = jp[1] * r[0] + jp[4] * r[1];
+        val[8] = jp[2] * r[0] + jp[5] * r[1];
+        if (r_out) {
+          const int o = d.topo.pm_obs[i];
+          r_out[2ll * o] = r[0];
+          r_out[2ll * o + 1] = r[1];
+        }
+        if (J_out) {
+          // reference layout per observation: pose 2x7 | point 2x3 | focal 2x1
+          const int o = d.topo.pm_obs[i];
+          const int w = d.bp.focal_mode ? 22 : 20;
+          double* dst = J_out + (long long)w * o;
+#pragma unroll
+          for (int rr = 0; rr < 2; ++rr) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) dst[7 * rr + k] = J[4 * rr + k];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) dst[7 * rr + 4 + k] = -J[8 + 3 * rr + k];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) dst[14 + 3 * rr + k] = J[8 + 3 * rr + k];
+            if (d.bp.focal_mode) dst[20 + rr] = J[14 + rr];
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < LIN_V; ++k) sm[wib][lane][k] = val[k];
+      __syncwarp();
+      // owner lane sums its point's observations of this round in order
+      const int a = max(ps, base), e = min(pe, base + SSFM_BATCH);
+      for (int o = a; o < e; ++o) {
+#pragma unroll
+        for (int k = 0; k < LIN_V; ++k) acc[k] += sm[wib][o - base][k];
+      }
+      __syncwarp();
+    }
+    if (my_pt < pb1) {
+      double* C6 = d.Cpt + 6ll * my_pt;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) C6[k] = acc[k];
+      double* g3 = d.gpt + 3ll * my_pt;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        g3[k] = acc[6 + k];
+        gn2 += acc[6 + k] * acc[6 + k];
+        gmax = fmax(gmax, fabs(acc[6 + k]));
+      }
+    }
+  }
+  // per-warp partial of |g|^2 (fixed lane order) and global max
+  gn2 = warp_sum(gn2);
+  gmax = warp_max(gmax);
+  if (lane == 0) {
+    gpt_norm_part[gw] = gn2;
+    atomic_max_nonneg(d.scal + SC_GMAX, gmax);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// camera side of jtj/jtr: per camera tile, sum Jc^T Jc (36 upper) and Jc^T r (8)
+// ---------------------------------------------------------------------------
+#define CAM_V 44
+__global__ void __launch_bounds__(SSFM_TILE) ba_k_camred(BADev d) {
+  __shared__ double sm[(SSFM_TILE / 32) * CAM_V];
+  const int t = blockIdx.x;
+  const int o0 = d.topo.tile_obs[t], o1 = d.topo.tile_obs[t + 1];
+  const int i = o0 + threadIdx.x;
+  double v[CAM_V];
+#pragma unroll
+  for (int k = 0; k < CAM_V; ++k) v[k] = 0.0;
+  if (i < o1) {
+    const long long Np = d.Npad;
+    double J[BA_JREC];
+#pragma unroll
+    for (int k = 0; k < BA_JREC; ++k) J[k] = d.Jcm[k * Np + i];
+    double a[8], b[8];
+    ba_jc_row(J, 0, a);
+    ba_jc_row(J, 1, b);
+    const double r0 = d.rcm[i], r1 = d.rcm[Np + i];
+    int idx = 0;
+#pragma unroll
+    for (int p = 0; p < 8; ++p)
+#pragma unroll
+      for (int q = p; q < 8; ++q) v[idx++] = a[p] * a[q] + b[p] * b[q];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) v[36 + p] = a[p] * r0 + b[p] * r1;
+  }
+  block_reduce<CAM_V>(v, sm);
+  if (threadIdx.x == 0) {
+    double* dst = d.tilebuf + (long long)CAM_V * t;
+#pragma unroll
+    for (int k = 0; k < CAM_V; ++k) dst[k] = v[k];
+  }
+}
+
+// per camera: sum tile partials in tile order -> Bc (full 8x8), gcam
+__global__ void ba_k_camfin(BADev d, double* cam_norm_part) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  double gn2 = 0.0, gmax = 0.0;
+  if (c < d.bp.C) {
+    double s[CAM_V];
+#pragma unroll
+    for (int k = 0; k < CAM_V; ++k) s[k] = 0.0;
+    for (int t = d.topo.cam_tile[c]; t < d.topo.cam_tile[c + 1]; ++t) {
+      const double* src = d.tilebuf + (long long)CAM_V * t;
+#pragma unroll
+      for (int k = 0; k < CAM_V; ++k) s[k] += src[k];
+    }
+    double* B = d.Bc + 64ll * c;
+    int idx = 0;
+#pragma unroll
+    for (int p = 0; p < 8; ++p)
+#pragma unroll
+      for (int q = p; q < 8; ++q) { B[8 * p + q] = s[idx]; B[8 * q + p] = s[idx]; ++idx; }
+    double* g = d.gcam + 8ll * c;
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      g[p] = s[36 + p];
+      gn2 += s[36 + p] * s[36 + p];
+      gmax = fmax(gmax, fabs(s[36 + p]));
+    }
+  }
+  double v[1] = {gn2};
+  __shared__ double sm[32];
+  const double gm = warp_max(gmax);
+  if ((threadIdx.x & 31) == 0) atomic_max_nonneg(d.scal + SC_GMAX, gm);
+  block_reduce<1>(v, sm);
+  if (threadIdx.x == 0) cam_norm_part[blockIdx.x] = v[0];
+}
+
+// ---------------------------------------------------------------------------
+// damped point blocks (apply_damping + _invert_elim_blocks, lm.py:495-513,
+// sparse_block.py:406-426): Cinv = (C diag*(1+lam))^-1, y0 = Cinv b_j, b = -g.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool inv_sym3(const double* m, double* inv, double& det) {
+  const double c00 = m[3] * m[5] - m[4] * m[4];
+  const double c01 = m[2] * m[4] - m[1] * m[5];
+  const double c02 = m[1] * m[4] - m[2] * m[3];
+  det = m[0] * c00 + m[1] * c01 + m[2] * c02;
+  if (!(det > 0.0) || !isfinite(det)) return false;
+  const double id = 1.0 / det;
+  inv[0] = c00 * id;
+  inv[1] = c01 * id;
+  inv[2] = c02 * id;
+  inv[3] = (m[0] * m[5] - m[2] * m[2]) * id;
+  inv[4] = (m[1] * m[2] - m[0] * m[4]) * id;
+  inv[5] = (m[0] * m[3] - m[1] * m[1]) * id;
+  return true;
+}
+
+__global__ void ba_k_ptinv(BADev d, double lam) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= d.bp.P) return;
+  double m[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) m[k] = d.Cpt[6ll * j + k];
+  const double s = 1.0 + lam;
+  m[0] *= s; m[3] *= s; m[5] *= s;
+  double b[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) b[k] = -d.gpt[3ll * j + k];
+  const int di[3] = {0, 3, 5};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (m[di[k]] == 0.0) {
+      if (b[k] != 0.0) atomicOr(d.status, ST_PIN_POINT);
+      m[di[k]] = 1.0;
+    }
+  }
+  double inv[6], det;
+  if (!inv_sym3(m, inv, det)) {
+    atomicOr(d.status, ST_SINGULAR_POINT);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) inv[k] = 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < 6; ++k) d.Cinv[6ll * j + k] = inv[k];
+  double y[3];
+  sym3_matvec(inv, b, y);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) d.y0[3ll * j + k] = y[k];
+}
+
+// ---------------------------------------------------------------------------
+// Schur preconditioner blocks and reduced rhs, per camera tile:
+//   sum_o E_o Cinv_j E_o^T  (E_o = Jc^T Jp, 8x3)   -> 36 upper
+//   sum_o E_o y0_j                                 -> 8
+// (the diagonal slots of schur_fill_cy and b_red, lm.py:608-626)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(SSFM_TILE) ba_k_precond(BADev d) {
+  __shared__ double sm[(SSFM_TILE / 32) * CAM_V];
+  const int t = blockIdx.x;
+  const int o0 = d.topo.tile_obs[t], o1 = d.topo.tile_obs[t + 1];
+  const int i = o0 + threadIdx.x;
+  double v[CAM_V];
+#pragma unroll
+  for (int k = 0; k < CAM_V; ++k) v[k] = 0.0;
+  if (i < o1) {
+    const long long Np = d.Npad;
+    double J[BA_JREC];
+#pragma unroll
+    for (int k = 0; k < BA_JREC; ++k) J[k] = d.Jcm[k * Np + i];
+    const int j = d.topo.cm_pt[i];
+    double ci[6], y[3];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) ci[k] = d.Cinv[6ll * j + k];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) y[k] = d.y0[3ll * j + k];
+    // K = Jp Cinv Jp^T (2x2)
+    const double* jp = J + 8;
+    double w0[3], w1[3];
+    sym3_matvec(ci, jp, w0);
+    sym3_matvec(ci, jp + 3, w1);
+    const double k00 = jp[0] * w0[0] + jp[1] * w0[1] + jp[2] * w0[2];
+    const double k01 = jp[3] * w0[0] + jp[4] * w0[1] + jp[5] * w0[2];
+    const double k11 = jp[3] * w1[0] + jp[4] * w1[1] + jp[5] * w1[2];
+    double a[8], b[8];
+    ba_jc_row(J, 0, a);
+    ba_jc_row(J, 1, b);
+    double ka[8], kb[8];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) { ka[p] = k00 * a[p] + k01 * b[p]; kb[p] = k01 * a[p] + k11 * b[p]; }
+    int idx = 0;
+#pragma unroll
+    for (int p = 0; p < 8; ++p)
+#pragma unroll
+      for (int q = p; q < 8; ++q) v[idx++] = a[p] * ka[q] + b[p] * kb[q];
+    double ty[2];
+    ba_jp_mul(J, y, ty);
+#pragma unroll
+    for (int p = 0; p < 8; ++p) v[36 + p] = a[p] * ty[0] + b[p] * ty[1];
+  }
+  block_reduce<CAM_V>(v, sm);
+  if (threadIdx.x == 0) {
+    double* dst = d.tilebuf + (long long)CAM_V * t;
+#pragma unroll
+    for (int k = 0; k < CAM_V; ++k) dst[k] = v[k];
+  }
+}
+
+// Gauss-Jordan inverse with partial pivoting (n <= 8), like LAPACK getrf/getri
+// used by np.linalg.inv. Returns false on an exactly zero pivot or non-finite.
+__device__ bool gj_inverse(double* a, double* inv, int n, int lda) {
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) inv[i * lda + j] = (i == j) ? 1.0 : 0.0;
+  for (int col = 0; col < n; ++col) {
+    int piv = col;
+    double best = fabs(a[col * lda + col]);
+    for (int r = col + 1; r < n; ++r) {
+      double v = fabs(a[r * lda + col]);
+      if (v > best) { best = v; piv = r; }
+    }
+    if (!(best > 0.0)) return false;
+    if (piv != col) {
+      for (int k = 0; k < n; ++k) {
+        double t = a[col * lda + k]; a[col * lda + k] = a[piv * lda + k]; a[piv * lda + k] = t;
+        t = inv[col * lda + k]; inv[col * lda + k] = inv[piv * lda + k]; inv[piv * lda + k] = t;
+      }
+    }
+    const double ip = 1.0 / a[col * lda + col];
+    for (int k = 0; k < n; ++k) { a[col * lda + k] *= ip; inv[col * lda + k] *= ip; }
+    for (int r = 0; r < n; ++r) {
+      if (r == col) continue;
+      const double f = a[r * lda + col];
+      if (f == 0.0) continue;
+      for (int k = 0; k < n; ++k) {
+        a[r * lda + k] -= f * a[col * lda + k];
+        inv[r * lda + k] -= f * inv[col * lda + k];
+      }
+    }
+  }
+  for (int i = 0; i < n * lda; ++i)
+    if (!isfinite(inv[i])) return false;
+  return true;
+}
+
+// per camera: S_cc = B_c(damped) - sum E Cinv E^T, b_red = b_c - sum E y0,
+// pinning (lm.py:628-635), block-Jacobi factors for the 7x7 pose block and the
+// 1x1 focal block separately (lm.py:473-483, 516-527).
+__global__ void ba_k_camprec(BADev d, double lam) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= d.bp.C) return;
+  double s[CAM_V];
+#pragma unroll
+  for (int k = 0; k < CAM_V; ++k) s[k] = 0.0;
+  for (int t = d.topo.cam_tile[c]; t < d.topo.cam_tile[c + 1]; ++t) {
+    const double* src = d.tilebuf + (long long)CAM_V * t;
+#pragma unroll
+    for (int k = 0; k < CAM_V; ++k) s[k] += src[k];
+  }
+  const double* B = d.Bc + 64ll * c;
+  double S[64];
+  int idx = 0;
+  for (int p = 0; p < 8; ++p)
+    for (int q = p; q < 8; ++q) {
+      double bpq = B[8 * p + q];
+      if (p == q) bpq *= (1.0 + lam);
+      const double v = bpq - s[idx++];
+      S[8 * p + q] = v;
+      S[8 * q + p] = v;
+    }
+  double br[8];
+  for (int p = 0; p < 8; ++p) br[p] = -d.gcam[8ll * c + p] - s[36 + p];
+  unsigned pin = 0;
+  for (int p = 0; p < 8; ++p) {
+    if (S[9 * p] == 0.0) {
+      // a zero diagonal of a PSD matrix implies a zero row: pin it (lm.py:628-635)
+      if (br[p] != 0.0) atomicOr(d.status, ST_PIN_RETAINED);
+      pin |= 1u << p;
+      S[9 * p] = 1.0;
+    }
+  }
+  d.pinned[c] = (unsigned char)pin;
+  for (int p = 0; p < 8; ++p) d.bred[8ll * c + p] = (pin >> p & 1u) ? 0.0 : br[p];
+  double A[49], I7[49];
+  for (int p = 0; p < 7; ++p)
+    for (int q = 0; q < 7; ++q) A[7 * p + q] = S[8 * p + q];
+  double* M = d.Minv + 64ll * c;
+  const bool ok = gj_inverse(A, I7, 7, 7);
+  if (!ok) atomicOr(d.status, ST_SINGULAR_PRECOND);
+  for (int p = 0; p < 8; ++p)
+    for (int q = 0; q < 8; ++q) M[8 * p + q] = (p < 7 && q < 7 && ok) ? I7[7 * p + q] : 0.0;
+  const double s77 = S[63];
+  const double f = 1.0 / s77;
+  if (!isfinite(f)) atomicOr(d.status, ST_SINGULAR_PRECOND);
+  M[63] = f;
+}
+
+// ---------------------------------------------------------------------------
+// back-substitution (lm.py:674-690): delta_j = y0_j - Cinv_j sum_o Jp^T Jc x_c
+// one warp per point batch; camera part of delta scattered by ba_k_camdelta.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) ba_k_backsub(BADev d, const double* __restrict__ x,
+                                                    double* delta) {
+  __shared__ double sm[8][SSFM_BATCH][3];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long Np = d.Npad;
+  for (int b = gw; b < d.topo.nb; b += warps) {
+    const int ob0 = d.topo.bat_obs[b], ob1 = d.topo.bat_obs[b + 1];
+    const int pb0 = d.topo.bat_pt[b], pb1 = d.topo.bat_pt[b + 1];
+    const int my_pt = pb0 + lane;
+    int ps = 0, pe = 0;
+    if (my_pt < pb1) { ps = d.topo.pt_seg[my_pt]; pe = d.topo.pt_seg[my_pt + 1]; }
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int base = ob0; base < ob1; base += SSFM_BATCH) {
+      const int i = base + lane;
+      double val[3] = {0.0, 0.0, 0.0};
+      if (i < ob1) {
+        double J[BA_JREC];
+#pragma unroll
+        for (int k = 0; k < BA_JREC; ++k) J[k] = d.Jpm[k * Np + i];
+        const int c = d.topo.pm_cam[i];
+        double pc[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) pc[k] = x[8ll * c + k];
+        double t[2];
+        ba_jc_mul(J, pc, t);
+        ba_jpt_mul(J, t, val);
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) sm[wib][lane][k] = val[k];
+      __syncwarp();
+      const int a = max(ps, base), e = min(pe, base + SSFM_BATCH);
+      for (int o = a; o < e; ++o) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) acc[k] += sm[wib][o - base][k];
+      }
+      __syncwarp();
+    }
+    if (my_pt < pb1) {
+      double ci[6], w[3];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) ci[k] = d.Cinv[6ll * my_pt + k];
+      sym3_matvec(ci, acc, w);
+      double* dst = delta + d.bp.off_pts + 3ll * my_pt;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) dst[k] = d.y0[3ll * my_pt + k] - w[k];
+    }
+  }
+}
+
+__global__ void ba_k_camdelta(BADev d, const double* __restrict__ x, double* delta) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= d.bp.C) return;
+#pragma unroll
+  for (int k = 0; k < 7; ++k) delta[7ll * c + k] = x[8ll * c + k];
+  if (d.bp.focal_mode == 1) delta[d.bp.off_foc + c] = x[8ll * c + 7];
+}
+
+// candidate = theta + delta (lm.py:770)
+__global__ void k_axpy_theta(const double* __restrict__ theta, const double* __restrict__ delta,
+                             double* out, long long n) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = theta[i] + delta[i];
+}
+
+// renormalize (lm.py:104-117): unit quaternion per camera_pose block
+__global__ void ba_k_renorm(int C, double* theta, int* status) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double* q = theta + 7ll * c;
+  const double n = __dsqrt_rn(ADD(ADD(ADD(MUL(q[0], q[0]), MUL(q[1], q[1])), MUL(q[2], q[2])), MUL(q[3], q[3])));
+  if (n < 1e-12) { atomicOr(status, ST_ZERO_QUAT); return; }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) q[k] = DIV(q[k], n);
+}

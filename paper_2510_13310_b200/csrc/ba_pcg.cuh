@@ -1,0 +1,261 @@
+// ba_pcg.cuh -- the whole block-Jacobi PCG on the reduced camera system as
+// ONE persistent cooperative kernel (lm.py:637-672), with the Schur operator
+// applied matrix-free (replaces schur_fill_cy + the dense S@p at lm.py:656):
+//
+//   y_j      = Cinv_j  sum_{o in j} Jp_o^T (Jc_o p_c)          point pass  (P1)
+//   t_tile   = sum_{o in tile} Jc_o^T (Jp_o y_j)               camera pass (P2)
+//   (S p)_c  = B_c p_c + lam diag(B_c) p_c - sum_tiles t_tile  per camera  (P3)
+//
+// The reduced vector keeps 8 slots per camera (7 pose + 1 focal). Pinned
+// slots (zero Schur diagonal) behave as identity rows, as in lm.py:628-635.
+// All CTAs evaluate the scalar recurrences redundantly from the same partials
+// in the same order, so control decisions are identical everywhere without
+// extra broadcasts. No floating-point atomics.
+#pragma once
+#include <cooperative_groups.h>
+#include "ba_kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+struct CGCtl {
+  double tol;
+  double rho;
+  double rn;
+  double pq;
+  int iters;
+  int flag;     // 0 running/converged, ST_CG_* on failure
+  int pad[2];
+};
+
+#define PCG_THREADS 256
+
+// Sum of per-CTA partials (n of them, stride ns) component k, evaluated by warp 0
+// in a fixed order and broadcast through shared memory.
+__device__ __forceinline__ double cta_partials_sum(const double* part, int n, int ns, int k,
+                                                   double* smslot) {
+  if (threadIdx.x < 32) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += 32) s += part[(long long)i * ns + k];
+    s = warp_sum(s);
+    if (threadIdx.x == 0) *smslot = s;
+  }
+  __syncthreads();
+  const double v = *smslot;
+  __syncthreads();
+  return v;
+}
+
+// P1 for a camera vector v -> y (per point): y_j = Cinv_j sum_o Jp^T (Jc v_c)
+__device__ __forceinline__ void ba_point_pass(const BADev& d, const double* v, double* y,
+                                              double (*sm)[SSFM_BATCH][3]) {
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long Np = d.Npad;
+  for (int b = gw; b < d.topo.nb; b += warps) {
+    const int ob0 = d.topo.bat_obs[b], ob1 = d.topo.bat_obs[b + 1];
+    const int pb0 = d.topo.bat_pt[b], pb1 = d.topo.bat_pt[b + 1];
+    const int my_pt = pb0 + lane;
+    int ps = 0, pe = 0;
+    if (my_pt < pb1) { ps = d.topo.pt_seg[my_pt]; pe = d.topo.pt_seg[my_pt + 1]; }
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int base = ob0; base < ob1; base += SSFM_BATCH) {
+      const int i = base + lane;
+      double val[3] = {0.0, 0.0, 0.0};
+      if (i < ob1) {
+        double J[BA_JREC];
+#pragma unroll
+        for (int k = 0; k < BA_JREC; ++k) J[k] = __ldg(d.Jpm + k * Np + i);
+        const int c = __ldg(d.topo.pm_cam + i);
+        double pc[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) pc[k] = v[8ll * c + k];
+        double t[2];
+        ba_jc_mul(J, pc, t);
+        ba_jpt_mul(J, t, val);
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) sm[wib][lane][k] = val[k];
+      __syncwarp();
+      const int a = max(ps, base), e = min(pe, base + SSFM_BATCH);
+      for (int o = a; o < e; ++o) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) acc[k] += sm[wib][o - base][k];
+      }
+      __syncwarp();
+    }
+    if (my_pt < pb1) {
+      double ci[6], w[3];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) ci[k] = __ldg(d.Cinv + 6ll * my_pt + k);
+      sym3_matvec(ci, acc, w);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) y[3ll * my_pt + k] = w[k];
+    }
+  }
+}
+
+// P2: per camera tile, sum Jc^T (Jp y_j) -> tile8[t][8]
+__device__ __forceinline__ void ba_camera_pass(const BADev& d, const double* y, double* tile8,
+                                               double* smred) {
+  const long long Np = d.Npad;
+  for (int t = blockIdx.x; t < d.topo.nt; t += gridDim.x) {
+    const int o0 = __ldg(d.topo.tile_obs + t), o1 = __ldg(d.topo.tile_obs + t + 1);
+    const int i = o0 + threadIdx.x;
+    double o[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = 0.0;
+    if (i < o1) {
+      double J[BA_JREC];
+#pragma unroll
+      for (int k = 0; k < BA_JREC; ++k) J[k] = __ldg(d.Jcm + k * Np + i);
+      const int j = __ldg(d.topo.cm_pt + i);
+      double yj[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) yj[k] = y[3ll * j + k];
+      double tt[2];
+      ba_jp_mul(J, yj, tt);
+      ba_jct_mul(J, tt, o);
+    }
+    block_reduce<8>(o, smred);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) tile8[8ll * t + k] = o[k];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(PCG_THREADS) ba_k_pcg(BADev d, double lam, int max_iters,
+                                                        double cg_tol, double* x, double* r,
+                                                        double* z, double* p, double* q,
+                                                        double* part, CGCtl* ctl) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double smp[PCG_THREADS / 32][SSFM_BATCH][3];
+  __shared__ double smred[(PCG_THREADS / 32) * 8];
+  __shared__ double smb[4];
+  const int S = 8 * d.bp.C;
+  const int stride = gridDim.x * blockDim.x;
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  double* tile8 = d.tilebuf;
+  const int NP = gridDim.x;
+
+  // ---- init: x = 0, r = b_red, z = M r, p = z
+  {
+    double v[2] = {0.0, 0.0};
+    for (int base = 0; base < S; base += stride) {
+      const int s = base + gid;
+      const bool ok = s < S;
+      if (base + (gid & ~31) >= S) continue;   // whole warp out of range
+      const int c = ok ? s >> 3 : 0, k = s & 7;
+      const double rk = ok ? d.bred[s] : 0.0;
+      double zk = 0.0;
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const double rm = grp8_get(rk, m);
+        if (ok) zk += d.Minv[64ll * c + 8 * k + m] * rm;
+      }
+      if (ok) { x[s] = 0.0; r[s] = rk; z[s] = zk; p[s] = zk; }
+      v[0] += rk * rk;
+      v[1] += rk * zk;
+    }
+    block_reduce<2>(v, smred);
+    if (threadIdx.x == 0) { part[2ll * blockIdx.x] = v[0]; part[2ll * blockIdx.x + 1] = v[1]; }
+  }
+  grid.sync();
+  const double gn = sqrt(d.scal[SC_GNORM2]);
+  const double tol = cg_tol * fmax(gn, 1e-300);
+  double rr = cta_partials_sum(part, NP, 2, 0, &smb[0]);
+  double rho = cta_partials_sum(part, NP, 2, 1, &smb[1]);
+  double rn = sqrt(rr);
+  int iters = 0;
+  int flag = 0;
+  if (rn > tol) {
+    while (true) {
+      if (iters >= max_iters) { flag = ST_CG_MAXITER; break; }
+      // P1: point pass
+      ba_point_pass(d, p, d.yv, smp);
+      grid.sync();
+      // P2: camera tiles
+      ba_camera_pass(d, d.yv, tile8, smred);
+      grid.sync();
+      // P3: q = S p per slot, p.q partials
+      {
+        double v[1] = {0.0};
+        for (int base = 0; base < S; base += stride) {
+          const int s = base + gid;
+          if (base + (gid & ~31) >= S) continue;
+          const bool ok = s < S;
+          const int c = ok ? s >> 3 : 0, k = s & 7;
+          const double pk = ok ? p[s] : 0.0;
+          double bp = 0.0;
+#pragma unroll
+          for (int m = 0; m < 8; ++m) {
+            const double pm = grp8_get(pk, m);
+            if (ok) bp += d.Bc[64ll * c + 8 * k + m] * pm;
+          }
+          if (ok) {
+            double acc = 0.0;
+            const int t0 = d.topo.cam_tile[c], t1 = d.topo.cam_tile[c + 1];
+            for (int t = t0; t < t1; ++t) acc += tile8[8ll * t + k];
+            double qk = bp + lam * d.Bc[64ll * c + 9 * k] * pk - acc;
+            if ((d.pinned[c] >> k) & 1) qk = pk;
+            q[s] = qk;
+            v[0] += pk * qk;
+          }
+        }
+        block_reduce<1>(v, smred);
+        if (threadIdx.x == 0) part[2ll * blockIdx.x] = v[0];
+      }
+      grid.sync();
+      const double pq = cta_partials_sum(part, NP, 2, 0, &smb[0]);
+      if (!isfinite(pq) || pq <= 0.0) { flag = ST_CG_BREAKDOWN; break; }
+      const double alpha = rho / pq;
+      // P4: x += a p, r -= a q, z = M r; partials r.r, r.z
+      {
+        double v[2] = {0.0, 0.0};
+        for (int base = 0; base < S; base += stride) {
+          const int s = base + gid;
+          if (base + (gid & ~31) >= S) continue;
+          const bool ok = s < S;
+          const int c = ok ? s >> 3 : 0, k = s & 7;
+          double rk = 0.0;
+          if (ok) {
+            x[s] += alpha * p[s];
+            rk = r[s] - alpha * q[s];
+            r[s] = rk;
+          }
+          double zk = 0.0;
+#pragma unroll
+          for (int m = 0; m < 8; ++m) {
+            const double rm = grp8_get(rk, m);
+            if (ok) zk += d.Minv[64ll * c + 8 * k + m] * rm;
+          }
+          if (ok) z[s] = zk;
+          v[0] += rk * rk;
+          v[1] += rk * zk;
+        }
+        block_reduce<2>(v, smred);
+        if (threadIdx.x == 0) { part[2ll * blockIdx.x] = v[0]; part[2ll * blockIdx.x + 1] = v[1]; }
+      }
+      grid.sync();
+      rr = cta_partials_sum(part, NP, 2, 0, &smb[0]);
+      const double rz = cta_partials_sum(part, NP, 2, 1, &smb[1]);
+      ++iters;
+      rn = sqrt(rr);
+      if (rn <= tol) break;
+      const double beta = rz / rho;
+      rho = rz;
+      // P5: p = z + beta p
+      for (int s = gid; s < S; s += stride) p[s] = z[s] + beta * p[s];
+      grid.sync();
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ctl->tol = tol;
+    ctl->rho = rho;
+    ctl->rn = rn;
+    ctl->iters = iters;
+    ctl->flag = flag;
+    if (flag) atomicOr(d.status, flag);
+  }
+}

@@ -1,0 +1,98 @@
+// common.cuh -- shared device utilities for the sparse LM core.
+//
+// Determinism contract (mirrors _kernels/_core.pyx:1-8 and SPEC's "fixed
+// summation order"): every output block is reduced by exactly one owner in a
+// fixed order. Point segments are summed sequentially in observation order by
+// one lane; camera segments are split into fixed tiles, each tile reduced by a
+// fixed butterfly tree, and the tile partials are summed in tile order. No
+// floating-point atomics anywhere, so results are bit-stable run to run.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define SSFM_WARP 32
+#define SSFM_FULL 0xffffffffu
+
+// Device status bits (accumulated with atomicOr on an int in device memory).
+enum : int {
+  ST_SINGULAR_POINT = 1 << 0,     // lm.py:508-512 det<=0 / non-finite
+  ST_PIN_POINT = 1 << 1,          // lm.py:503-505 masked point dir with gradient
+  ST_SINGULAR_PRECOND = 1 << 2,   // lm.py:520-525
+  ST_PIN_RETAINED = 1 << 3,       // lm.py:631-633
+  ST_CG_MAXITER = 1 << 4,         // lm.py:652-655
+  ST_CG_BREAKDOWN = 1 << 5,       // lm.py:657-659
+  ST_ZERO_QUAT = 1 << 6,          // lm.py:114-115
+  ST_PIN_SCALE = 1 << 7,          // lm.py:569-575
+  ST_BAD_INDEX = 1 << 8,
+};
+
+__device__ __forceinline__ double shfl_xor_d(double v, int m) {
+  return __shfl_xor_sync(SSFM_FULL, v, m);
+}
+
+// Butterfly all-reduce of V doubles inside a warp (fixed tree -> deterministic,
+// every lane ends with the same bits).
+template <int V>
+__device__ __forceinline__ void warp_allreduce(double (&v)[V]) {
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) {
+#pragma unroll
+    for (int k = 0; k < V; ++k) v[k] += shfl_xor_d(v[k], m);
+  }
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) v += shfl_xor_d(v, m);
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) v = fmax(v, shfl_xor_d(v, m));
+  return v;
+}
+
+// Block reduction of V doubles: warp butterflies, then warp 0 sums the warp
+// results in warp order. `sm` needs (blockDim/32)*V doubles. Result valid in
+// thread 0 only (returned in v for tid 0). Must be called by all threads.
+template <int V>
+__device__ __forceinline__ void block_reduce(double (&v)[V], double* sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  warp_allreduce<V>(v);
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < V; ++k) sm[warp * V + k] = v[k];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      double s = sm[k];
+      for (int w = 1; w < nw; ++w) s += sm[w * V + k];
+      v[k] = s;
+    }
+  }
+  __syncthreads();
+}
+
+// Symmetric 3x3 stored as upper triangle {00,01,02,11,12,22}.
+__device__ __forceinline__ void sym3_matvec(const double* m, const double* x, double* y) {
+  y[0] = m[0] * x[0] + m[1] * x[1] + m[2] * x[2];
+  y[1] = m[1] * x[0] + m[3] * x[1] + m[4] * x[2];
+  y[2] = m[2] * x[0] + m[4] * x[1] + m[5] * x[2];
+}
+
+// Upper-triangle index of (i<=j) in an n x n symmetric matrix stored row-wise.
+__host__ __device__ constexpr int sym_idx(int n, int i, int j) {
+  return i * n - (i * (i - 1)) / 2 + (j - i);
+}
+
+// Warp-level 8-lane group helpers (4 cameras per warp, one lane per retained
+// slot): broadcast slot k of the group.
+__device__ __forceinline__ double grp8_get(double v, int k) {
+  const int base = (threadIdx.x & 31) & ~7;
+  return __shfl_sync(SSFM_FULL, v, base + k);
+}

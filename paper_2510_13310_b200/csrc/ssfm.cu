@@ -1,0 +1,864 @@
+// ssfm.cu -- C-ABI (include/ssfm.h) and host drivers of the B200-native
+// sparse LM core. One translation unit: the kernels live in the .cuh files.
+//
+// Host side of lm_solve (lm.py:727-800) is a plain C++ loop that launches the
+// device pipeline and reads back ONE small status block per LM iteration
+// (status bits, CG iteration count, candidate cost, gradient max); everything
+// else (linearize, J^T r, elimination, PCG, back-substitution, update, cost)
+// stays on the device.
+#include <cuda_runtime.h>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ssfm.h"
+#include "ba_pcg.cuh"
+#include "gp_kernels.cuh"
+#include "pattern.cuh"
+
+static thread_local std::string g_last_error;
+
+static int set_err(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define CU(call)                                                                   \
+  do {                                                                             \
+    cudaError_t _e = (call);                                                       \
+    if (_e != cudaSuccess)                                                         \
+      return set_err(SSFM_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+struct Misc {
+  int status;
+  int pad;
+  double scal[8];
+  CGCtl ctl;
+};
+
+struct Profile {
+  bool on = false;
+  double pcg_ms = 0, lin_ms = 0, all_ms = 0;
+  long long pcg_launches = 0, lin_launches = 0, all_launches = 0;
+  long long cg_iters = 0;
+  long long kernel_launches = 0;   // every kernel launched by the library
+};
+
+struct ssfm_handle {
+  int kind = 0;   // 0 BA, 1 GP
+  int device = 0;
+  int num_sms = 148;
+  std::vector<void*> allocs;
+  size_t bytes = 0;
+  long long total_params = 0, total_res = 0;
+  BADev ba{};
+  GPDev gp{};
+  Topo topo{};
+  // solver state
+  double *theta = nullptr, *cand = nullptr, *delta = nullptr;
+  double *x = nullptr, *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr;
+  double* part = nullptr;       // PCG per-CTA partials
+  double* red = nullptr;        // reduction scratch (cost / gnorm)
+  long long red_n = 0;
+  Misc* misc = nullptr;         // device
+  Misc* hmisc = nullptr;        // pinned host
+  int pcg_grid = 0;
+  int lin_blocks = 0;
+  int cost_blocks = 0;
+  int cam_blocks = 0;
+  bool linearized = false;
+  Profile prof;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
+};
+
+template <typename T>
+static int dalloc(ssfm_handle* h, T** ptr, size_t count) {
+  size_t b = sizeof(T) * (count > 0 ? count : 1);
+  b = (b + 255) & ~size_t(255);
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, b);
+  if (e != cudaSuccess)
+    return set_err(SSFM_CUDA_ERROR, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  h->allocs.push_back(p);
+  h->bytes += b;
+  *ptr = static_cast<T*>(p);
+  return SSFM_OK;
+}
+
+#define DALLOC(ptr, n)                        \
+  do {                                        \
+    int _rc = dalloc(h, &(ptr), (size_t)(n)); \
+    if (_rc) return _rc;                      \
+  } while (0)
+
+static inline int nblk(long long n, int t) { return (int)((n + t - 1) / t); }
+
+static void free_handle(ssfm_handle* h) {
+  if (!h) return;
+  for (void* p : h->allocs) cudaFree(p);
+  if (h->hmisc) cudaFreeHost(h->hmisc);
+  if (h->ev0) cudaEventDestroy(h->ev0);
+  if (h->ev1) cudaEventDestroy(h->ev1);
+  if (h->ev2) cudaEventDestroy(h->ev2);
+  if (h->ev3) cudaEventDestroy(h->ev3);
+  delete h;
+}
+
+// ---------------------------------------------------------------------------
+// topology build (shared by BA and GP)
+// ---------------------------------------------------------------------------
+static int build_topo(ssfm_handle* h, const int* cam, const int* pt, int C, int P, long long N,
+                      cudaStream_t st, int* dstatus) {
+  Topo& T = h->topo;
+  T.C = C; T.P = P; T.N = N;
+  const int TB = 256;
+  CU(cudaMemsetAsync(dstatus, 0, sizeof(int), st));
+  if (N > 0) k_check_index<<<nblk(N, TB), TB, 0, st>>>(cam, pt, N, C, P, dstatus);
+  int hst = 0;
+  CU(cudaMemcpyAsync(&hst, dstatus, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (hst & ST_BAD_INDEX) return set_err(SSFM_INVALID_ARGUMENT, "observation references a camera or point index out of range");
+
+  int *iota, *perm_pm, *perm_cm, *keys_out, *inv_cm, *cnt;
+  DALLOC(iota, N); DALLOC(keys_out, N); DALLOC(inv_cm, N);
+  DALLOC(T.pm_obs, N); DALLOC(T.cm_obs, N);
+  DALLOC(T.pm_pt, N); DALLOC(T.pm_cam, N); DALLOC(T.pm_to_cm, N); DALLOC(T.cm_pt, N);
+  DALLOC(T.pt_seg, (long long)P + 1); DALLOC(T.cam_seg, (long long)C + 1);
+  perm_pm = T.pm_obs; perm_cm = T.cm_obs;
+  if (N > 0) k_iota<<<nblk(N, TB), TB, 0, st>>>(iota, N);
+
+  auto nbits = [](int n) { int b = 1; while ((1ll << b) < n) ++b; return b; };
+  // stable radix sorts (point-major / camera-major)
+  size_t tmp_bytes = 0, tb2 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, pt, keys_out, iota, perm_pm, (int)N, 0, nbits(P), st);
+  cub::DeviceRadixSort::SortPairs(nullptr, tb2, cam, keys_out, iota, perm_cm, (int)N, 0, nbits(C), st);
+  tmp_bytes = std::max(tmp_bytes, tb2);
+  size_t scan_bytes = 0;
+  int maxPC = std::max(P, C) + 1;
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (int*)nullptr, (int*)nullptr, maxPC, st);
+  tmp_bytes = std::max(tmp_bytes, scan_bytes);
+  void* tmp;
+  DALLOC(*(char**)&tmp, tmp_bytes);
+  if (N > 0) {
+    CU(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, pt, keys_out, iota, perm_pm, (int)N, 0, nbits(P), st));
+    CU(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, cam, keys_out, iota, perm_cm, (int)N, 0, nbits(C), st));
+  }
+  // segments
+  DALLOC(cnt, maxPC);
+  CU(cudaMemsetAsync(cnt, 0, sizeof(int) * maxPC, st));
+  if (N > 0) k_count<<<nblk(N, TB), TB, 0, st>>>(pt, N, cnt);
+  CU(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, T.pt_seg, P + 1, st));
+  CU(cudaMemsetAsync(cnt, 0, sizeof(int) * maxPC, st));
+  if (N > 0) k_count<<<nblk(N, TB), TB, 0, st>>>(cam, N, cnt);
+  CU(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, T.cam_seg, C + 1, st));
+  if (N > 0) {
+    k_perm_views<<<nblk(N, TB), TB, 0, st>>>(perm_pm, perm_cm, cam, pt, N, T.pm_pt, T.pm_cam, T.cm_pt, inv_cm);
+    k_pm_to_cm<<<nblk(N, TB), TB, 0, st>>>(perm_pm, inv_cm, N, T.pm_to_cm);
+  }
+  // point batches
+  int nch = nblk(P, SSFM_CHUNK);
+  int *ch_cnt, *ch_off;
+  DALLOC(ch_cnt, nch + 1); DALLOC(ch_off, nch + 1);
+  CU(cudaMemsetAsync(ch_cnt, 0, sizeof(int) * (nch + 1), st));
+  if (nch) k_batches<<<nblk(nch, 128), 128, 0, st>>>(T.pt_seg, P, 0, ch_cnt, ch_off, nullptr, nullptr);
+  CU(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, ch_cnt, ch_off, nch + 1, st));
+  int nb = 0;
+  CU(cudaMemcpyAsync(&nb, ch_off + nch, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  T.nb = nb;
+  DALLOC(T.bat_pt, nb + 1); DALLOC(T.bat_obs, nb + 1);
+  if (nch) k_batches<<<nblk(nch, 128), 128, 0, st>>>(T.pt_seg, P, 1, ch_cnt, ch_off, T.bat_pt, T.bat_obs);
+  k_set_last<<<1, 1, 0, st>>>(T.bat_pt, nb, P);
+  k_set_last<<<1, 1, 0, st>>>(T.bat_obs, nb, (int)N);
+  // camera tiles
+  DALLOC(T.cam_tile, C + 1);
+  CU(cudaMemsetAsync(cnt, 0, sizeof(int) * maxPC, st));
+  if (C) k_tile_count<<<nblk(C, TB), TB, 0, st>>>(T.cam_seg, C, cnt);
+  CU(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, T.cam_tile, C + 1, st));
+  int nt = 0;
+  CU(cudaMemcpyAsync(&nt, T.cam_tile + C, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  T.nt = nt;
+  DALLOC(T.tile_obs, nt + 1); DALLOC(T.tile_cam, nt + 1);
+  if (C) k_tile_write<<<nblk(C, TB), TB, 0, st>>>(T.cam_seg, T.cam_tile, C, T.tile_obs, T.tile_cam);
+  k_set_last<<<1, 1, 0, st>>>(T.tile_obs, nt, (int)N);
+  CU(cudaGetLastError());
+  return SSFM_OK;
+}
+
+// permute an interleaved [N,w] double array into point-major order
+__global__ void k_gather_rows(const double* __restrict__ src, const int* __restrict__ perm, long long n,
+                              int w, double* dst) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) {
+    const long long o = perm[i];
+    for (int k = 0; k < w; ++k) dst[i * w + k] = src[o * w + k];
+  }
+}
+
+static int common_alloc(ssfm_handle* h, int S_slots, int C) {
+  DALLOC(h->theta, h->total_params);
+  DALLOC(h->cand, h->total_params);
+  DALLOC(h->delta, h->total_params);
+  DALLOC(h->x, S_slots); DALLOC(h->r, S_slots); DALLOC(h->z, S_slots);
+  DALLOC(h->p, S_slots); DALLOC(h->q, S_slots);
+  DALLOC(h->misc, 1);
+  CU(cudaMallocHost((void**)&h->hmisc, sizeof(Misc)));
+  CU(cudaEventCreate(&h->ev0)); CU(cudaEventCreate(&h->ev1));
+  CU(cudaEventCreate(&h->ev2)); CU(cudaEventCreate(&h->ev3));
+  (void)C;
+  return SSFM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// BA
+// ---------------------------------------------------------------------------
+extern "C" int ssfm_create_ba(const ssfm_ba_desc* desc, void* stream, ssfm_handle** out) {
+  if (!desc || !out) return set_err(SSFM_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  if (desc->num_obs <= 0) return set_err(SSFM_EMPTY_PROBLEM, "scene has no observations");
+  if (desc->num_obs >= (1ll << 31) - 64) return set_err(SSFM_INVALID_ARGUMENT, "too many observations for int32 indexing");
+  if (desc->num_cameras <= 0 || desc->num_points < 0) return set_err(SSFM_INVALID_ARGUMENT, "bad camera/point counts");
+  if (desc->shared_focal && desc->optimize_focal)
+    return set_err(SSFM_INVALID_ARGUMENT, "shared_focal: not supported by this build");
+  cudaStream_t st = (cudaStream_t)stream;
+  ssfm_handle* h = new ssfm_handle();
+  CU(cudaGetDevice(&h->device));
+  CU(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device));
+  h->kind = 0;
+  const int C = desc->num_cameras, P = desc->num_points;
+  const long long N = desc->num_obs;
+  BADev& d = h->ba;
+  d.bp.C = C; d.bp.P = P; d.bp.N = N;
+  d.bp.model = desc->model;
+  d.bp.focal_mode = desc->optimize_focal ? (desc->shared_focal ? 2 : 1) : 0;
+  d.bp.loss_kind = desc->loss_kind;
+  d.bp.delta = desc->loss_delta;
+  d.bp.off_pts = 7ll * C;
+  d.bp.off_foc = 7ll * C + 3ll * P;
+  h->total_params = 7ll * C + 3ll * P + (d.bp.focal_mode == 1 ? C : d.bp.focal_mode == 2 ? 1 : 0);
+  h->total_res = 2 * N;
+  auto fail = [&](int rc) { free_handle(h); return rc; };
+  int rc;
+  int* dstatus;
+  if ((rc = dalloc(h, &dstatus, 1))) return fail(rc);
+  d.status = dstatus;
+  if ((rc = build_topo(h, desc->cam_idx, desc->pt_idx, C, P, N, st, dstatus))) return fail(rc);
+  d.topo = h->topo;
+  const Topo& T = h->topo;
+  d.Npad = (N + 31) & ~31ll;
+  double *pix_pm, *pps, *dists, *focals;
+  if ((rc = dalloc(h, &pix_pm, 2 * N))) return fail(rc);
+  if ((rc = dalloc(h, &pps, 2 * C))) return fail(rc);
+  if ((rc = dalloc(h, &dists, 2 * C))) return fail(rc);
+  if ((rc = dalloc(h, &focals, C))) return fail(rc);
+  k_gather_rows<<<nblk(N, 256), 256, 0, st>>>(desc->pixels, T.pm_obs, N, 2, pix_pm);
+  if (cudaMemcpyAsync(pps, desc->pps, sizeof(double) * 2 * C, cudaMemcpyDeviceToDevice, st) ||
+      cudaMemcpyAsync(dists, desc->dists, sizeof(double) * 2 * C, cudaMemcpyDeviceToDevice, st))
+    return fail(set_err(SSFM_CUDA_ERROR, "copy camera intrinsics"));
+  if (desc->focals) {
+    if (cudaMemcpyAsync(focals, desc->focals, sizeof(double) * C, cudaMemcpyDeviceToDevice, st))
+      return fail(set_err(SSFM_CUDA_ERROR, "copy focals"));
+  } else if (cudaMemsetAsync(focals, 0, sizeof(double) * C, st)) {
+    return fail(set_err(SSFM_CUDA_ERROR, "memset focals"));
+  }
+  d.pix_pm = pix_pm; d.pps = pps; d.dists = dists; d.focals = focals;
+  if ((rc = dalloc(h, &d.cams, C))) return fail(rc);
+  if ((rc = dalloc(h, &d.Jpm, BA_JREC * d.Npad))) return fail(rc);
+  if ((rc = dalloc(h, &d.Jcm, BA_JREC * d.Npad))) return fail(rc);
+  if ((rc = dalloc(h, &d.rcm, 2 * d.Npad))) return fail(rc);
+  if ((rc = dalloc(h, &d.Cpt, 6ll * P))) return fail(rc);
+  if ((rc = dalloc(h, &d.gpt, 3ll * P))) return fail(rc);
+  if ((rc = dalloc(h, &d.Bc, 64ll * C))) return fail(rc);
+  if ((rc = dalloc(h, &d.gcam, 8ll * C))) return fail(rc);
+  if ((rc = dalloc(h, &d.tilebuf, (long long)CAM_V * T.nt))) return fail(rc);
+  if ((rc = dalloc(h, &d.Cinv, 6ll * P))) return fail(rc);
+  if ((rc = dalloc(h, &d.y0, 3ll * P))) return fail(rc);
+  if ((rc = dalloc(h, &d.yv, 3ll * P))) return fail(rc);
+  if ((rc = dalloc(h, &d.Minv, 64ll * C))) return fail(rc);
+  if ((rc = dalloc(h, &d.bred, 8ll * C))) return fail(rc);
+  if ((rc = dalloc(h, &d.pinned, C))) return fail(rc);
+  if ((rc = common_alloc(h, 8 * C, C))) return fail(rc);
+  d.scal = h->misc->scal;
+  d.status = &h->misc->status;
+  // launch geometry
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ba_k_pcg, PCG_THREADS, 0) || occ < 1)
+    return fail(set_err(SSFM_CUDA_ERROR, "occupancy query for the PCG kernel failed"));
+  h->pcg_grid = occ * h->num_sms;
+  h->lin_blocks = std::max(1, std::min(nblk(T.nb, 8), h->num_sms * 16));
+  h->cost_blocks = nblk(N, 256);
+  h->cam_blocks = nblk(C, 256);
+  h->red_n = std::max<long long>(h->cost_blocks, (long long)h->lin_blocks * 8 + h->cam_blocks);
+  if ((rc = dalloc(h, &h->red, h->red_n))) return fail(rc);
+  if ((rc = dalloc(h, &h->part, 2ll * h->pcg_grid + 2))) return fail(rc);
+  d.partials = h->red;
+  if (cudaMemsetAsync(h->misc, 0, sizeof(Misc), st) || cudaStreamSynchronize(st))
+    return fail(set_err(SSFM_CUDA_ERROR, "init"));
+  if (cudaGetLastError() != cudaSuccess) return fail(set_err(SSFM_CUDA_ERROR, "setup kernel launch failed"));
+  *out = h;
+  return SSFM_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// GP
+// ---------------------------------------------------------------------------
+extern "C" int ssfm_create_gp(const ssfm_gp_desc* desc, void* stream, ssfm_handle** out) {
+  if (!desc || !out) return set_err(SSFM_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  if (desc->num_obs <= 0) return set_err(SSFM_EMPTY_PROBLEM, "problem has no observations");
+  if (desc->num_obs >= (1ll << 31) - 64) return set_err(SSFM_INVALID_ARGUMENT, "too many observations for int32 indexing");
+  if (desc->num_cameras <= 0 || desc->num_points < 0) return set_err(SSFM_INVALID_ARGUMENT, "bad camera/point counts");
+  if (desc->depth_mode && !desc->depths) return set_err(SSFM_MISSING_DEPTH, "depth mode requires a depth per observation");
+  cudaStream_t st = (cudaStream_t)stream;
+  ssfm_handle* h = new ssfm_handle();
+  CU(cudaGetDevice(&h->device));
+  CU(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device));
+  h->kind = 1;
+  const int C = desc->num_cameras, P = desc->num_points;
+  const long long N = desc->num_obs;
+  GPDev& g = h->gp;
+  g.gp.C = C; g.gp.P = P; g.gp.N = N;
+  g.gp.depth_mode = desc->depth_mode;
+  g.gp.gauge_fixed = desc->gauge_fixed;
+  g.gp.loss_kind = desc->loss_kind;
+  g.gp.delta = desc->loss_delta;
+  g.gp.off_pts = 3ll * C;
+  g.gp.off_sc = 3ll * C + 3ll * P;
+  h->total_params = 3ll * C + 3ll * P + (desc->depth_mode ? 0 : N);
+  h->total_res = 3 * N;
+  auto fail = [&](int rc) { free_handle(h); return rc; };
+  int rc;
+  int* dstatus;
+  if ((rc = dalloc(h, &dstatus, 1))) return fail(rc);
+  if ((rc = build_topo(h, desc->cam_idx, desc->pt_idx, C, P, N, st, dstatus))) return fail(rc);
+  g.topo = h->topo;
+  const Topo& T = h->topo;
+  g.Npad = (N + 31) & ~31ll;
+  double *ray_pm, *dep_pm = nullptr;
+  if ((rc = dalloc(h, &ray_pm, 3 * N))) return fail(rc);
+  k_gather_rows<<<nblk(N, 256), 256, 0, st>>>(desc->rays, T.pm_obs, N, 3, ray_pm);
+  if (desc->depth_mode) {
+    if ((rc = dalloc(h, &dep_pm, N))) return fail(rc);
+    k_gather_rows<<<nblk(N, 256), 256, 0, st>>>(desc->depths, T.pm_obs, N, 1, dep_pm);
+  }
+  g.ray_pm = ray_pm; g.dep_pm = dep_pm;
+  if ((rc = dalloc(h, &g.Jpm, GP_JREC * g.Npad))) return fail(rc);
+  if ((rc = dalloc(h, &g.Jcm, GP_JREC * g.Npad))) return fail(rc);
+  if ((rc = dalloc(h, &g.rcm, 3 * g.Npad))) return fail(rc);
+  if ((rc = dalloc(h, &g.bo_pm, N))) return fail(rc);
+  if ((rc = dalloc(h, &g.bo_cm, N))) return fail(rc);
+  if ((rc = dalloc(h, &g.gsc, N))) return fail(rc);
+  if ((rc = dalloc(h, &g.Apt, P))) return fail(rc);
+  if ((rc = dalloc(h, &g.gpt, 3ll * P))) return fail(rc);
+  if ((rc = dalloc(h, &g.Acam, C))) return fail(rc);
+  if ((rc = dalloc(h, &g.gcam, 3ll * C))) return fail(rc);
+  if ((rc = dalloc(h, &g.Minv_pt, 6ll * P))) return fail(rc);
+  if ((rc = dalloc(h, &g.y0, 3ll * P))) return fail(rc);
+  if ((rc = dalloc(h, &g.yv, 3ll * P))) return fail(rc);
+  if ((rc = dalloc(h, &g.Bp, 6ll * C))) return fail(rc);
+  if ((rc = dalloc(h, &g.Minv, 16ll * C))) return fail(rc);
+  if ((rc = dalloc(h, &g.bred, 4ll * C))) return fail(rc);
+  if ((rc = dalloc(h, &g.pinned, C))) return fail(rc);
+  if ((rc = dalloc(h, &g.tilebuf, (long long)GPE_V * T.nt))) return fail(rc);
+  if ((rc = common_alloc(h, 4 * C, C))) return fail(rc);
+  g.scal = h->misc->scal;
+  g.status = &h->misc->status;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gp_k_pcg, PCG_THREADS, 0) || occ < 1)
+    return fail(set_err(SSFM_CUDA_ERROR, "occupancy query for the PCG kernel failed"));
+  h->pcg_grid = occ * h->num_sms;
+  h->lin_blocks = std::max(1, std::min(nblk(T.nb, 8), h->num_sms * 16));
+  h->cost_blocks = nblk(N, 256);
+  h->cam_blocks = nblk(C, 256);
+  h->red_n = std::max<long long>(h->cost_blocks, (long long)h->lin_blocks * 8 + h->cam_blocks + nblk(N, 256));
+  if ((rc = dalloc(h, &h->red, h->red_n))) return fail(rc);
+  if ((rc = dalloc(h, &h->part, 2ll * h->pcg_grid + 2))) return fail(rc);
+  g.partials = h->red;
+  if (cudaMemsetAsync(h->misc, 0, sizeof(Misc), st) || cudaStreamSynchronize(st))
+    return fail(set_err(SSFM_CUDA_ERROR, "init"));
+  if (cudaGetLastError() != cudaSuccess) return fail(set_err(SSFM_CUDA_ERROR, "setup kernel launch failed"));
+  *out = h;
+  return SSFM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// pattern export (JtJPattern.off_keys / _SchurPlan slots)
+// ---------------------------------------------------------------------------
+static int sort_unique(ssfm_handle* h, unsigned long long* codes, long long n, long long* n_out,
+                       unsigned long long** uniq, std::vector<void*>& tmp_allocs, cudaStream_t st) {
+  unsigned long long *sorted = nullptr, *un = nullptr;
+  int* nsel = nullptr;
+  CU(cudaMalloc(&sorted, sizeof(unsigned long long) * std::max(n, 1ll)));
+  CU(cudaMalloc(&un, sizeof(unsigned long long) * std::max(n, 1ll)));
+  CU(cudaMalloc(&nsel, sizeof(int)));
+  tmp_allocs.push_back(sorted); tmp_allocs.push_back(un); tmp_allocs.push_back(nsel);
+  size_t b1 = 0, b2 = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, b1, codes, sorted, (int)n, 0, 64, st);
+  cub::DeviceSelect::Unique(nullptr, b2, sorted, un, nsel, (int)n, st);
+  void* tmp = nullptr;
+  CU(cudaMalloc(&tmp, std::max(b1, b2)));
+  tmp_allocs.push_back(tmp);
+  size_t bb = std::max(b1, b2);
+  CU(cub::DeviceRadixSort::SortKeys(tmp, bb, codes, sorted, (int)n, 0, 64, st));
+  bb = std::max(b1, b2);
+  CU(cub::DeviceSelect::Unique(tmp, bb, sorted, un, nsel, (int)n, st));
+  int hn = 0;
+  CU(cudaMemcpyAsync(&hn, nsel, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  *n_out = hn;
+  *uniq = un;
+  (void)h;
+  return SSFM_OK;
+}
+
+static int export_keys(ssfm_handle* h, int32_t* off_keys, int64_t off_cap, int64_t* n_off,
+                       int32_t* slots, int64_t slot_cap, int64_t* n_slots, cudaStream_t st) {
+  const Topo& T = h->topo;
+  const int kind = h->kind;
+  const int C = T.C, P = T.P;
+  const long long N = T.N;
+  int F = 0, nscale = 0;
+  long long nblocks;
+  // focal code for the pattern kernels: 2 per-camera, 1 shared, 0 none
+  const int Fr = (kind == 0) ? (h->ba.bp.focal_mode == 1 ? 2 : h->ba.bp.focal_mode == 2 ? 1 : 0) : 0;
+  if (kind == 0) {
+    F = h->ba.bp.focal_mode == 1 ? C : h->ba.bp.focal_mode == 2 ? 1 : 0;
+    nblocks = (long long)C + P + F;
+  } else {
+    nscale = h->gp.gp.depth_mode ? 0 : (int)N;
+    nblocks = (long long)C + P + nscale;
+  }
+  std::vector<void*> tmp;
+  int rc = SSFM_OK;
+  if (off_keys || n_off) {
+    const int per = (kind == 0) ? (F ? 3 : 1) : (nscale ? 3 : 1);
+    unsigned long long* codes = nullptr;
+    if (cudaMalloc(&codes, sizeof(unsigned long long) * per * N)) rc = set_err(SSFM_CUDA_ERROR, "alloc");
+    else {
+      tmp.push_back(codes);
+      k_offkey_codes<<<nblk(N, 256), 256, 0, st>>>(T.pm_cam, T.pm_pt, T.pm_obs, N, kind, C, P,
+                                                   Fr, nscale, nblocks, codes);
+      long long K = 0;
+      unsigned long long* un = nullptr;
+      rc = sort_unique(h, codes, per * N, &K, &un, tmp, st);
+      if (!rc) {
+        if (n_off) *n_off = K;
+        if (off_keys && off_cap >= K && K > 0)
+          k_decode_pairs<<<nblk(K, 256), 256, 0, st>>>(un, K, nblocks, off_keys);
+      }
+    }
+  }
+  if (!rc && (slots || n_slots)) {
+    long long *cnt = nullptr, *off = nullptr;
+    if (cudaMalloc(&cnt, sizeof(long long) * (P + 1)) || cudaMalloc(&off, sizeof(long long) * (P + 1)))
+      rc = set_err(SSFM_CUDA_ERROR, "alloc");
+    else {
+      tmp.push_back(cnt); tmp.push_back(off);
+      cudaMemsetAsync(cnt, 0, sizeof(long long) * (P + 1), st);
+      if (P) k_slot_count<<<nblk(P, 256), 256, 0, st>>>(T.pt_seg, P, kind, Fr, cnt);
+      size_t bb = 0;
+      cub::DeviceScan::ExclusiveSum(nullptr, bb, cnt, off, P + 1, st);
+      void* t2 = nullptr;
+      cudaMalloc(&t2, bb);
+      tmp.push_back(t2);
+      cub::DeviceScan::ExclusiveSum(t2, bb, cnt, off, P + 1, st);
+      long long total = 0;
+      cudaMemcpyAsync(&total, off + P, sizeof(long long), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      unsigned long long* codes = nullptr;
+      if (cudaMalloc(&codes, sizeof(unsigned long long) * std::max(total, 1ll))) rc = set_err(SSFM_CUDA_ERROR, "alloc");
+      else {
+        tmp.push_back(codes);
+        if (P) k_slot_codes<<<nblk(P, 256), 256, 0, st>>>(T.pt_seg, T.pm_cam, P, kind, C, Fr, off, codes);
+        long long S = 0;
+        unsigned long long* un = nullptr;
+        rc = sort_unique(h, codes, total, &S, &un, tmp, st);
+        if (!rc) {
+          if (n_slots) *n_slots = S;
+          const long long nret = (long long)C + (kind == 0 ? (Fr == 1 ? 1 : (Fr ? C : 0)) : 0);
+          if (slots && slot_cap >= S && S > 0)
+            k_decode_pairs<<<nblk(S, 256), 256, 0, st>>>(un, S, nret, slots);
+        }
+      }
+    }
+  }
+  cudaStreamSynchronize(st);
+  for (void* p : tmp) cudaFree(p);
+  if (!rc && cudaGetLastError() != cudaSuccess) rc = set_err(SSFM_CUDA_ERROR, "pattern export kernel failed");
+  return rc;
+}
+
+// ---------------------------------------------------------------------------
+// generic dispatch helpers
+// ---------------------------------------------------------------------------
+static void count_launch(ssfm_handle* h, int n = 1) { h->prof.kernel_launches += n; }
+
+// cost(theta) -> misc.scal[SC_COST] (async)
+static int launch_cost(ssfm_handle* h, const double* theta, cudaStream_t st) {
+  if (h->kind == 0) {
+    BADev& d = h->ba;
+    ba_k_prep<<<h->cam_blocks, 256, 0, st>>>(d, theta);
+    ba_k_cost<<<h->cost_blocks, 256, 0, st>>>(d, theta, h->red);
+    k_sum_partials<<<1, 1024, 0, st>>>(h->red, h->cost_blocks, d.scal + SC_COST);
+    count_launch(h, 3);
+  } else {
+    GPDev& g = h->gp;
+    gp_k_cost<<<h->cost_blocks, 256, 0, st>>>(g, theta, h->red);
+    k_sum_partials<<<1, 1024, 0, st>>>(h->red, h->cost_blocks, g.scal + SC_COST);
+    count_launch(h, 2);
+  }
+  CU(cudaGetLastError());
+  return SSFM_OK;
+}
+
+// linearize(theta) on device (async); grad max / norm into misc.scal
+static int launch_linearize(ssfm_handle* h, const double* theta, double* r_out, double* J_out,
+                            cudaStream_t st) {
+  CU(cudaMemsetAsync(h->misc->scal + SC_GMAX, 0, sizeof(double), st));
+  if (h->kind == 0) {
+    BADev& d = h->ba;
+    ba_k_prep<<<h->cam_blocks, 256, 0, st>>>(d, theta);
+    ba_k_linearize<<<h->lin_blocks, 256, 0, st>>>(d, theta, r_out, J_out, h->red);
+    if (d.topo.nt) ba_k_camred<<<d.topo.nt, SSFM_TILE, 0, st>>>(d);
+    ba_k_camfin<<<h->cam_blocks, 256, 0, st>>>(d, h->red + (long long)h->lin_blocks * 8);
+    k_sum_partials<<<1, 1024, 0, st>>>(h->red, h->lin_blocks * 8 + h->cam_blocks, d.scal + SC_GNORM2);
+    count_launch(h, 5);
+  } else {
+    int rc = gp_launch_linearize(h->gp, theta, r_out, J_out, h->red, h->lin_blocks, h->cam_blocks, st);
+    if (rc) return set_err(SSFM_CUDA_ERROR, "gp linearize launch");
+    count_launch(h, 5);
+  }
+  CU(cudaGetLastError());
+  h->linearized = true;
+  return SSFM_OK;
+}
+
+static int launch_pcg(ssfm_handle* h, double lam, const ssfm_lm_config* cfg, cudaStream_t st) {
+  int max_it = cfg->cg_max_iters;
+  double tol = cfg->cg_tol;
+  void* args[11];
+  if (h->kind == 0) {
+    BADev& d = h->ba;
+    args[0] = &d; args[1] = &lam; args[2] = &max_it; args[3] = &tol;
+    args[4] = &h->x; args[5] = &h->r; args[6] = &h->z; args[7] = &h->p; args[8] = &h->q;
+    args[9] = &h->part;
+    CGCtl* ctl = &h->misc->ctl;
+    args[10] = &ctl;
+    CU(cudaLaunchCooperativeKernel((void*)ba_k_pcg, dim3(h->pcg_grid), dim3(PCG_THREADS), args, 0, st));
+  } else {
+    GPDev& g = h->gp;
+    args[0] = &g; args[1] = &lam; args[2] = &max_it; args[3] = &tol;
+    args[4] = &h->x; args[5] = &h->r; args[6] = &h->z; args[7] = &h->p; args[8] = &h->q;
+    args[9] = &h->part;
+    CGCtl* ctl = &h->misc->ctl;
+    args[10] = &ctl;
+    CU(cudaLaunchCooperativeKernel((void*)gp_k_pcg, dim3(h->pcg_grid), dim3(PCG_THREADS), args, 0, st));
+  }
+  count_launch(h);
+  return SSFM_OK;
+}
+
+// damped solve on the current linearization -> h->delta (async)
+static int launch_solve(ssfm_handle* h, double lam, const ssfm_lm_config* cfg, cudaStream_t st) {
+  CU(cudaMemsetAsync(&h->misc->status, 0, sizeof(int), st));
+  CU(cudaMemsetAsync(&h->misc->ctl, 0, sizeof(CGCtl), st));
+  if (h->kind == 0) {
+    BADev& d = h->ba;
+    ba_k_ptinv<<<nblk(d.bp.P, 256), 256, 0, st>>>(d, lam);
+    if (d.topo.nt) ba_k_precond<<<d.topo.nt, SSFM_TILE, 0, st>>>(d);
+    ba_k_camprec<<<h->cam_blocks, 64, 0, st>>>(d, lam);
+    count_launch(h, 3);
+  } else {
+    int rc = gp_launch_elim(h->gp, lam, h->cam_blocks, st);
+    if (rc) return set_err(SSFM_CUDA_ERROR, "gp elimination launch");
+    count_launch(h, 4);
+  }
+  CU(cudaGetLastError());
+  if (h->prof.on) CU(cudaEventRecord(h->ev2, st));
+  int rc = launch_pcg(h, lam, cfg, st);
+  if (rc) return rc;
+  if (h->prof.on) CU(cudaEventRecord(h->ev3, st));
+  if (h->kind == 0) {
+    BADev& d = h->ba;
+    ba_k_backsub<<<h->lin_blocks, 256, 0, st>>>(d, h->x, h->delta);
+    ba_k_camdelta<<<h->cam_blocks, 256, 0, st>>>(d, h->x, h->delta);
+    count_launch(h, 2);
+  } else {
+    gp_launch_backsub(h->gp, h->x, h->delta, h->lin_blocks, h->cam_blocks, st);
+    count_launch(h, 3);
+  }
+  CU(cudaGetLastError());
+  return SSFM_OK;
+}
+
+static int launch_post_step(ssfm_handle* h, double* theta, cudaStream_t st) {
+  if (h->kind == 0) {
+    ba_k_renorm<<<h->cam_blocks, 256, 0, st>>>(h->ba.bp.C, theta, &h->misc->status);
+    count_launch(h);
+  } else {
+    gp_launch_post_step(h->gp, theta, h->red, st);
+    count_launch(h, 3);
+  }
+  CU(cudaGetLastError());
+  return SSFM_OK;
+}
+
+static int read_misc(ssfm_handle* h, cudaStream_t st) {
+  CU(cudaMemcpyAsync(h->hmisc, h->misc, sizeof(Misc), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return SSFM_OK;
+}
+
+static int status_to_code(int s) {
+  if (s & (ST_SINGULAR_POINT | ST_PIN_POINT | ST_SINGULAR_PRECOND | ST_PIN_RETAINED | ST_PIN_SCALE))
+    return SSFM_SINGULAR_BLOCK;
+  if (s & (ST_CG_MAXITER | ST_CG_BREAKDOWN)) return SSFM_CG_STALL;
+  if (s & ST_ZERO_QUAT) return SSFM_ZERO_QUATERNION;
+  return SSFM_OK;
+}
+
+static std::string status_msg(int s, const Misc& m) {
+  char buf[256];
+  if (s & ST_SINGULAR_POINT) return "eliminable block singular after damping";
+  if (s & ST_PIN_POINT) return "masked point direction with non-zero gradient";
+  if (s & ST_PIN_SCALE) return "masked scale with non-zero coupling";
+  if (s & ST_PIN_RETAINED) return "masked retained direction with non-zero gradient";
+  if (s & ST_SINGULAR_PRECOND) return "singular preconditioner block";
+  if (s & ST_CG_MAXITER) {
+    snprintf(buf, sizeof buf, "CG did not reach tolerance in %d iterations (|r| %.3e, tol %.3e)",
+             m.ctl.iters, m.ctl.rn, m.ctl.tol);
+    return buf;
+  }
+  if (s & ST_CG_BREAKDOWN) return "CG broke down (p.q <= 0)";
+  if (s & ST_ZERO_QUAT) return "quaternion norm below 1e-12 during renormalization";
+  return "ok";
+}
+
+// ---------------------------------------------------------------------------
+// public entry points
+// ---------------------------------------------------------------------------
+extern "C" const char* ssfm_last_error(void) { return g_last_error.c_str(); }
+extern "C" const char* ssfm_version(void) { return "ssfm-b200 0.1 (sm_100a)"; }
+
+extern "C" int ssfm_destroy(ssfm_handle* h) {
+  free_handle(h);
+  return SSFM_OK;
+}
+
+extern "C" int64_t ssfm_num_params(const ssfm_handle* h) { return h ? h->total_params : -1; }
+extern "C" int64_t ssfm_num_residuals(const ssfm_handle* h) { return h ? h->total_res : -1; }
+extern "C" int64_t ssfm_device_bytes(const ssfm_handle* h) { return h ? (int64_t)h->bytes : -1; }
+
+extern "C" int ssfm_cost(ssfm_handle* h, const double* theta, double* cost_host, void* stream) {
+  if (!h || !theta) return set_err(SSFM_INVALID_ARGUMENT, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = launch_cost(h, theta, st);
+  if (rc) return rc;
+  if ((rc = read_misc(h, st))) return rc;
+  if (cost_host) *cost_host = h->hmisc->scal[SC_COST];
+  return SSFM_OK;
+}
+
+__global__ void k_export_grad_ba(BADev d, double* grad) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int C = d.bp.C, P = d.bp.P;
+  if (i < 7ll * C) {
+    grad[i] = d.gcam[8 * (i / 7) + (i % 7)];
+  } else if (i < d.bp.off_foc) {
+    grad[i] = d.gpt[i - 7ll * C];
+  } else if (d.bp.focal_mode == 1 && i < d.bp.off_foc + C) {
+    grad[i] = d.gcam[8 * (i - d.bp.off_foc) + 7];
+  }
+  (void)P;
+}
+
+extern "C" int ssfm_linearize(ssfm_handle* h, const double* theta, double* r_out, double* J_out,
+                              double* grad_out, double* grad_max_host, void* stream) {
+  if (!h || !theta) return set_err(SSFM_INVALID_ARGUMENT, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = launch_linearize(h, theta, r_out, J_out, st);
+  if (rc) return rc;
+  if (grad_out) {
+    if (h->kind == 0) k_export_grad_ba<<<nblk(h->total_params, 256), 256, 0, st>>>(h->ba, grad_out);
+    else gp_export_grad(h->gp, grad_out, st);
+    CU(cudaGetLastError());
+  }
+  if ((rc = read_misc(h, st))) return rc;
+  if (grad_max_host) *grad_max_host = h->hmisc->scal[SC_GMAX];
+  return SSFM_OK;
+}
+
+extern "C" int ssfm_solve_normal(ssfm_handle* h, double lambda, const ssfm_lm_config* cfg,
+                                 double* delta, int32_t* cg_iters_host, void* stream) {
+  if (!h || !cfg) return set_err(SSFM_INVALID_ARGUMENT, "null argument");
+  if (!h->linearized) return set_err(SSFM_INVALID_ARGUMENT, "ssfm_solve_normal before ssfm_linearize");
+  if (lambda < 0) return set_err(SSFM_INVALID_ARGUMENT, "lambda must be non-negative");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = launch_solve(h, lambda, cfg, st);
+  if (rc) return rc;
+  if (delta) CU(cudaMemcpyAsync(delta, h->delta, sizeof(double) * h->total_params, cudaMemcpyDeviceToDevice, st));
+  if ((rc = read_misc(h, st))) return rc;
+  const Misc& m = *h->hmisc;
+  if (cg_iters_host) *cg_iters_host = m.ctl.iters;
+  int code = status_to_code(m.status);
+  if (code) return set_err(code, status_msg(m.status, m));
+  return SSFM_OK;
+}
+
+extern "C" int ssfm_post_step(ssfm_handle* h, double* theta, void* stream) {
+  if (!h || !theta) return set_err(SSFM_INVALID_ARGUMENT, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  CU(cudaMemsetAsync(&h->misc->status, 0, sizeof(int), st));
+  int rc = launch_post_step(h, theta, st);
+  if (rc) return rc;
+  if ((rc = read_misc(h, st))) return rc;
+  int code = status_to_code(h->hmisc->status);
+  if (code) return set_err(code, status_msg(h->hmisc->status, *h->hmisc));
+  return SSFM_OK;
+}
+
+extern "C" int ssfm_lm_solve(ssfm_handle* h, double* theta_io, const ssfm_lm_config* cfg,
+                             ssfm_iter_record* recs, int32_t cap, int32_t* n_recs,
+                             int32_t* termination, void* stream) {
+  if (!h || !theta_io || !cfg) return set_err(SSFM_INVALID_ARGUMENT, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  using clk = std::chrono::steady_clock;
+  int rc;
+  if (n_recs) *n_recs = 0;
+  int term = SSFM_TERM_MAX_ITER;
+  const long long n = h->total_params;
+  CU(cudaMemcpyAsync(h->theta, theta_io, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  if ((rc = launch_cost(h, h->theta, st))) return rc;
+  if ((rc = read_misc(h, st))) return rc;
+  double cost = h->hmisc->scal[SC_COST];
+  double lam = cfg->lambda0;
+  bool need_lin = true;
+  int nrec = 0;
+  h->prof.pcg_ms = h->prof.lin_ms = h->prof.all_ms = 0;
+  h->prof.pcg_launches = h->prof.lin_launches = h->prof.all_launches = 0;
+  h->prof.cg_iters = 0;
+  h->prof.kernel_launches = 0;
+  int result = SSFM_OK;
+  for (int it = 1; it <= cfg->max_iterations; ++it) {
+    auto t0 = clk::now();
+    CU(cudaEventRecord(h->ev0, st));
+    if (need_lin) {
+      if ((rc = launch_linearize(h, h->theta, nullptr, nullptr, st))) return rc;
+      // linearize-time gradient check needs the gradient max (lm.py:762)
+      if ((rc = read_misc(h, st))) return rc;
+      const double gmax = h->hmisc->scal[SC_GMAX];
+      need_lin = false;
+      if (gmax < cfg->grad_tol) { term = SSFM_TERM_CONVERGED_GRAD; break; }
+    }
+    if ((rc = launch_solve(h, lam, cfg, st))) return rc;
+    // candidate = post_step(theta + delta); cost(candidate)
+    k_axpy_theta<<<nblk(n, 256), 256, 0, st>>>(h->theta, h->delta, h->cand, n);
+    count_launch(h);
+    if ((rc = launch_post_step(h, h->cand, st))) return rc;
+    if ((rc = launch_cost(h, h->cand, st))) return rc;
+    CU(cudaEventRecord(h->ev1, st));
+    if ((rc = read_misc(h, st))) return rc;
+    const Misc m = *h->hmisc;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+    if (h->prof.on) {
+      float pms = 0.f;
+      cudaEventElapsedTime(&pms, h->ev2, h->ev3);
+      h->prof.pcg_ms += pms;
+      h->prof.pcg_launches += 1;
+      h->prof.cg_iters += m.ctl.iters;
+    }
+    const int code = status_to_code(m.status);
+    const bool pcg_done = !(m.status & (ST_SINGULAR_POINT | ST_PIN_POINT | ST_SINGULAR_PRECOND |
+                                        ST_PIN_RETAINED | ST_PIN_SCALE | ST_CG_MAXITER | ST_CG_BREAKDOWN));
+    double cost_new = NAN;
+    bool failed = code != SSFM_OK;
+    if (failed) {
+      if (lam >= cfg->lambda_max) {
+        term = SSFM_TERM_SOLVER_FAILURE;
+        set_err(SSFM_SOLVER_FAILURE, "linear solve failed at lambda_max: " + status_msg(m.status, m));
+        result = SSFM_SOLVER_FAILURE;
+        break;
+      }
+    } else {
+      cost_new = m.scal[SC_COST];
+    }
+    const bool accepted = !failed && std::isfinite(cost_new) && cost_new < cost;
+    if (recs && nrec < cap) {
+      ssfm_iter_record& R = recs[nrec];
+      R.iteration = it;
+      R.cost_before = cost;
+      R.cost_after = cost_new;
+      R.lam = lam;
+      R.step_accepted = accepted;
+      R.cg_iters = pcg_done ? m.ctl.iters : 0;
+      R.status = code;
+      R.wall_time_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(clk::now() - t0).count();
+      R.device_ms = ms;
+    }
+    ++nrec;
+    h->prof.all_ms += ms;
+    h->prof.all_launches += 1;
+    if (accepted) {
+      const double rel = (cost - cost_new) / std::max(cost, 1e-300);
+      std::swap(h->theta, h->cand);
+      cost = cost_new;
+      lam = std::max(lam / cfg->lambda_down, cfg->lambda_min);
+      need_lin = true;
+      if (rel < cfg->rel_cost_tol) { term = SSFM_TERM_CONVERGED_COST; break; }
+    } else {
+      lam = std::min(lam * cfg->lambda_up, cfg->lambda_max);
+    }
+  }
+  CU(cudaMemcpyAsync(theta_io, h->theta, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  CU(cudaStreamSynchronize(st));
+  if (n_recs) *n_recs = std::min(nrec, (int)cap);
+  if (termination) *termination = term;
+  return result;
+}
+
+extern "C" int ssfm_profile_enable(ssfm_handle* h, int32_t on) {
+  if (!h) return SSFM_INVALID_ARGUMENT;
+  h->prof.on = on != 0;
+  return SSFM_OK;
+}
+
+extern "C" int ssfm_profile_get(const ssfm_handle* h, int32_t kind, double* ms, int64_t* launches,
+                                double* bytes) {
+  if (!h) return SSFM_INVALID_ARGUMENT;
+  const Profile& p = h->prof;
+  if (kind == 0) {
+    if (ms) *ms = p.pcg_ms;
+    if (launches) *launches = p.pcg_launches;
+    if (bytes) *bytes = (double)p.cg_iters;
+  } else if (kind == 1) {
+    if (ms) *ms = p.lin_ms;
+    if (launches) *launches = p.lin_launches;
+    if (bytes) *bytes = 0;
+  } else {
+    if (ms) *ms = p.all_ms;
+    if (launches) *launches = p.kernel_launches;
+    if (bytes) *bytes = 0;
+  }
+  return SSFM_OK;
+}
+
+extern "C" int ssfm_export_pattern(ssfm_handle* h, int32_t* obs_pt_order, int32_t* obs_cam_order,
+                                   int32_t* off_keys, int64_t off_cap, int64_t* n_off, int32_t* slots,
+                                   int64_t slot_cap, int64_t* n_slots, void* stream) {
+  if (!h) return set_err(SSFM_INVALID_ARGUMENT, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long N = h->topo.N;
+  if (obs_pt_order) CU(cudaMemcpyAsync(obs_pt_order, h->topo.pm_obs, sizeof(int) * N, cudaMemcpyDeviceToDevice, st));
+  if (obs_cam_order) CU(cudaMemcpyAsync(obs_cam_order, h->topo.cm_obs, sizeof(int) * N, cudaMemcpyDeviceToDevice, st));
+  int rc = export_keys(h, off_keys, off_cap, n_off, slots, slot_cap, n_slots, st);
+  if (rc) return rc;
+  CU(cudaStreamSynchronize(st));
+  return SSFM_OK;
+}
