@@ -1,0 +1,401 @@
+"""Benchmark: BA LM-iteration time and observations/s on B200 (vs the CPU reference).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config c5|c4ba|c3|c1] [--no-cpu-baseline] [--no-e2e]
+
+Workload (BASELINE.json `metric`): synthetic BA,
+default C5 = 5000 cameras / 2,000,000 points / 20,000,000 observations (k=10
+views per point), generate(sigma=1, seed 0) -> perturb(rot 1 deg, centre 1%,
+focal 2%, point 0.5%, seed 1) -> BAProblem(Huber 1.0) -> lm_solve with the
+reference's default LMConfig. A "step" is one LM iteration of that solve
+(linearize + J^T r + elimination + PCG + back-substitution + candidate cost).
+W warm-up iterations run first; the K timed iterations continue the same
+trajectory (theta and lambda carried over) in one lm_solve call bracketed by
+CUDA events on the launching stream, synchronize + barrier on both sides,
+max over ranks. The working set (compact Jacobian 2 x 2.56 GB) is far larger
+than the 126 MB L2, so no explicit flush is needed between iterations.
+
+`e2e` runs the same solve through the public API from HOST numpy arrays:
+problem construction (H2D copy + device ordering build), the LM iterations and
+the D2H copy of theta are inside the timed region.
+
+--impl reference times the unmodified reference package (oracle/_ref,
+sparsesfm Cython/OpenMP + numpy/scipy) on the host cores on a bounded sample of
+the same workload (rank 0 only).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (cameras, points, visibility k, sigma, loss delta, workload label)
+    "c1": (50, 5000, 4, 1.0, 1.0, "synthetic BA 50 cams / 5k pts / 20k obs (C1)"),
+    "c3": (1700, 150000, 5, 1.0, 1.0, "synthetic BA 1.7k cams / 150k pts / 750k obs (C3 shape)"),
+    "c4ba": (1000, 500000, 8, 1.0, 1.0, "synthetic BA 1k cams / 500k pts / 4M obs (C4 BA stage)"),
+    "c5": (5000, 2000000, 10, 1.0, 1.0, "synthetic large-scale BA 5000 cams / 2M pts / 20M obs (C5)"),
+}
+# bounded CPU sample of the C5 shape for the reference (same k = 10 views per point)
+REF_SAMPLE = (1000, 40000, 10)
+METRIC = "BA/GP LM iteration time and observations/sec at 1/2/4/8 B200 vs CPU ref"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (B200_PROFILING.md recipe)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# workload
+# ---------------------------------------------------------------------------
+def make_arrays(cams, pts, k, sigma, seed=0):
+    from paper_2510_13310_b200 import synth
+    cfg = synth.SynthConfig(num_cameras=cams, num_points=pts, visibility_fraction=k / cams,
+                            pixel_noise_sigma=sigma, seed=seed)
+    _, observed = synth.generate_arrays(cfg)
+    return synth.perturb_arrays(observed, rot_deg=1.0, center_frac=0.01, focal_frac=0.02,
+                                point_frac=0.005, seed=1)
+
+
+def next_lambda(cfg, rec):
+    if rec.step_accepted:
+        return max(rec.lam / cfg.lambda_down, cfg.lambda_min)
+    return min(rec.lam * cfg.lambda_up, cfg.lambda_max)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def run_b200(args, ws, rank, local):
+    import torch
+    import paper_2510_13310_b200 as b2
+    from paper_2510_13310_b200 import _native
+    import ctypes as ct
+
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cams, pts, k, sigma, delta, label = CONFIGS[args.config]
+    t0 = time.time()
+    arr = make_arrays(cams, pts, k, sigma)
+    N, P, C = arr.num_observations, arr.num_points, arr.num_cameras
+    log(f"[rank {rank}] generated {label}: N={N} in {time.time() - t0:.1f}s")
+    loss = b2.RobustLoss("huber", delta)
+    base_cfg = b2.LMConfig()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-resident run (value)
+    problem = b2.BAProblem(arr, loss)
+    theta0 = torch.as_tensor(problem.encode()).cuda()
+    h = problem._native_handle()
+    lib = _native.load()
+    t_setup = time.time()
+    # warm-up iterations (untimed)
+    wcfg = b2.LMConfig(max_iterations=args.warmup)
+    theta_w, rep_w = b2.lm_solve(problem, theta0, wcfg)
+    lam = next_lambda(base_cfg, rep_w.iterations[-1]) if rep_w.iterations else base_cfg.lambda0
+    lam = min(max(lam, base_cfg.lambda_min * 1.0000001), base_cfg.lambda_max * 0.9999999)
+    log(f"[rank {rank}] warmup {len(rep_w.iterations)} its {time.time() - t_setup:.1f}s, lambda -> {lam:g}")
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    stream = torch.cuda.current_stream()
+    # exactly K timed LM iterations: continue the warm-up trajectory; if a
+    # solve converges early, the next one restarts from theta0 (same workload)
+    ms_total, steps, iters = 0.0, 0, []
+    pms_sum, pl_sum, cg_sum, launch_sum = 0.0, 0, 0.0, 0
+    theta_cur, lam_cur = theta_w, lam
+    barrier()
+    while steps < args.steps:
+        tcfg = b2.LMConfig(max_iterations=args.steps - steps, lambda0=lam_cur)
+        lib.ssfm_profile_enable(ct.c_void_p(h.ptr), 1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        theta_t, rep_t = b2.lm_solve(problem, theta_cur, tcfg)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms_total += e0.elapsed_time(e1)
+        pms, pl, cgit = ct.c_double(0), ct.c_int64(0), ct.c_double(0)
+        lib.ssfm_profile_get(ct.c_void_p(h.ptr), 0, ct.byref(pms), ct.byref(pl), ct.byref(cgit))
+        ams, launches, _ = ct.c_double(0), ct.c_int64(0), ct.c_double(0)
+        lib.ssfm_profile_get(ct.c_void_p(h.ptr), 2, ct.byref(ams), ct.byref(launches), ct.byref(_))
+        pms_sum += pms.value; pl_sum += pl.value; cg_sum += cgit.value; launch_sum += launches.value
+        iters += rep_t.iterations
+        steps += len(rep_t.iterations)
+        if rep_t.termination != "max_iter" or not rep_t.iterations:
+            theta_cur, lam_cur = theta0, base_cfg.lambda0
+        else:
+            theta_cur = theta_t
+            lam_cur = min(max(next_lambda(base_cfg, rep_t.iterations[-1]), base_cfg.lambda_min * 1.0000001),
+                          base_cfg.lambda_max * 0.9999999)
+    barrier()
+    clocks = sampler.stop()
+    lib.ssfm_profile_enable(ct.c_void_p(h.ptr), 0)
+    pms, pl, cgit = ct.c_double(pms_sum), ct.c_int64(pl_sum), ct.c_double(cg_sum)
+    launches = ct.c_int64(launch_sum)
+    rep_t.iterations = iters
+    ms_max = ms_total
+    if dist is not None:
+        t = torch.tensor([ms_total], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    ms_per_step = ms_max / max(steps, 1)
+    value = ws * N * steps / (ms_max / 1e3)
+    log(f"[rank {rank}] timed {steps} its in {ms_total:.1f} ms; cg {[i.cg_iters for i in rep_t.iterations]}; "
+        f"term {rep_t.termination}")
+
+    # roofline of the dominant kernel: the PCG solve (ba_k_pcg), S*p dominated
+    peak, peak_kind = peaks()
+    bytes_per_cg = 136.0 * N + 72.0 * P + 128.0 * C          # SURVEY.md 8(d), S*p per CG iteration
+    roof = None
+    if pms.value > 0 and cgit.value > 0:
+        ach = bytes_per_cg * cgit.value / (pms.value / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(ach / peak, 4), "traffic": None, "peak_source": peak_kind,
+                "kernel": "ba_k_pcg", "launches": int(pl.value), "cg_iters": int(cgit.value),
+                "kernel_ms": round(pms.value, 3),
+                "algorithmic_bytes_per_cg_iter": bytes_per_cg,
+                "kernel_share_of_step": round(pms.value / max(ms_total, 1e-9), 4)}
+    del theta_t
+
+    # ---- end to end through the public API from host arrays
+    e2e = None
+    if not args.no_e2e:
+        theta_host = problem.encode()
+        barrier()
+        t_a = time.perf_counter()
+        e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e_a.record(stream)
+        p2 = b2.BAProblem(arr, loss)
+        th_out, rep_e = b2.lm_solve(p2, theta_host, b2.LMConfig(max_iterations=args.warmup + args.steps))
+        e_b.record(stream)
+        barrier()
+        wall = time.perf_counter() - t_a
+        e_ms = e_a.elapsed_time(e_b)
+        its = max(len(rep_e.iterations), 1)
+        if dist is not None:
+            t = torch.tensor([wall], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            wall = float(t.item())
+        h2d = (N * (4 + 4 + 16) + C * (16 + 16 + 8) + theta_host.nbytes)
+        e2e = {"value": ws * N * its / wall, "unit": "obs/s",
+               "h2d_bytes_per_step": int(h2d / its), "d2h_bytes_per_step": int(theta_host.nbytes / its),
+               "iterations": its, "wall_s": round(wall, 3), "device_ms": round(e_ms, 1),
+               "termination": rep_e.termination}
+        del p2
+    result = {
+        "metric": METRIC, "value": value, "unit": "obs/s", "n_gpus": ws, "steps": steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": label, "cameras": C, "points": P, "observations": N,
+                   "views_per_point": k, "loss": f"huber({delta})", "lm": "LMConfig() defaults",
+                   "parallelism": "replicas" if ws > 1 else "single",
+                   "l2": "inputs larger than L2 (J 2x2.56 GB)" if N >= 10**6 else "small (latency bound)"},
+        "cg_iters_per_step": [i.cg_iters for i in rep_t.iterations],
+        "lm_ms_per_iteration": [round(i.device_ms, 3) for i in rep_t.iterations],
+        "roofline": roof, "e2e": e2e, "clocks": clocks, "gpu_launches": int(launches.value),
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline_sample(max_iterations=4)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return result
+
+
+# ---------------------------------------------------------------------------
+# reference (CPU) side
+# ---------------------------------------------------------------------------
+def _import_reference():
+    ref_dir = os.path.join(ROOT, "oracle", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "sparsesfm")):
+        return None, f"reference not built ({ref_dir}); run oracle/build_ref.sh"
+    if ref_dir not in sys.path:
+        sys.path.insert(0, ref_dir)
+    os.environ.setdefault("SPARSESFM_BACKEND", "cython")
+    ncpu = os.cpu_count() or 1
+    os.environ.setdefault("SPARSESFM_WORKERS", str(ncpu))
+    import sparsesfm
+    return sparsesfm, None
+
+
+def cpu_baseline_sample(max_iterations=4):
+    """Bounded sample: the reference on a C5-shaped reduction (k = 10)."""
+    ref, why = _import_reference()
+    if ref is None:
+        return {"value": None, "unit": "obs/s", "cores": 0, "kind": "reference", "sample": why}
+    from sparsesfm import synth_metrics as rsm
+    cams, pts, k = REF_SAMPLE
+    truth, obs = rsm.generate(rsm.SynthConfig(num_cameras=cams, num_points=pts,
+                                              visibility_fraction=k / cams, pixel_noise_sigma=1.0, seed=0))
+    start = rsm.perturb(obs, rot_deg=1.0, center_frac=0.01, focal_frac=0.02, point_frac=0.005, seed=1)
+    prob = ref.BAProblem(start, ref.RobustLoss("huber", 1.0))
+    t0 = time.perf_counter()
+    _, rep = ref.lm_solve(prob, prob.encode(), ref.LMConfig(max_iterations=max_iterations))
+    wall = time.perf_counter() - t0
+    its = rep.iterations
+    later = [i.wall_time_ns for i in its[1:]] or [i.wall_time_ns for i in its]
+    med = statistics.median(later) / 1e9
+    n = start.num_observations
+    return {"value": n / med, "unit": "obs/s", "cores": int(os.environ.get("SPARSESFM_WORKERS", "1")),
+            "kind": "reference",
+            "sample": f"reference sparsesfm (Cython/OpenMP backend) BA {cams} cams / {pts} pts / {n} obs "
+                      f"(C5 shape, k={k}), {len(its)} LM iterations, median of iterations 2..n "
+                      f"({med:.2f} s/iter; first {its[0].wall_time_ns / 1e9:.2f} s incl. pattern build); "
+                      f"total {wall:.1f} s",
+            "s_per_iter_median": med}
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return None
+    ref, why = _import_reference()
+    cams, pts, k, sigma, delta, label = CONFIGS[args.config]
+    if ref is None:
+        return {"impl": "reference", "unavailable": why}
+    from sparsesfm import synth_metrics as rsm
+    scams, spts, sk = REF_SAMPLE if args.config == "c5" else (cams, pts, k)
+    truth, obs = rsm.generate(rsm.SynthConfig(num_cameras=scams, num_points=spts,
+                                              visibility_fraction=sk / scams, pixel_noise_sigma=sigma,
+                                              seed=0))
+    start = rsm.perturb(obs, rot_deg=1.0, center_frac=0.01, focal_frac=0.02, point_frac=0.005, seed=1)
+    prob = ref.BAProblem(start, ref.RobustLoss("huber", delta))
+    n = start.num_observations
+    cfg = ref.LMConfig(max_iterations=args.warmup + args.steps)
+    t0 = time.perf_counter()
+    _, rep = ref.lm_solve(prob, prob.encode(), cfg)
+    wall = time.perf_counter() - t0
+    its = rep.iterations
+    timed = its[args.warmup:] or its
+    t_timed = sum(i.wall_time_ns for i in timed) / 1e9
+    value = n * len(timed) / t_timed
+    cores = int(os.environ.get("SPARSESFM_WORKERS", "1"))
+    sample = (f"reference sparsesfm BA {scams} cams / {spts} pts / {n} obs (k={sk}"
+              f"{', bounded C5-shaped sample' if args.config == 'c5' else ''}); "
+              f"{len(its)} LM iterations, last {len(timed)} timed; total {wall:.1f} s")
+    return {"metric": METRIC, "value": value, "unit": "obs/s", "n_gpus": ws, "steps": len(timed),
+            "warmup": args.warmup, "ms_per_step": 1e3 * t_timed / len(timed), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": label, "sample_cameras": scams, "sample_points": spts,
+                       "sample_observations": n},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "obs/s", "cores": cores, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "obs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "termination": rep.termination}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warmup raised to 3 (timing rules)")
+        args.warmup = 3
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        res = run_reference(args, ws, rank)
+    else:
+        res = run_b200(args, ws, rank, local)
+    if rank == 0 and res is not None:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -572,7 +572,7 @@ static int launch_solve(ssfm_handle* h, double lam, const ssfm_lm_config* cfg, c
     BADev& d = h->ba;
     ba_k_ptinv<<<nblk(d.bp.P, 256), 256, 0, st>>>(d, lam);
     if (d.topo.nt) ba_k_precond<<<d.topo.nt, SSFM_TILE, 0, st>>>(d);
-    ba_k_camprec<<<h->cam_blocks, 64, 0, st>>>(d, lam);
+    ba_k_camprec<<<nblk(d.bp.C, 64), 64, 0, st>>>(d, lam);
     count_launch(h, 3);
   } else {
     int rc = gp_launch_elim(h->gp, lam, h->cam_blocks, st);

@@ -59,6 +59,7 @@ class IterationRecord:
     cg_iters: int
     wall_time_ns: int
     device_ms: float = 0.0
+    status: int = 0           # ssfm_status of an in-step failure (rejection), else 0
 
 
 @dataclass(slots=True)
@@ -168,7 +169,8 @@ def lm_solve(problem, theta0, config: LMConfig | None = None,
         r = recs[k]
         report.iterations.append(IterationRecord(
             int(r.iteration), float(r.cost_before), float(r.cost_after), float(r.lam),
-            bool(r.step_accepted), int(r.cg_iters), int(r.wall_time_ns), float(r.device_ms)))
+            bool(r.step_accepted), int(r.cg_iters), int(r.wall_time_ns), float(r.device_ms),
+            int(r.status)))
     if rc == 3:
         msg = lib.ssfm_last_error().decode(errors="replace")
         report.termination = "solver_failure"
