@@ -48,7 +48,8 @@ __global__ void k_slot_codes(const int* __restrict__ pt_seg, const int* __restri
   const int s = pt_seg[j];
   const int m = pt_seg[j + 1] - s;
   const int L = (kind == 0 && F) ? 2 * m : m;
-  const long long nret = (long long)C + (kind == 0 ? F : 0);
+  // F: 2 per-camera focal (C focal blocks), 1 shared focal, 0 none
+  const long long nret = (long long)C + (kind == 0 ? (F == 1 ? 1 : (F == 2 ? C : 0)) : 0);
   long long o = off[j];
   for (int a = 0; a < L; ++a) {
     const long long ra0 = ret_item(pm_cam, s, a, m, kind, C, F);

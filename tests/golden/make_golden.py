@@ -1,0 +1,197 @@
+"""Generate the golden fixtures under tests/golden/ from the UNMODIFIED reference.
+
+Run in the build container (needs oracle/_ref, built by oracle/build_ref.sh
+from /root/reference):
+
+    python tests/golden/make_golden.py
+
+Every fixture records reference inputs and outputs for the hot path; the
+tests compare the oracle port (oracle/sparsesfm_port.py) and the B200 path
+against them. Nothing here runs at test time.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, os.path.join(ROOT, "oracle", "_ref"))
+os.environ["SPARSESFM_BACKEND"] = "cython"
+
+import sparsesfm as ref  # noqa: E402
+from sparsesfm import synth_metrics as rsm  # noqa: E402
+from sparsesfm.lm import _get_schur_plan  # noqa: E402
+from sparsesfm.scene import (project, quat_from_axis_angle, quat_multiply,  # noqa: E402
+                             scene_to_arrays)
+from sparsesfm.sparse_block import apply_damping, jtj, jtr  # noqa: E402
+
+
+def arrays_of(scene):
+    a = scene_to_arrays(scene)
+    return dict(quats=a.quats, centers=a.centers, focals=a.focals, pps=a.pps, dists=a.dists,
+                points=a.points, cam=a.cam_idx, pt=a.pt_idx, pixels=a.pixels,
+                depths=a.depths if a.depths is not None else np.zeros(0))
+
+
+def records(rep):
+    return np.array([(i.iteration, i.cost_before, i.cost_after, i.lam, float(i.step_accepted),
+                      i.cg_iters) for i in rep.iterations], dtype=np.float64).reshape(-1, 6)
+
+
+def schur_slot_pairs(sys, ws):
+    plan = _get_schur_plan(sys, ws)
+    ret_off = plan.ret_s_off
+    ra = np.searchsorted(ret_off, plan.slot_row, side="right") - 1
+    rb = np.searchsorted(ret_off, plan.slot_col, side="right") - 1
+    return np.stack([ra, rb], axis=1).astype(np.int64)
+
+
+def ba_fixture(name, scene, loss, optimize_focal=True, shared_focal=False, iters=30, model_tag=None):
+    prob = ref.BAProblem(scene, loss, optimize_focal, shared_focal)
+    th0 = prob.encode()
+    cost0 = prob.cost(th0)
+    r0, J0 = prob.linearize(th0)
+    r0 = r0.copy()
+    Jd = J0.data.copy()
+    g0 = jtr(J0, r0)
+    sys_ = jtj(J0)
+    sys_.gradient[:] = -g0
+    ws = ref.Workspace()
+    delta = ref.solve_normal(apply_damping(sys_, 1e-3), prob.layout, ref.LMConfig(), ws,
+                             info := {})
+    slots = schur_slot_pairs(apply_damping(sys_, 1e-3), ws)
+    th, rep = ref.lm_solve(prob, th0, ref.LMConfig(max_iterations=iters))
+    out = arrays_of(scene)
+    out.update(theta0=th0, cost0=cost0, r0=r0, J0=Jd, grad0=g0, off_keys=sys_.off_keys.astype(np.int64),
+               schur_slots=slots, delta_lam1e3=delta, cg_lam1e3=info.get("cg_iters", 0),
+               theta_final=th, records=records(rep), termination=rep.termination,
+               optimize_focal=int(optimize_focal), shared_focal=int(shared_focal),
+               loss_kind=loss.kind, loss_delta=loss.delta,
+               model=scene.cameras[0].model_tag)
+    np.savez_compressed(os.path.join(HERE, name), **out)
+    print(name, rep.termination, len(rep.iterations), "its, final", rep.iterations[-1].cost_after)
+
+
+def gp_fixture(name, scene, loss, depth_mode, iters=40):
+    prob = ref.fix_gauge(ref.make_rays(scene, depth_mode, loss, seed=0))
+    th0 = prob.initial_theta()
+    cost0 = prob.cost(th0)
+    r0, J0 = prob.linearize(th0)
+    r0 = r0.copy()
+    Jd = J0.data.copy()
+    g0 = jtr(J0, r0)
+    sys_ = jtj(J0)
+    sys_.gradient[:] = -g0
+    ws = ref.Workspace()
+    delta = ref.solve_normal(apply_damping(sys_, 1e-2), prob.layout, ref.LMConfig(), ws, info := {})
+    slots = schur_slot_pairs(apply_damping(sys_, 1e-2), ws)
+    post = prob.post_step(th0 + 0.1 * np.sin(np.arange(len(th0))))
+    th, rep = ref.lm_solve(prob, th0, ref.LMConfig(max_iterations=iters))
+    out = arrays_of(scene)
+    out.update(rays=prob.rays, ray_depths=prob.depths if prob.depths is not None else np.zeros(0),
+               theta0=th0, cost0=cost0, r0=r0, J0=Jd, grad0=g0, off_keys=sys_.off_keys.astype(np.int64),
+               schur_slots=slots, delta_lam1e2=delta, cg_lam1e2=info.get("cg_iters", 0),
+               post_step_probe=post, theta_final=th, records=records(rep), termination=rep.termination,
+               depth_mode=int(depth_mode), loss_kind=loss.kind, loss_delta=loss.delta)
+    np.savez_compressed(os.path.join(HERE, name), **out)
+    print(name, rep.termination, len(rep.iterations), "its, final", rep.iterations[-1].cost_after)
+
+
+def bal_scene(seed=5):
+    """BAL-radial scene: cameras look down -z (rotation composed with 180 deg
+    about x), pixels from the reference's own bal_radial projection + noise."""
+    truth, _ = rsm.generate(rsm.SynthConfig(num_cameras=6, num_points=80, visibility_fraction=4 / 6,
+                                            radius=8.0, focal=300.0, seed=seed))
+    rng = np.random.default_rng(seed)
+    flip = quat_from_axis_angle([1.0, 0.0, 0.0], np.pi)
+    cams = []
+    for c in truth.cameras:
+        cams.append(ref.Camera(quat_multiply(flip, np.asarray(c.rotation)), c.center, c.focal,
+                               np.array([1.5, -2.0]), "bal_radial",
+                               np.array([rng.uniform(-0.05, 0.05), rng.uniform(-0.01, 0.01)])))
+    obs = []
+    for o in truth.observations:
+        px = project(cams[o.camera_id], truth.points[o.point_id]) + rng.normal(0, 0.5, 2)
+        obs.append(ref.Observation(o.camera_id, o.point_id, px))
+    scene = ref.Scene(cams, truth.points, obs)
+    return rsm.perturb(scene, rot_deg=0.5, center_frac=0.005, focal_frac=0.01, point_frac=0.003, seed=2)
+
+
+def digest(arrs):
+    h = hashlib.sha256()
+    for k in ("quats", "centers", "focals", "points", "cam", "pt", "pixels", "depths"):
+        h.update(np.ascontiguousarray(arrs[k]).tobytes())
+    return h.hexdigest()
+
+
+def main():
+    # --- BA fixtures
+    truth, obs = rsm.generate(rsm.SynthConfig(num_cameras=8, num_points=120, visibility_fraction=0.5,
+                                              pixel_noise_sigma=1.0, seed=3))
+    start = rsm.perturb(obs, rot_deg=1.0, center_frac=0.01, focal_frac=0.02, point_frac=0.005, seed=1)
+    ba_fixture("ba_small.npz", start, ref.RobustLoss("huber", 1.0))
+    ba_fixture("ba_nofocal.npz", start, ref.RobustLoss("trivial"), optimize_focal=False)
+    ba_fixture("ba_bal.npz", bal_scene(), ref.RobustLoss("huber", 2.0))
+    # --- GP fixtures
+    truth, obs = rsm.generate(rsm.SynthConfig(num_cameras=10, num_points=200, visibility_fraction=0.4,
+                                              pixel_noise_sigma=0.5, seed=2))
+    gp_fixture("gp_small.npz", obs, ref.RobustLoss("huber", 0.1), depth_mode=False)
+    gp_fixture("gp_depth.npz", obs, ref.RobustLoss("trivial"), depth_mode=True, iters=30)
+    # --- C1 and generator digests
+    summary = {}
+    truth, obs = rsm.generate(rsm.SynthConfig(num_cameras=50, num_points=5000, visibility_fraction=4 / 50,
+                                              pixel_noise_sigma=1.0, seed=0))
+    start = rsm.perturb(obs, rot_deg=1.0, center_frac=0.01, focal_frac=0.02, point_frac=0.005, seed=1)
+    prob = ref.BAProblem(start, ref.RobustLoss("huber", 1.0))
+    th, rep = ref.lm_solve(prob, prob.encode(), ref.LMConfig())
+    res = prob.decode(th)
+    summary["c1"] = dict(termination=rep.termination, iterations=len(rep.iterations),
+                         final_cost=rep.iterations[-1].cost_after,
+                         cg_iters=[i.cg_iters for i in rep.iterations],
+                         accepted=[bool(i.step_accepted) for i in rep.iterations],
+                         rmse=rsm.reproj_rmse(res), cost0=prob.cost(prob.encode()),
+                         start_digest=digest(arrays_of(start)))
+    np.save(os.path.join(HERE, "c1_theta_final.npy"), th)
+    digests = {}
+    for name, cfg, pert in [
+        ("c1_observed", dict(num_cameras=50, num_points=5000, visibility_fraction=4 / 50,
+                             pixel_noise_sigma=1.0, seed=0), None),
+        ("sphere_outliers", dict(num_cameras=30, num_points=3000, rig="sphere", visibility_fraction=0.2,
+                                 pixel_noise_sigma=0.7, outlier_fraction=0.05, seed=4), None),
+        ("big_pop", dict(num_cameras=12000, num_points=200, visibility_fraction=10 / 12000,
+                         pixel_noise_sigma=1.0, seed=9), None),
+        ("c5_shape_small", dict(num_cameras=5000, num_points=20000, visibility_fraction=10 / 5000,
+                                pixel_noise_sigma=1.0, seed=0),
+         dict(rot_deg=1.0, center_frac=0.01, focal_frac=0.02, point_frac=0.005, seed=1)),
+    ]:
+        t, o = rsm.generate(rsm.SynthConfig(**cfg))
+        digests[name + ":truth"] = digest(arrays_of(t))
+        digests[name + ":observed"] = digest(arrays_of(o))
+        if pert:
+            digests[name + ":perturbed"] = digest(arrays_of(rsm.perturb(o, **pert)))
+        digests[name + ":config"] = cfg
+        digests[name + ":perturb"] = pert
+    summary["digests"] = digests
+    # --- GP C2 at 40 iterations (SURVEY.md 8(c) survey-recorded golden)
+    truth, obs = rsm.generate(rsm.SynthConfig(num_cameras=200, num_points=50000, visibility_fraction=6 / 200,
+                                              pixel_noise_sigma=0.5, seed=0))
+    gp = ref.fix_gauge(ref.make_rays(obs, depth_mode=False, loss=ref.RobustLoss("huber", 0.1), seed=0))
+    th, rep = ref.lm_solve(gp, gp.initial_theta(), ref.LMConfig(max_iterations=40))
+    summary["c2"] = dict(termination=rep.termination, iterations=len(rep.iterations),
+                         final_cost=rep.iterations[-1].cost_after,
+                         cg_iters=[i.cg_iters for i in rep.iterations],
+                         accepted=[bool(i.step_accepted) for i in rep.iterations])
+    np.save(os.path.join(HERE, "c2_theta_final.npy"), th[:3 * 200 + 3 * 50000])
+    with open(os.path.join(HERE, "summary.json"), "w") as fh:
+        json.dump(summary, fh, indent=1)
+    print(json.dumps({k: (v if k != "digests" else "...") for k, v in summary.items()}, indent=1)[:2000])
+
+
+if __name__ == "__main__":
+    main()
