@@ -189,6 +189,15 @@ int ssfm_profile_get(const ssfm_handle* h, int32_t kind, double* ms,
                      int64_t* launches, double* bytes);
 int ssfm_profile_enable(ssfm_handle* h, int32_t on);
 
+/* Which Schur operator the PCG kernel of this handle runs (no reference
+ * counterpart; it replaces the dense S@p of lm.py:656). *slot_groups = 0: the
+ * two-pass operator (point-major then camera-major Jacobian reads); >= 1: the
+ * fused single-pass operator with the 8 camera slots split over that many CTAs
+ * (fused.cuh). *grid / *threads: the persistent kernel's launch geometry.
+ * *smem_bytes: dynamic shared memory per CTA. Any pointer may be NULL. */
+int ssfm_operator_info(const ssfm_handle* h, int32_t* slot_groups, int32_t* grid,
+                       int32_t* threads, int64_t* smem_bytes);
+
 #ifdef __cplusplus
 }
 #endif

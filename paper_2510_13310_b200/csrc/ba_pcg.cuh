@@ -14,6 +14,7 @@
 #pragma once
 #include <cooperative_groups.h>
 #include "ba_kernels.cuh"
+#include "fused.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -125,19 +126,139 @@ __device__ __forceinline__ void ba_camera_pass(const BADev& d, const double* y, 
   }
 }
 
-__global__ void __launch_bounds__(PCG_THREADS) ba_k_pcg(BADev d, double lam, int max_iters,
-                                                        double cg_tol, double* x, double* r,
-                                                        double* z, double* p, double* q,
-                                                        double* part, CGCtl* ctl) {
+
+// Fused single pass (fused.cuh): y_j for every point of the step's batches,
+// then the camera terms Jc^T Jp y_j accumulated into the CTA's slot group of
+// the shared-memory camera vector `acc` (SL slots per camera), rank by rank.
+// Finally the CTA writes its slot group to gpart[grp][8C].
+template <int SL>
+__device__ __forceinline__ void ba_fused_pass(const BADev& d, const FusedTopo& fz,
+                                              const double* __restrict__ v, double* acc,
+                                              double (*smv)[SSFM_BATCH][3],
+                                              double (*smy)[SSFM_BATCH][3],
+                                              int (*smown)[SSFM_BATCH]) {
+  constexpr int G = 8 / SL;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = blockIdx.x % G, grp = blockIdx.x / G, ngrp = gridDim.x / G;
+  const int C = d.bp.C;
+  const long long Np = d.Npad;
+  for (int k = threadIdx.x; k < SL * C; k += blockDim.x) acc[k] = 0.0;
+  __syncthreads();
+  for (int s = grp; s < fz.nsteps; s += ngrp) {
+    const int b = s * FZ_WARPS + warp;
+    int ob0 = 0, ob1 = 0, pb0 = 0, pb1 = 0;
+    if (b < d.topo.nb) {
+      ob0 = __ldg(d.topo.bat_obs + b); ob1 = __ldg(d.topo.bat_obs + b + 1);
+      pb0 = __ldg(d.topo.bat_pt + b); pb1 = __ldg(d.topo.bat_pt + b + 1);
+    }
+    const int rounds = (ob1 - ob0 + 31) >> 5;
+    const int my_pt = pb0 + lane;
+    int ps = 0, pe = 0;
+    if (my_pt < pb1) { ps = __ldg(d.topo.pt_seg + my_pt); pe = __ldg(d.topo.pt_seg + my_pt + 1); }
+    double J[BA_JREC];
+    int cr = 0;
+    double a3[3] = {0.0, 0.0, 0.0};
+    // phase 1: per-point sums of Jp^T Jc p (observation order)
+    for (int r = 0; r < rounds; ++r) {
+      const int base = ob0 + 32 * r;
+      const int i = base + lane;
+      double val[3] = {0.0, 0.0, 0.0};
+      if (i < ob1) {
+#pragma unroll
+        for (int k = 0; k < BA_JREC; ++k) J[k] = __ldg(d.Jpm + k * Np + i);
+        cr = __ldg(fz.camr + i);
+        const int c = cr & FZ_CMASK;
+        double pc[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) pc[k] = v[8ll * c + k];
+        double t[2];
+        ba_jc_mul(J, pc, t);
+        ba_jpt_mul(J, t, val);
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) smv[warp][lane][k] = val[k];
+      __syncwarp();
+      const int a = max(ps, base), e = min(pe, base + SSFM_BATCH);
+      for (int o = a; o < e; ++o) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) a3[k] += smv[warp][o - base][k];
+        smown[warp][o - base] = lane;
+      }
+      __syncwarp();
+    }
+    if (my_pt < pb1) {
+      double ci[6], w[3];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) ci[k] = __ldg(d.Cinv + 6ll * my_pt + k);
+      sym3_matvec(ci, a3, w);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) smy[warp][lane][k] = w[k];
+    }
+    __syncwarp();
+    // phase 2: camera terms, rank-ordered accumulation
+    const int info = __ldg(fz.step_info + s);
+    const int R = info & 0xffff, K = info >> 16;
+    for (int r = 0; r < R; ++r) {
+      const int i = ob0 + 32 * r + lane;
+      const bool have = r < rounds && i < ob1;
+      double u[SL];
+      int c = 0, rk = -1;
+      if (have) {
+        if (rounds > 1) {   // a single point with > 32 observations: reload its round
+#pragma unroll
+          for (int k = 0; k < BA_JREC; ++k) J[k] = __ldg(d.Jpm + k * Np + i);
+          cr = __ldg(fz.camr + i);
+        }
+        c = cr & FZ_CMASK;
+        rk = cr >> FZ_RSHIFT;
+        const int owner = rounds > 1 ? 0 : smown[warp][lane];
+        double y[3], t2[2], o[8];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) y[k] = smy[warp][owner][k];
+        ba_jp_mul(J, y, t2);
+        ba_jct_mul(J, t2, o);
+#pragma unroll
+        for (int m = 0; m < 8; ++m)
+          if (m / SL == g) u[m % SL] = o[m];
+      }
+      for (int k = 0; k < K; ++k) {
+        if (rk == k) {
+#pragma unroll
+          for (int j = 0; j < SL; ++j) acc[c * SL + j] += u[j];
+        }
+        __syncthreads();
+      }
+    }
+  }
+  __syncthreads();
+  double* dst = fz.gpart + (long long)grp * 8 * C;
+  for (int k = threadIdx.x; k < SL * C; k += blockDim.x) {
+    const int c = k / SL, j = k - c * SL;
+    dst[8ll * c + g * SL + j] = acc[k];
+  }
+}
+
+// The whole PCG as one persistent cooperative kernel. SL = 0: two-pass
+// operator (P1 point pass, P2 camera tiles). SL > 0: fused single pass with
+// 8/SL slot groups (fused.cuh); needs SL*C doubles of dynamic shared memory.
+template <int SL>
+__global__ void __launch_bounds__(SL ? FZ_THREADS : PCG_THREADS, SL ? 1 : 4)
+ba_k_pcg(BADev d, FusedTopo fz, double lam, int max_iters, double cg_tol, double* x, double* r,
+         double* z, double* p, double* q, double* part, CGCtl* ctl) {
+  constexpr int NT = SL ? FZ_THREADS : PCG_THREADS;
   cg::grid_group grid = cg::this_grid();
-  __shared__ double smp[PCG_THREADS / 32][SSFM_BATCH][3];
-  __shared__ double smred[(PCG_THREADS / 32) * 8];
+  __shared__ double smp[NT / 32][SSFM_BATCH][3];
+  __shared__ double smy[SL ? NT / 32 : 1][SSFM_BATCH][3];
+  __shared__ int smown[SL ? NT / 32 : 1][SSFM_BATCH];
+  __shared__ double smred[(NT / 32) * 8];
   __shared__ double smb[4];
+  extern __shared__ double dyn_acc[];
   const int S = 8 * d.bp.C;
   const int stride = gridDim.x * blockDim.x;
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   double* tile8 = d.tilebuf;
   const int NP = gridDim.x;
+  const int ngrp = SL ? gridDim.x / (8 / (SL ? SL : 8)) : 0;
 
   // ---- init: x = 0, r = b_red, z = M r, p = z
   {
@@ -172,11 +293,15 @@ __global__ void __launch_bounds__(PCG_THREADS) ba_k_pcg(BADev d, double lam, int
   if (rn > tol) {
     while (true) {
       if (iters >= max_iters) { flag = ST_CG_MAXITER; break; }
-      // P1: point pass
-      ba_point_pass(d, p, d.yv, smp);
-      grid.sync();
-      // P2: camera tiles
-      ba_camera_pass(d, d.yv, tile8, smred);
+      if constexpr (SL == 0) {
+        // P1: point pass
+        ba_point_pass(d, p, d.yv, smp);
+        grid.sync();
+        // P2: camera tiles
+        ba_camera_pass(d, d.yv, tile8, smred);
+      } else {
+        ba_fused_pass<SL>(d, fz, p, dyn_acc, smp, smy, smown);
+      }
       grid.sync();
       // P3: q = S p per slot, p.q partials
       {
@@ -195,8 +320,12 @@ __global__ void __launch_bounds__(PCG_THREADS) ba_k_pcg(BADev d, double lam, int
           }
           if (ok) {
             double acc = 0.0;
-            const int t0 = d.topo.cam_tile[c], t1 = d.topo.cam_tile[c + 1];
-            for (int t = t0; t < t1; ++t) acc += tile8[8ll * t + k];
+            if constexpr (SL == 0) {
+              const int t0 = d.topo.cam_tile[c], t1 = d.topo.cam_tile[c + 1];
+              for (int t = t0; t < t1; ++t) acc += tile8[8ll * t + k];
+            } else {
+              for (int gq = 0; gq < ngrp; ++gq) acc += fz.gpart[(long long)gq * S + s];
+            }
             double qk = bp + lam * d.Bc[64ll * c + 9 * k] * pk - acc;
             if ((d.pinned[c] >> k) & 1) qk = pk;
             q[s] = qk;

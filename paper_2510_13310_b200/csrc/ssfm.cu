@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -67,6 +68,10 @@ struct ssfm_handle {
   Misc* misc = nullptr;         // device
   Misc* hmisc = nullptr;        // pinned host
   int pcg_grid = 0;
+  int pcg_threads = PCG_THREADS;
+  size_t pcg_smem = 0;
+  void* pcg_fn = nullptr;
+  FusedTopo fz{};
   int lin_blocks = 0;
   int cost_blocks = 0;
   int cam_blocks = 0;
@@ -214,6 +219,70 @@ static int common_alloc(ssfm_handle* h, int S_slots, int C) {
   return SSFM_OK;
 }
 
+// Choose the BA PCG operator and its launch geometry; build the fused schedule.
+template <int SL>
+static int try_fused_ba(ssfm_handle* h, int* ok) {
+  *ok = 0;
+  const int C = h->ba.bp.C;
+  cudaFuncAttributes fa;
+  CU(cudaFuncGetAttributes(&fa, ba_k_pcg<SL>));
+  int optin = 0;
+  CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+  const size_t dyn = sizeof(double) * (size_t)SL * C;
+  if (fa.sharedSizeBytes + dyn > (size_t)optin) return SSFM_OK;
+  CU(cudaFuncSetAttribute(ba_k_pcg<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+  int occ = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ba_k_pcg<SL>, FZ_THREADS, dyn));
+  if (occ < 1) return SSFM_OK;
+  const int G = 8 / SL;
+  int grid = occ * h->num_sms;
+  grid -= grid % G;
+  if (grid < G) return SSFM_OK;
+  h->pcg_grid = grid;
+  h->pcg_threads = FZ_THREADS;
+  h->pcg_smem = dyn;
+  h->pcg_fn = (void*)ba_k_pcg<SL>;
+  h->fz.G = G;
+  h->fz.SL = SL;
+  h->fz.ngrp = grid / G;
+  *ok = 1;
+  return SSFM_OK;
+}
+
+static int setup_ba_pcg(ssfm_handle* h, cudaStream_t st) {
+  const Topo& T = h->topo;
+  const int C = h->ba.bp.C;
+  const char* env = getenv("SSFM_FUSED");
+  const bool want = !(env && env[0] == '0') && C < FZ_MAX_CAMERAS;
+  // SSFM_FUSED=0 forces the two-pass operator; SSFM_FUSED=2/4/8 forces that many
+  // slot groups (tests exercise the multi-group path on small problems)
+  const int force_g = (env && (env[0] == '2' || env[0] == '4' || env[0] == '8')) ? env[0] - '0' : 1;
+  int ok = 0, rc;
+  if (want && force_g <= 1 && (rc = try_fused_ba<8>(h, &ok))) return rc;
+  if (want && !ok && force_g <= 2 && (rc = try_fused_ba<4>(h, &ok))) return rc;
+  if (want && !ok && force_g <= 4 && (rc = try_fused_ba<2>(h, &ok))) return rc;
+  if (want && !ok && (rc = try_fused_ba<1>(h, &ok))) return rc;
+  if (ok) {
+    FusedTopo& fz = h->fz;
+    fz.nsteps = nblk(T.nb, FZ_WARPS);
+    DALLOC(fz.camr, T.N);
+    DALLOC(fz.step_info, fz.nsteps);
+    DALLOC(fz.gpart, (long long)fz.ngrp * 8 * C);
+    if (fz.nsteps) k_fz_ranks<<<fz.nsteps, FZ_THREADS, 0, st>>>(T, fz.camr, fz.step_info, fz.nsteps);
+    CU(cudaGetLastError());
+    return SSFM_OK;
+  }
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ba_k_pcg<0>, PCG_THREADS, 0) || occ < 1)
+    return set_err(SSFM_CUDA_ERROR, "occupancy query for the PCG kernel failed");
+  h->pcg_grid = occ * h->num_sms;
+  h->pcg_threads = PCG_THREADS;
+  h->pcg_smem = 0;
+  h->pcg_fn = (void*)ba_k_pcg<0>;
+  h->fz = FusedTopo{};
+  return SSFM_OK;
+}
+
 // ---------------------------------------------------------------------------
 // BA
 // ---------------------------------------------------------------------------
@@ -285,11 +354,9 @@ extern "C" int ssfm_create_ba(const ssfm_ba_desc* desc, void* stream, ssfm_handl
   if ((rc = common_alloc(h, 8 * C, C))) return fail(rc);
   d.scal = h->misc->scal;
   d.status = &h->misc->status;
-  // launch geometry
-  int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ba_k_pcg, PCG_THREADS, 0) || occ < 1)
-    return fail(set_err(SSFM_CUDA_ERROR, "occupancy query for the PCG kernel failed"));
-  h->pcg_grid = occ * h->num_sms;
+  // launch geometry of the PCG kernel (fused single-pass operator when the
+  // camera vector fits the shared memory of <= 8 CTAs, else two-pass)
+  if ((rc = setup_ba_pcg(h, st))) return fail(rc);
   h->lin_blocks = std::max(1, std::min(nblk(T.nb, 8), h->num_sms * 16));
   h->cost_blocks = nblk(N, 256);
   h->cam_blocks = nblk(C, 256);
@@ -545,12 +612,12 @@ static int launch_pcg(ssfm_handle* h, double lam, const ssfm_lm_config* cfg, cud
   void* args[11];
   if (h->kind == 0) {
     BADev& d = h->ba;
-    args[0] = &d; args[1] = &lam; args[2] = &max_it; args[3] = &tol;
-    args[4] = &h->x; args[5] = &h->r; args[6] = &h->z; args[7] = &h->p; args[8] = &h->q;
-    args[9] = &h->part;
+    void* a[12];
     CGCtl* ctl = &h->misc->ctl;
-    args[10] = &ctl;
-    CU(cudaLaunchCooperativeKernel((void*)ba_k_pcg, dim3(h->pcg_grid), dim3(PCG_THREADS), args, 0, st));
+    a[0] = &d; a[1] = &h->fz; a[2] = &lam; a[3] = &max_it; a[4] = &tol;
+    a[5] = &h->x; a[6] = &h->r; a[7] = &h->z; a[8] = &h->p; a[9] = &h->q;
+    a[10] = &h->part; a[11] = &ctl;
+    CU(cudaLaunchCooperativeKernel(h->pcg_fn, dim3(h->pcg_grid), dim3(h->pcg_threads), a, h->pcg_smem, st));
   } else {
     GPDev& g = h->gp;
     args[0] = &g; args[1] = &lam; args[2] = &max_it; args[3] = &tol;
@@ -846,6 +913,16 @@ extern "C" int ssfm_profile_get(const ssfm_handle* h, int32_t kind, double* ms, 
     if (launches) *launches = p.kernel_launches;
     if (bytes) *bytes = 0;
   }
+  return SSFM_OK;
+}
+
+extern "C" int ssfm_operator_info(const ssfm_handle* h, int32_t* slot_groups, int32_t* grid,
+                                  int32_t* threads, int64_t* smem_bytes) {
+  if (!h) return set_err(SSFM_INVALID_ARGUMENT, "null argument");
+  if (slot_groups) *slot_groups = h->fz.G;
+  if (grid) *grid = h->pcg_grid;
+  if (threads) *threads = h->kind == 0 ? h->pcg_threads : PCG_THREADS;
+  if (smem_bytes) *smem_bytes = (int64_t)h->pcg_smem;
   return SSFM_OK;
 }
 
