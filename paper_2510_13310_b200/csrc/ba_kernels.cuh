@@ -6,7 +6,7 @@
 //   Jpm[16][N]  compact Jacobian, SoA, point-major   (read by point passes)
 //   Jcm[16][N]  same records, SoA, camera-major       (read by camera passes)
 //   rcm[2][N]   weighted residual, camera-major
-//   per point (AoS): Cpt[6] (Jp^T Jp), gpt[3] (Jp^T r), Cinv[6], y0[3], yv[3]
+//   per point (AoS): Cpt[6] (Jp^T Jp), gpt[3] (Jp^T r), Cinv[6], y0[3], yv[4]
 //   per camera (AoS): Bc[64] (Jc^T Jc, 8x8 full), gcam[8], Minv[64], bred[8]
 // The compact record is 16 fp64 per observation instead of the reference's
 // 22 (ba.py:63): the pose-center block equals -(point block) (ba.py:187-188).
@@ -33,7 +33,7 @@ struct BADev {
   double* tilebuf;        // [44 * nt]
   double* Cinv;           // [6P]
   double* y0;             // [3P]
-  double* yv;             // [3P]
+  double* yv;             // [4P] (padded for 32-byte gathers)
   double* Minv;           // [64C]
   double* bred;           // [8C]
   unsigned char* pinned;  // [C] bitmask of pinned retained slots
@@ -508,8 +508,8 @@ __global__ void __launch_bounds__(256) ba_k_backsub(BADev d, const double* __res
         for (int k = 0; k < BA_JREC; ++k) J[k] = d.Jpm[k * Np + i];
         const int c = d.topo.pm_cam[i];
         double pc[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) pc[k] = x[8ll * c + k];
+        ld_v4(x + 8ll * c, pc);
+        ld_v4(x + 8ll * c + 4, pc + 4);
         double t[2];
         ba_jc_mul(J, pc, t);
         ba_jpt_mul(J, t, val);

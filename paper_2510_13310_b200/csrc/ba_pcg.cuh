@@ -69,8 +69,8 @@ __device__ __forceinline__ void ba_point_pass(const BADev& d, const double* v, d
         for (int k = 0; k < BA_JREC; ++k) J[k] = __ldg(d.Jpm + k * Np + i);
         const int c = __ldg(d.topo.pm_cam + i);
         double pc[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) pc[k] = v[8ll * c + k];
+        ld_v4(v + 8ll * c, pc);
+        ld_v4(v + 8ll * c + 4, pc + 4);
         double t[2];
         ba_jc_mul(J, pc, t);
         ba_jpt_mul(J, t, val);
@@ -91,7 +91,7 @@ __device__ __forceinline__ void ba_point_pass(const BADev& d, const double* v, d
       for (int k = 0; k < 6; ++k) ci[k] = __ldg(d.Cinv + 6ll * my_pt + k);
       sym3_matvec(ci, acc, w);
 #pragma unroll
-      for (int k = 0; k < 3; ++k) y[3ll * my_pt + k] = w[k];
+      for (int k = 0; k < 3; ++k) y[4ll * my_pt + k] = w[k];
     }
   }
 }
@@ -111,9 +111,8 @@ __device__ __forceinline__ void ba_camera_pass(const BADev& d, const double* y, 
 #pragma unroll
       for (int k = 0; k < BA_JREC; ++k) J[k] = __ldg(d.Jcm + k * Np + i);
       const int j = __ldg(d.topo.cm_pt + i);
-      double yj[3];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) yj[k] = y[3ll * j + k];
+      double yj[4];
+      ld_v4(y + 4ll * j, yj);
       double tt[2];
       ba_jp_mul(J, yj, tt);
       ba_jct_mul(J, tt, o);
@@ -127,13 +126,15 @@ __device__ __forceinline__ void ba_camera_pass(const BADev& d, const double* y, 
 }
 
 
-// Fused single pass (fused.cuh): y_j for every point of the step's batches,
-// then the camera terms Jc^T Jp y_j accumulated into the CTA's slot group of
-// the shared-memory camera vector `acc` (SL slots per camera), rank by rank.
+// Fused single pass (fused.cuh): y_j for every point of the warp's batch,
+// then the camera terms Jc^T Jp y_j added into the CTA's slot group of the
+// shared-memory camera vector `acc` (SL slots per camera) in ticket order.
 // Finally the CTA writes its slot group to gpart[grp][8C].
+// Dynamic shared memory: acc [SL*C] doubles | stage [FZ_WARPS][32][SL] doubles |
+// cnt [C] ints.
 template <int SL>
 __device__ __forceinline__ void ba_fused_pass(const BADev& d, const FusedTopo& fz,
-                                              const double* __restrict__ v, double* acc,
+                                              const double* __restrict__ v, double* dyn,
                                               double (*smv)[SSFM_BATCH][3],
                                               double (*smy)[SSFM_BATCH][3],
                                               int (*smown)[SSFM_BATCH]) {
@@ -142,21 +143,43 @@ __device__ __forceinline__ void ba_fused_pass(const BADev& d, const FusedTopo& f
   const int g = blockIdx.x % G, grp = blockIdx.x / G, ngrp = gridDim.x / G;
   const int C = d.bp.C;
   const long long Np = d.Npad;
+  double* acc = dyn;
+  double* stage = dyn + (long long)SL * C + (long long)warp * 32 * SL;
+  int* cnt = reinterpret_cast<int*>(dyn + (long long)SL * C + FZ_WARPS * 32 * SL);
   for (int k = threadIdx.x; k < SL * C; k += blockDim.x) acc[k] = 0.0;
+  for (int k = threadIdx.x; k < C; k += blockDim.x) cnt[k] = 0;
   __syncthreads();
-  for (int s = grp; s < fz.nsteps; s += ngrp) {
-    const int b = s * FZ_WARPS + warp;
-    int ob0 = 0, ob1 = 0, pb0 = 0, pb1 = 0;
-    if (b < d.topo.nb) {
-      ob0 = __ldg(d.topo.bat_obs + b); ob1 = __ldg(d.topo.bat_obs + b + 1);
-      pb0 = __ldg(d.topo.bat_pt + b); pb1 = __ldg(d.topo.bat_pt + b + 1);
+  // batch metadata is prefetched one batch ahead; Cinv, ticket and J of a
+  // batch are issued together so each batch costs ~2 dependent latencies
+  // (J/cam -> p gather) instead of a chain of five.
+  const int sstride = ngrp * FZ_WARPS;
+  int b = grp * FZ_WARPS + warp;
+  int nob0 = 0, nob1 = 0, npb0 = 0, npb1 = 0;
+  if (b < d.topo.nb) {
+    nob0 = __ldg(d.topo.bat_obs + b); nob1 = __ldg(d.topo.bat_obs + b + 1);
+    npb0 = __ldg(d.topo.bat_pt + b); npb1 = __ldg(d.topo.bat_pt + b + 1);
+  }
+  for (; b < d.topo.nb; b += sstride) {
+    const int ob0 = nob0, ob1 = nob1, pb0 = npb0, pb1 = npb1;
+    const int my_pt = pb0 + lane;
+    const bool own = my_pt < pb1;
+    int ps = 0, pe = 0;
+    double ci[6];
+    if (own) {
+      ps = __ldg(d.topo.pt_seg + my_pt); pe = __ldg(d.topo.pt_seg + my_pt + 1);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) ci[k] = __ldg(d.Cinv + 6ll * my_pt + k);
+    }
+    {
+      const int bn = b + sstride;
+      if (bn < d.topo.nb) {
+        nob0 = __ldg(d.topo.bat_obs + bn); nob1 = __ldg(d.topo.bat_obs + bn + 1);
+        npb0 = __ldg(d.topo.bat_pt + bn); npb1 = __ldg(d.topo.bat_pt + bn + 1);
+      }
     }
     const int rounds = (ob1 - ob0 + 31) >> 5;
-    const int my_pt = pb0 + lane;
-    int ps = 0, pe = 0;
-    if (my_pt < pb1) { ps = __ldg(d.topo.pt_seg + my_pt); pe = __ldg(d.topo.pt_seg + my_pt + 1); }
     double J[BA_JREC];
-    int cr = 0;
+    int c = 0, tk = 0;
     double a3[3] = {0.0, 0.0, 0.0};
     // phase 1: per-point sums of Jp^T Jc p (observation order)
     for (int r = 0; r < rounds; ++r) {
@@ -164,13 +187,13 @@ __device__ __forceinline__ void ba_fused_pass(const BADev& d, const FusedTopo& f
       const int i = base + lane;
       double val[3] = {0.0, 0.0, 0.0};
       if (i < ob1) {
+        c = __ldg(d.topo.pm_cam + i);
 #pragma unroll
         for (int k = 0; k < BA_JREC; ++k) J[k] = __ldg(d.Jpm + k * Np + i);
-        cr = __ldg(fz.camr + i);
-        const int c = cr & FZ_CMASK;
+        tk = __ldg(fz.tick + i);
         double pc[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) pc[k] = v[8ll * c + k];
+        ld_v4(v + 8ll * c, pc);
+        ld_v4(v + 8ll * c + 4, pc + 4);
         double t[2];
         ba_jc_mul(J, pc, t);
         ba_jpt_mul(J, t, val);
@@ -186,31 +209,29 @@ __device__ __forceinline__ void ba_fused_pass(const BADev& d, const FusedTopo& f
       }
       __syncwarp();
     }
-    if (my_pt < pb1) {
-      double ci[6], w[3];
-#pragma unroll
-      for (int k = 0; k < 6; ++k) ci[k] = __ldg(d.Cinv + 6ll * my_pt + k);
+    if (own) {
+      double w[3];
       sym3_matvec(ci, a3, w);
 #pragma unroll
       for (int k = 0; k < 3; ++k) smy[warp][lane][k] = w[k];
     }
     __syncwarp();
-    // phase 2: camera terms, rank-ordered accumulation
-    const int info = __ldg(fz.step_info + s);
-    const int R = info & 0xffff, K = info >> 16;
-    for (int r = 0; r < R; ++r) {
+    // phase 2: camera terms, ticket-ordered accumulation
+    for (int r = 0; r < rounds; ++r) {
       const int i = ob0 + 32 * r + lane;
-      const bool have = r < rounds && i < ob1;
+      const bool have = i < ob1;
       double u[SL];
-      int c = 0, rk = -1;
+#pragma unroll
+      for (int j = 0; j < SL; ++j) u[j] = 0.0;
+      int t = 0;
       if (have) {
         if (rounds > 1) {   // a single point with > 32 observations: reload its round
 #pragma unroll
           for (int k = 0; k < BA_JREC; ++k) J[k] = __ldg(d.Jpm + k * Np + i);
-          cr = __ldg(fz.camr + i);
+          c = __ldg(d.topo.pm_cam + i);
+          tk = __ldg(fz.tick + i);
         }
-        c = cr & FZ_CMASK;
-        rk = cr >> FZ_RSHIFT;
+        t = tk;
         const int owner = rounds > 1 ? 0 : smown[warp][lane];
         double y[3], t2[2], o[8];
 #pragma unroll
@@ -221,14 +242,42 @@ __device__ __forceinline__ void ba_fused_pass(const BADev& d, const FusedTopo& f
         for (int m = 0; m < 8; ++m)
           if (m / SL == g) u[m % SL] = o[m];
       }
-      for (int k = 0; k < K; ++k) {
-        if (rk == k) {
+      if (fz.atomic) {   // experiment: unordered shared-memory fp64 atomics (not bit-stable)
+        if (have) {
 #pragma unroll
-          for (int j = 0; j < SL; ++j) acc[c * SL + j] += u[j];
+          for (int j = 0; j < SL; ++j) atomicAdd(acc + c * SL + j, u[j]);
         }
-        __syncthreads();
+        continue;
+      }
+      const unsigned same = __match_any_sync(SSFM_FULL, have ? c : -1);
+      const bool dup = __popc(same) > 1;
+      if (__any_sync(SSFM_FULL, dup && have)) {
+#pragma unroll
+        for (int j = 0; j < SL; ++j) stage[lane * SL + j] = u[j];
+        __syncwarp();
+        if (have && dup && lane == __ffs(same) - 1) {
+#pragma unroll
+          for (int j = 0; j < SL; ++j) u[j] = 0.0;
+          for (unsigned m = same; m; m &= m - 1) {
+            const int l = __ffs(m) - 1;
+#pragma unroll
+            for (int j = 0; j < SL; ++j) u[j] += stage[l * SL + j];
+          }
+        }
+        __syncwarp();
+      }
+      if (have && lane == __ffs(same) - 1) {
+        cuda::atomic_ref<int, cuda::thread_scope_block> ca(cnt[c]);
+        int spins = 0;
+        while (ca.load(cuda::memory_order_acquire) != t) {
+          if (++spins > FZ_SPIN_LIMIT) { atomicOr(d.status, ST_SCHEDULE); break; }
+        }
+#pragma unroll
+        for (int j = 0; j < SL; ++j) acc[c * SL + j] += u[j];
+        ca.store(t + 1, cuda::memory_order_release);
       }
     }
+    __syncwarp();
   }
   __syncthreads();
   double* dst = fz.gpart + (long long)grp * 8 * C;

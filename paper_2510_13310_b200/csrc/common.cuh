@@ -25,6 +25,7 @@ enum : int {
   ST_ZERO_QUAT = 1 << 6,          // lm.py:114-115
   ST_PIN_SCALE = 1 << 7,          // lm.py:569-575
   ST_BAD_INDEX = 1 << 8,
+  ST_SCHEDULE = 1 << 9,           // fused-operator ticket schedule violated (internal error)
 };
 
 __device__ __forceinline__ double shfl_xor_d(double v, int m) {
@@ -76,6 +77,16 @@ __device__ __forceinline__ void block_reduce(double (&v)[V], double* sm) {
     }
   }
   __syncthreads();
+}
+
+// 32-byte vector load (LDG.E.ENL2.256 on sm_100a): 4 consecutive doubles, the
+// address must be 32-byte aligned. One instruction per 4 doubles of a gathered
+// camera/point block instead of four 8-byte gathers (L1 wavefronts dominate
+// scattered gathers). Coherent (no .nc): the vectors gathered this way are
+// rewritten between grid barriers inside the persistent PCG kernels.
+__device__ __forceinline__ void ld_v4(const double* a, double* x) {
+  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(x[0]), "=d"(x[1]), "=d"(x[2]), "=d"(x[3]) : "l"(a));
 }
 
 // Symmetric 3x3 stored as upper triangle {00,01,02,11,12,22}.

@@ -228,7 +228,7 @@ static int try_fused_ba(ssfm_handle* h, int* ok) {
   CU(cudaFuncGetAttributes(&fa, ba_k_pcg<SL>));
   int optin = 0;
   CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
-  const size_t dyn = sizeof(double) * (size_t)SL * C;
+  const size_t dyn = sizeof(double) * ((size_t)SL * C + FZ_WARPS * 32 * SL) + sizeof(int) * (size_t)C;
   if (fa.sharedSizeBytes + dyn > (size_t)optin) return SSFM_OK;
   CU(cudaFuncSetAttribute(ba_k_pcg<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
   int occ = 0;
@@ -259,18 +259,52 @@ static int setup_ba_pcg(ssfm_handle* h, cudaStream_t st) {
   const int force_g = (env && (env[0] == '2' || env[0] == '4' || env[0] == '8')) ? env[0] - '0' : 1;
   int ok = 0, rc;
   if (want && force_g <= 1 && (rc = try_fused_ba<8>(h, &ok))) return rc;
-  if (want && !ok && force_g <= 2 && (rc = try_fused_ba<4>(h, &ok))) return rc;
-  if (want && !ok && force_g <= 4 && (rc = try_fused_ba<2>(h, &ok))) return rc;
-  if (want && !ok && (rc = try_fused_ba<1>(h, &ok))) return rc;
+  // By default only the single-group fused operator is used: with G > 1 the
+  // redundant point-side work of the G CTAs costs more than the second
+  // Jacobian read it saves (measured at C5: 1.91 vs 1.32 ms per CG iteration).
+  const bool multi = force_g > 1;
+  if (want && multi && !ok && force_g <= 2 && (rc = try_fused_ba<4>(h, &ok))) return rc;
+  if (want && multi && !ok && force_g <= 4 && (rc = try_fused_ba<2>(h, &ok))) return rc;
+  if (want && multi && !ok && (rc = try_fused_ba<1>(h, &ok))) return rc;
   if (ok) {
     FusedTopo& fz = h->fz;
+    CU(cudaMemsetAsync(h->ba.status, 0, sizeof(int), st));
+    const char* ea = getenv("SSFM_FUSED_ATOMIC");
+    fz.atomic = (ea && ea[0] == '1') ? 1 : 0;
     fz.nsteps = nblk(T.nb, FZ_WARPS);
-    DALLOC(fz.camr, T.N);
-    DALLOC(fz.step_info, fz.nsteps);
+    DALLOC(fz.tick, T.N);
     DALLOC(fz.gpart, (long long)fz.ngrp * 8 * C);
-    if (fz.nsteps) k_fz_ranks<<<fz.nsteps, FZ_THREADS, 0, st>>>(T, fz.camr, fz.step_info, fz.nsteps);
+    // tickets: stable sort of observations by (CTA group, camera), runs walked in order
+    unsigned long long *key, *skey;
+    int *unit, *idx, *sidx;
+    std::vector<void*> tmp;
+    auto talloc = [&](void** p, size_t b) { cudaError_t e = cudaMalloc(p, b); if (!e) tmp.push_back(*p); return e; };
+    auto tfree = [&]() { cudaStreamSynchronize(st); for (void* q : tmp) cudaFree(q); };
+    const long long N = T.N;
+    if (talloc((void**)&key, 8 * N) || talloc((void**)&skey, 8 * N) || talloc((void**)&unit, 4 * N) ||
+        talloc((void**)&idx, 4 * N) || talloc((void**)&sidx, 4 * N)) {
+      tfree();
+      return set_err(SSFM_CUDA_ERROR, "fused schedule: out of device memory");
+    }
+    k_fz_keys<<<nblk((long long)T.nb * 32, 256), 256, 0, st>>>(T, fz.ngrp, key, unit, idx);
+    int kbits = 1;
+    while ((1ull << kbits) < (unsigned long long)fz.ngrp * C) ++kbits;
+    size_t sb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, sb, key, skey, idx, sidx, (int)N, 0, kbits, st);
+    void* stmp = nullptr;
+    if (talloc(&stmp, sb)) { tfree(); return set_err(SSFM_CUDA_ERROR, "fused schedule: out of device memory"); }
+    cub::DeviceRadixSort::SortPairs(stmp, sb, key, skey, idx, sidx, (int)N, 0, kbits, st);
+    k_fz_tickets<<<nblk(N, 256), 256, 0, st>>>(skey, sidx, unit, N, fz.tick, h->ba.status);
+    int hst = 0;
+    cudaMemcpyAsync(&hst, h->ba.status, sizeof(int), cudaMemcpyDeviceToHost, st);
+    tfree();
+    if (hst & ST_SCHEDULE) {   // a camera with > 65535 units in one CTA group: two-pass operator
+      h->fz = FusedTopo{};
+      cudaMemsetAsync(h->ba.status, 0, sizeof(int), st);
+      ok = 0;
+    }
     CU(cudaGetLastError());
-    return SSFM_OK;
+    if (ok) return SSFM_OK;
   }
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ba_k_pcg<0>, PCG_THREADS, 0) || occ < 1)
@@ -347,7 +381,7 @@ extern "C" int ssfm_create_ba(const ssfm_ba_desc* desc, void* stream, ssfm_handl
   if ((rc = dalloc(h, &d.tilebuf, (long long)CAM_V * T.nt))) return fail(rc);
   if ((rc = dalloc(h, &d.Cinv, 6ll * P))) return fail(rc);
   if ((rc = dalloc(h, &d.y0, 3ll * P))) return fail(rc);
-  if ((rc = dalloc(h, &d.yv, 3ll * P))) return fail(rc);
+  if ((rc = dalloc(h, &d.yv, 4ll * P))) return fail(rc);   // padded: 32-byte gathers
   if ((rc = dalloc(h, &d.Minv, 64ll * C))) return fail(rc);
   if ((rc = dalloc(h, &d.bred, 8ll * C))) return fail(rc);
   if ((rc = dalloc(h, &d.pinned, C))) return fail(rc);
