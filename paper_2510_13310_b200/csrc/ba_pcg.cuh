@@ -144,7 +144,7 @@ __device__ __forceinline__ void ba_fused_pass(const BADev& d, const FusedTopo& f
   const int C = d.bp.C;
   const long long Np = d.Npad;
   double* acc = dyn;
-  double* stage = dyn + (long long)SL * C + (long long)warp * 32 * SL;
+  double* stage = dyn + (long long)SL * C + (long long)warp * 32 * SL;   // [SL][32] per warp
   int* cnt = reinterpret_cast<int*>(dyn + (long long)SL * C + FZ_WARPS * 32 * SL);
   for (int k = threadIdx.x; k < SL * C; k += blockDim.x) acc[k] = 0.0;
   for (int k = threadIdx.x; k < C; k += blockDim.x) cnt[k] = 0;
@@ -245,7 +245,7 @@ __device__ __forceinline__ void ba_fused_pass(const BADev& d, const FusedTopo& f
       if (fz.atomic) {   // experiment: unordered shared-memory fp64 atomics (not bit-stable)
         if (have) {
 #pragma unroll
-          for (int j = 0; j < SL; ++j) atomicAdd(acc + c * SL + j, u[j]);
+          for (int j = 0; j < SL; ++j) atomicAdd(acc + fz_slot<SL>(c, j), u[j]);
         }
         continue;
       }
@@ -253,7 +253,7 @@ __device__ __forceinline__ void ba_fused_pass(const BADev& d, const FusedTopo& f
       const bool dup = __popc(same) > 1;
       if (__any_sync(SSFM_FULL, dup && have)) {
 #pragma unroll
-        for (int j = 0; j < SL; ++j) stage[lane * SL + j] = u[j];
+        for (int j = 0; j < SL; ++j) stage[j * 32 + lane] = u[j];
         __syncwarp();
         if (have && dup && lane == __ffs(same) - 1) {
 #pragma unroll
@@ -261,20 +261,18 @@ __device__ __forceinline__ void ba_fused_pass(const BADev& d, const FusedTopo& f
           for (unsigned m = same; m; m &= m - 1) {
             const int l = __ffs(m) - 1;
 #pragma unroll
-            for (int j = 0; j < SL; ++j) u[j] += stage[l * SL + j];
+            for (int j = 0; j < SL; ++j) u[j] += stage[j * 32 + l];
           }
         }
         __syncwarp();
       }
       if (have && lane == __ffs(same) - 1) {
-        cuda::atomic_ref<int, cuda::thread_scope_block> ca(cnt[c]);
         int spins = 0;
-        while (ca.load(cuda::memory_order_acquire) != t) {
+        while (ld_acquire_smem(cnt + c) != t) {
           if (++spins > FZ_SPIN_LIMIT) { atomicOr(d.status, ST_SCHEDULE); break; }
         }
-#pragma unroll
-        for (int j = 0; j < SL; ++j) acc[c * SL + j] += u[j];
-        ca.store(t + 1, cuda::memory_order_release);
+        fz_add<SL>(acc, c, u);
+        st_release_smem(cnt + c, t + 1);
       }
     }
     __syncwarp();
@@ -283,7 +281,7 @@ __device__ __forceinline__ void ba_fused_pass(const BADev& d, const FusedTopo& f
   double* dst = fz.gpart + (long long)grp * 8 * C;
   for (int k = threadIdx.x; k < SL * C; k += blockDim.x) {
     const int c = k / SL, j = k - c * SL;
-    dst[8ll * c + g * SL + j] = acc[k];
+    dst[8ll * c + g * SL + j] = acc[fz_slot<SL>(c, j)];
   }
 }
 

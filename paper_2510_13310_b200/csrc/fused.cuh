@@ -50,6 +50,51 @@ struct FusedTopo {
 
 #define FZ_MAX_TICKET 65535
 
+// Ticket counters live in shared memory; acquire/release at CTA scope on the
+// shared window (generic atomics would go through the generic LSU path).
+__device__ __forceinline__ int ld_acquire_smem(const int* p) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_smem(int* p, int v) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// Camera accumulator layout: SL doubles per camera, its 16-byte chunks XOR-
+// swizzled by the camera id so that lanes updating random cameras spread over
+// all 32 banks (an unswizzled 64-byte record maps every camera onto 2 bank
+// groups: 16-way conflicts).
+template <int SL>
+__device__ __forceinline__ int fz_slot(int c, int j) {
+  if constexpr (SL >= 4) {
+    constexpr int M = SL / 2 - 1;
+    return c * SL + ((((j >> 1) ^ (c & M))) << 1) + (j & 1);
+  } else {
+    return c * SL + j;
+  }
+}
+
+template <int SL>
+__device__ __forceinline__ void fz_add(double* acc, int c, const double* u) {
+  if constexpr (SL >= 2) {
+    constexpr int M = SL / 2 - 1;
+    double2* a2 = reinterpret_cast<double2*>(acc + (long long)c * SL);
+#pragma unroll
+    for (int q = 0; q < SL / 2; ++q) {   // logical chunk q lives at physical chunk q ^ (c & M)
+      const int pq = q ^ (c & M);
+      double2 cur = a2[pq];
+      cur.x += u[2 * q];
+      cur.y += u[2 * q + 1];
+      a2[pq] = cur;
+    }
+  } else {
+    acc[c] += u[0];
+  }
+}
+
 // per observation: sort key (CTA group, camera) and unit id (first observation
 // index of its 32-round). One warp per batch.
 __global__ void k_fz_keys(Topo T, int ngrp, unsigned long long* key, int* unit, int* idx) {
