@@ -155,11 +155,16 @@ def run_b200(args, ws, rank, local):
     from paper_2510_13310_b200 import _native
     import ctypes as ct
 
-    torch.cuda.set_device(local)
+    same_dev = ws > 1 and args.same_device
+    torch.cuda.set_device(0 if same_dev else local)
     dist = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if same_dev:   # plumbing check of the sharded path on one GPU (not a measurement)
+            os.environ["SSFM_PCG_SMS"] = str(140 // ws)
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cams, pts, k, sigma, delta, label = CONFIGS[args.config]
     t0 = time.time()
     arr = make_arrays(cams, pts, k, sigma)
@@ -174,8 +179,17 @@ def run_b200(args, ws, rank, local):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # ---- device-resident run (value)
-    problem = b2.BAProblem(arr, loss)
+    # ---- device-resident run (value). N > 1: points sharded over the ranks,
+    # cameras replicated, camera sums exchanged through peer memory (dist.py)
+    from paper_2510_13310_b200 import dist as bdist
+
+    def make_problem():
+        if ws > 1:
+            return bdist.ShardedBAProblem(arr, loss, rank=rank, world=ws)
+        return b2.BAProblem(arr, loss)
+
+    problem = make_problem()
+    Nl, Pl = problem.num_obs, problem.num_points
     theta0 = torch.as_tensor(problem.encode()).cuda()
     h = problem._native_handle()
     lib = _native.load()
@@ -230,13 +244,13 @@ def run_b200(args, ws, rank, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_max = float(t.item())
     ms_per_step = ms_max / max(steps, 1)
-    value = ws * N * steps / (ms_max / 1e3)
+    value = N * steps / (ms_max / 1e3)
     log(f"[rank {rank}] timed {steps} its in {ms_total:.1f} ms; cg {[i.cg_iters for i in rep_t.iterations]}; "
         f"term {rep_t.termination}")
 
     # roofline of the dominant kernel: the PCG solve (ba_k_pcg), S*p dominated
     peak, peak_kind = peaks()
-    bytes_per_cg = 136.0 * N + 72.0 * P + 128.0 * C          # SURVEY.md 8(d), S*p per CG iteration
+    bytes_per_cg = 136.0 * Nl + 72.0 * Pl + 128.0 * C        # SURVEY.md 8(d), S*p per CG iteration (this rank)
     roof = None
     if pms.value > 0 and cgit.value > 0:
         ach = bytes_per_cg * cgit.value / (pms.value / 1e3) / 1e9
@@ -256,7 +270,7 @@ def run_b200(args, ws, rank, local):
         t_a = time.perf_counter()
         e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e_a.record(stream)
-        p2 = b2.BAProblem(arr, loss)
+        p2 = make_problem()
         th_out, rep_e = b2.lm_solve(p2, theta_host, b2.LMConfig(max_iterations=args.warmup + args.steps))
         e_b.record(stream)
         barrier()
@@ -267,8 +281,8 @@ def run_b200(args, ws, rank, local):
             t = torch.tensor([wall], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             wall = float(t.item())
-        h2d = (N * (4 + 4 + 16) + C * (16 + 16 + 8) + theta_host.nbytes)
-        e2e = {"value": ws * N * its / wall, "unit": "obs/s",
+        h2d = (Nl * (4 + 4 + 16) + C * (16 + 16 + 8) + theta_host.nbytes)
+        e2e = {"value": N * its / wall, "unit": "obs/s",
                "h2d_bytes_per_step": int(h2d / its), "d2h_bytes_per_step": int(theta_host.nbytes / its),
                "iterations": its, "wall_s": round(wall, 3), "device_ms": round(e_ms, 1),
                "termination": rep_e.termination}
@@ -276,10 +290,11 @@ def run_b200(args, ws, rank, local):
     result = {
         "metric": METRIC, "value": value, "unit": "obs/s", "n_gpus": ws, "steps": steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": label, "cameras": C, "points": P, "observations": N,
                    "views_per_point": k, "loss": f"huber({delta})", "lm": "LMConfig() defaults",
-                   "parallelism": "replicas" if ws > 1 else "single",
+                   "parallelism": f"points sharded over {ws} GPUs" if ws > 1 else "single",
+                   "observations_per_rank": Nl,
                    "l2": "inputs larger than L2 (J 2x2.56 GB)" if N >= 10**6 else "small (latency bound)"},
         "cg_iters_per_step": [i.cg_iters for i in rep_t.iterations],
         "lm_ms_per_iteration": [round(i.device_ms, 3) for i in rep_t.iterations],
@@ -365,7 +380,7 @@ def run_reference(args, ws, rank):
               f"{len(its)} LM iterations, last {len(timed)} timed; total {wall:.1f} s")
     return {"metric": METRIC, "value": value, "unit": "obs/s", "n_gpus": ws, "steps": len(timed),
             "warmup": args.warmup, "ms_per_step": 1e3 * t_timed / len(timed), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": label, "sample_cameras": scams, "sample_points": spts,
                        "sample_observations": n},
             "impl": "reference",
@@ -384,6 +399,8 @@ def main():
     ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--same-device", action="store_true",
+                    help="N>1 ranks all on cuda:0 over gloo: plumbing check of the sharded path, not a measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup raised to 3 (timing rules)")

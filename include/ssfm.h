@@ -54,7 +54,7 @@ typedef enum {
   SSFM_DIMENSION_MISMATCH = 8,  /* errors.DimensionMismatch  (errors.py:16)  */
   SSFM_INVALID_ARGUMENT = 9,    /* ValueError / IndexError                    */
   SSFM_CUDA_ERROR = 10,
-  SSFM_NCCL_ERROR = 11
+  SSFM_COMM_ERROR = 11         /* peer exchange of a sharded handle failed / timed out */
 } ssfm_status;
 
 /* Termination reasons of SolveReport.termination (lm.py:61-83). */
@@ -188,6 +188,27 @@ int ssfm_export_pattern(ssfm_handle* h, int32_t* obs_pt_order,
 int ssfm_profile_get(const ssfm_handle* h, int32_t kind, double* ms,
                      int64_t* launches, double* bytes);
 int ssfm_profile_enable(ssfm_handle* h, int32_t on);
+
+/* ---- point-sharded multi-GPU solve -------------------
+ * Each rank creates its handle from ITS shard: every camera (replicated), a
+ * contiguous range of points renumbered from 0 and all observations of those
+ * points (theta = [7C poses | 3 P_local points | focals]). Camera-side sums
+ * and scalar reductions are exchanged through peer memory (csrc/comm.cuh);
+ * the camera half of S*p is exchanged inside the persistent PCG kernel every
+ * CG iteration. Replicated quantities are combined in rank order on every
+ * rank, so all ranks hold bitwise-identical camera parameters and take the
+ * same LM / CG decisions. After ssfm_comm_connect every call that computes
+ * (cost, linearize, solve_normal, lm_solve) is collective over the ranks.
+ *
+ * ssfm_comm_init: allocate this rank's exchange region; *ipc_handle_out (64
+ *   bytes, may be NULL) receives its cudaIpcMemHandle_t, *region_out (may be
+ *   NULL) its device pointer. nranks <= 16. BA handles only.
+ * ssfm_comm_connect: map the peers' regions, from IPC handles (nranks x 64
+ *   bytes, one process per GPU) or from raw device pointers (several handles
+ *   of one process on one device); entries for this rank are ignored. */
+int ssfm_comm_init(ssfm_handle* h, int32_t rank, int32_t nranks, void* ipc_handle_out,
+                   void** region_out);
+int ssfm_comm_connect(ssfm_handle* h, const void* ipc_handles, void* const* regions);
 
 /* Which Schur operator the PCG kernel of this handle runs (no reference
  * counterpart; it replaces the dense S@p of lm.py:656). *slot_groups = 0: the

@@ -249,18 +249,41 @@ __global__ void __launch_bounds__(SSFM_TILE) ba_k_camred(BADev d) {
 }
 
 // per camera: sum tile partials in tile order -> Bc (full 8x8), gcam
-__global__ void ba_k_camfin(BADev d, double* cam_norm_part) {
+// per camera: sum of its tile partials in tile order (the local part of a
+// camera block when the observations are sharded over ranks)
+__global__ void k_cam_tilesum(const Topo T, const double* __restrict__ tilebuf, int V, double* camsum) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= T.C) return;
+  for (int k = 0; k < V; ++k) {
+    double s = 0.0;
+    for (int t = T.cam_tile[c]; t < T.cam_tile[c + 1]; ++t) s += tilebuf[(long long)V * t + k];
+    camsum[(long long)V * c + k] = s;
+  }
+}
+
+// camsum != nullptr: per-camera sums already reduced over ranks (k_cam_tilesum
+// + allreduce); otherwise the local tiles are summed here.
+__device__ __forceinline__ void cam_sums(const BADev& d, int c, const double* camsum, double* s) {
+  if (camsum) {
+#pragma unroll
+    for (int k = 0; k < CAM_V; ++k) s[k] = camsum[(long long)CAM_V * c + k];
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < CAM_V; ++k) s[k] = 0.0;
+  for (int t = d.topo.cam_tile[c]; t < d.topo.cam_tile[c + 1]; ++t) {
+    const double* src = d.tilebuf + (long long)CAM_V * t;
+#pragma unroll
+    for (int k = 0; k < CAM_V; ++k) s[k] += src[k];
+  }
+}
+
+__global__ void ba_k_camfin(BADev d, double* cam_norm_part, const double* camsum) {
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   double gn2 = 0.0, gmax = 0.0;
   if (c < d.bp.C) {
     double s[CAM_V];
-#pragma unroll
-    for (int k = 0; k < CAM_V; ++k) s[k] = 0.0;
-    for (int t = d.topo.cam_tile[c]; t < d.topo.cam_tile[c + 1]; ++t) {
-      const double* src = d.tilebuf + (long long)CAM_V * t;
-#pragma unroll
-      for (int k = 0; k < CAM_V; ++k) s[k] += src[k];
-    }
+    cam_sums(d, c, camsum, s);
     double* B = d.Bc + 64ll * c;
     int idx = 0;
 #pragma unroll
@@ -432,17 +455,11 @@ __device__ bool gj_inverse(double* a, double* inv, int n, int lda) {
 // per camera: S_cc = B_c(damped) - sum E Cinv E^T, b_red = b_c - sum E y0,
 // pinning (lm.py:628-635), block-Jacobi factors for the 7x7 pose block and the
 // 1x1 focal block separately (lm.py:473-483, 516-527).
-__global__ void ba_k_camprec(BADev d, double lam) {
+__global__ void ba_k_camprec(BADev d, double lam, const double* camsum) {
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= d.bp.C) return;
   double s[CAM_V];
-#pragma unroll
-  for (int k = 0; k < CAM_V; ++k) s[k] = 0.0;
-  for (int t = d.topo.cam_tile[c]; t < d.topo.cam_tile[c + 1]; ++t) {
-    const double* src = d.tilebuf + (long long)CAM_V * t;
-#pragma unroll
-    for (int k = 0; k < CAM_V; ++k) s[k] += src[k];
-  }
+  cam_sums(d, c, camsum, s);
   const double* B = d.Bc + 64ll * c;
   double S[64];
   int idx = 0;

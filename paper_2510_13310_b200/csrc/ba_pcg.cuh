@@ -15,6 +15,7 @@
 #include <cooperative_groups.h>
 #include "ba_kernels.cuh"
 #include "fused.cuh"
+#include "comm.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -290,8 +291,8 @@ __device__ __forceinline__ void ba_fused_pass(const BADev& d, const FusedTopo& f
 // 8/SL slot groups (fused.cuh); needs SL*C doubles of dynamic shared memory.
 template <int SL>
 __global__ void __launch_bounds__(SL ? FZ_THREADS : PCG_THREADS, SL ? 1 : 4)
-ba_k_pcg(BADev d, FusedTopo fz, double lam, int max_iters, double cg_tol, double* x, double* r,
-         double* z, double* p, double* q, double* part, CGCtl* ctl) {
+ba_k_pcg(BADev d, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg_tol, double* x,
+         double* r, double* z, double* p, double* q, double* part, CGCtl* ctl) {
   constexpr int NT = SL ? FZ_THREADS : PCG_THREADS;
   cg::grid_group grid = cg::this_grid();
   __shared__ double smp[NT / 32][SSFM_BATCH][3];
@@ -306,6 +307,19 @@ ba_k_pcg(BADev d, FusedTopo fz, double lam, int max_iters, double cg_tol, double
   double* tile8 = d.tilebuf;
   const int NP = gridDim.x;
   const int ngrp = SL ? gridDim.x / (8 / (SL ? SL : 8)) : 0;
+  // local camera half of S*p for slot s = 8c + k (tile or group partials in order)
+  auto local_cam = [&](int s) -> double {
+    double a = 0.0;
+    if constexpr (SL == 0) {
+      const int c = s >> 3, k = s & 7;
+      const int t0 = d.topo.cam_tile[c], t1 = d.topo.cam_tile[c + 1];
+      for (int t = t0; t < t1; ++t) a += tile8[8ll * t + k];
+    } else {
+      for (int gq = 0; gq < ngrp; ++gq) a += fz.gpart[(long long)gq * S + s];
+    }
+    return a;
+  };
+  unsigned long long ep = cm.nranks > 1 ? *cm.epoch : 0ull;
 
   // ---- init: x = 0, r = b_red, z = M r, p = z
   {
@@ -350,6 +364,16 @@ ba_k_pcg(BADev d, FusedTopo fz, double lam, int max_iters, double cg_tol, double
         ba_fused_pass<SL>(d, fz, p, dyn_acc, smp, smy, smown);
       }
       grid.sync();
+      // P2x (sharded): exchange the local camera half of S*p with the peer
+      // ranks inside the kernel (comm.cuh); P3 then sums the ranks in order.
+      if (cm.nranks > 1) {
+        ++ep;
+        double* mine = cm.buf[cm.rank] + (long long)(ep & 1) * cm.cap;
+        for (int s = gid; s < S; s += stride) mine[s] = local_cam(s);
+        grid.sync();
+        if (blockIdx.x == 0 && threadIdx.x == 0) comm_signal_wait(cm, ep);
+        grid.sync();
+      }
       // P3: q = S p per slot, p.q partials
       {
         double v[1] = {0.0};
@@ -366,12 +390,13 @@ ba_k_pcg(BADev d, FusedTopo fz, double lam, int max_iters, double cg_tol, double
             if (ok) bp += d.Bc[64ll * c + 8 * k + m] * pm;
           }
           if (ok) {
-            double acc = 0.0;
-            if constexpr (SL == 0) {
-              const int t0 = d.topo.cam_tile[c], t1 = d.topo.cam_tile[c + 1];
-              for (int t = t0; t < t1; ++t) acc += tile8[8ll * t + k];
+            double acc;
+            if (cm.nranks > 1) {
+              const long long off = (long long)(ep & 1) * cm.cap + s;
+              acc = comm_peer_load(cm.buf[0] + off);
+              for (int rk = 1; rk < cm.nranks; ++rk) acc += comm_peer_load(cm.buf[rk] + off);
             } else {
-              for (int gq = 0; gq < ngrp; ++gq) acc += fz.gpart[(long long)gq * S + s];
+              acc = local_cam(s);
             }
             double qk = bp + lam * d.Bc[64ll * c + 9 * k] * pk - acc;
             if ((d.pinned[c] >> k) & 1) qk = pk;
@@ -427,6 +452,7 @@ ba_k_pcg(BADev d, FusedTopo fz, double lam, int max_iters, double cg_tol, double
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (cm.nranks > 1) *cm.epoch = ep;
     ctl->tol = tol;
     ctl->rho = rho;
     ctl->rn = rn;

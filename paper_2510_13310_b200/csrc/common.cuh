@@ -26,6 +26,7 @@ enum : int {
   ST_PIN_SCALE = 1 << 7,          // lm.py:569-575
   ST_BAD_INDEX = 1 << 8,
   ST_SCHEDULE = 1 << 9,           // fused-operator ticket schedule violated (internal error)
+  ST_COMM_TIMEOUT = 1 << 10,      // a peer rank did not reach the exchange (comm.cuh)
 };
 
 __device__ __forceinline__ double shfl_xor_d(double v, int m) {

@@ -53,6 +53,7 @@ struct ssfm_handle {
   int kind = 0;   // 0 BA, 1 GP
   int device = 0;
   int num_sms = 148;
+  int pcg_sms = 148;            // SMs the persistent PCG grid may occupy (SSFM_PCG_SMS)
   std::vector<void*> allocs;
   size_t bytes = 0;
   long long total_params = 0, total_res = 0;
@@ -72,6 +73,13 @@ struct ssfm_handle {
   size_t pcg_smem = 0;
   void* pcg_fn = nullptr;
   FusedTopo fz{};
+  // point sharding (comm.cuh)
+  CommDev cm{};
+  void* region = nullptr;
+  std::vector<void*> ipc_opened;
+  double* camsum = nullptr;     // [CAM_V * C] per-camera sums exchanged between ranks
+  double* ar_tmp = nullptr;     // [16] scalar scratch
+  int comm_nranks = 1;
   int lin_blocks = 0;
   int cost_blocks = 0;
   int cam_blocks = 0;
@@ -104,7 +112,9 @@ static inline int nblk(long long n, int t) { return (int)((n + t - 1) / t); }
 
 static void free_handle(ssfm_handle* h) {
   if (!h) return;
+  for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void* p : h->allocs) cudaFree(p);
+  if (h->region) cudaFree(h->region);
   if (h->hmisc) cudaFreeHost(h->hmisc);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
@@ -235,7 +245,7 @@ static int try_fused_ba(ssfm_handle* h, int* ok) {
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ba_k_pcg<SL>, FZ_THREADS, dyn));
   if (occ < 1) return SSFM_OK;
   const int G = 8 / SL;
-  int grid = occ * h->num_sms;
+  int grid = occ * h->pcg_sms;
   grid -= grid % G;
   if (grid < G) return SSFM_OK;
   h->pcg_grid = grid;
@@ -251,6 +261,13 @@ static int try_fused_ba(ssfm_handle* h, int* ok) {
 
 static int setup_ba_pcg(ssfm_handle* h, cudaStream_t st) {
   const Topo& T = h->topo;
+  // SSFM_PCG_SMS caps the SMs of the persistent PCG grid (several sharded
+  // handles on one device must be co-resident: their kernels wait on each other)
+  h->pcg_sms = h->num_sms;
+  if (const char* e = getenv("SSFM_PCG_SMS")) {
+    const int v = atoi(e);
+    if (v > 0 && v < h->num_sms) h->pcg_sms = v;
+  }
   const int C = h->ba.bp.C;
   const char* env = getenv("SSFM_FUSED");
   const bool want = !(env && env[0] == '0') && C < FZ_MAX_CAMERAS;
@@ -309,7 +326,7 @@ static int setup_ba_pcg(ssfm_handle* h, cudaStream_t st) {
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ba_k_pcg<0>, PCG_THREADS, 0) || occ < 1)
     return set_err(SSFM_CUDA_ERROR, "occupancy query for the PCG kernel failed");
-  h->pcg_grid = occ * h->num_sms;
+  h->pcg_grid = occ * h->pcg_sms;
   h->pcg_threads = PCG_THREADS;
   h->pcg_smem = 0;
   h->pcg_fn = (void*)ba_k_pcg<0>;
@@ -600,6 +617,34 @@ static int export_keys(ssfm_handle* h, int32_t* off_keys, int64_t off_cap, int64
 // ---------------------------------------------------------------------------
 static void count_launch(ssfm_handle* h, int n = 1) { h->prof.kernel_launches += n; }
 
+static bool sharded(const ssfm_handle* h) { return h->cm.nranks > 1; }
+
+// peer-memory allreduce of n doubles in place (comm.cuh), stream-ordered
+static int allreduce(ssfm_handle* h, double* data, long long n, int op, cudaStream_t st) {
+  if (!sharded(h) || n <= 0) return SSFM_OK;
+  if (n > h->cm.cap) return set_err(SSFM_INVALID_ARGUMENT, "allreduce larger than the exchange buffer");
+  const int blocks = std::max(1, std::min(nblk(n, 256), h->num_sms));
+  k_ar_post<<<blocks, 256, 0, st>>>(h->cm, data, n);
+  k_ar_barrier<<<1, 32, 0, st>>>(h->cm);
+  k_ar_reduce<<<blocks, 256, 0, st>>>(h->cm, data, n, op);
+  count_launch(h, 3);
+  CU(cudaGetLastError());
+  return SSFM_OK;
+}
+
+// OR of the device status words over ranks (rejections must agree everywhere)
+static int sync_status(ssfm_handle* h, cudaStream_t st) {
+  if (!sharded(h)) return SSFM_OK;
+  k_status_to_double<<<1, 1, 0, st>>>(&h->misc->status, h->ar_tmp);
+  int rc = allreduce(h, h->ar_tmp, 1, AR_OR, st);
+  if (rc) return rc;
+  k_double_to_status<<<1, 1, 0, st>>>(h->ar_tmp, &h->misc->status);
+  count_launch(h, 2);
+  return SSFM_OK;
+}
+
+__global__ void k_add2(const double* a, const double* b, double* out) { *out = *a + *b; }
+
 // cost(theta) -> misc.scal[SC_COST] (async)
 static int launch_cost(ssfm_handle* h, const double* theta, cudaStream_t st) {
   if (h->kind == 0) {
@@ -608,6 +653,8 @@ static int launch_cost(ssfm_handle* h, const double* theta, cudaStream_t st) {
     ba_k_cost<<<h->cost_blocks, 256, 0, st>>>(d, theta, h->red);
     k_sum_partials<<<1, 1024, 0, st>>>(h->red, h->cost_blocks, d.scal + SC_COST);
     count_launch(h, 3);
+    int rc = allreduce(h, d.scal + SC_COST, 1, AR_SUM, st);
+    if (rc) return rc;
   } else {
     GPDev& g = h->gp;
     gp_k_cost<<<h->cost_blocks, 256, 0, st>>>(g, theta, h->red);
@@ -627,9 +674,24 @@ static int launch_linearize(ssfm_handle* h, const double* theta, double* r_out, 
     ba_k_prep<<<h->cam_blocks, 256, 0, st>>>(d, theta);
     ba_k_linearize<<<h->lin_blocks, 256, 0, st>>>(d, theta, r_out, J_out, h->red);
     if (d.topo.nt) ba_k_camred<<<d.topo.nt, SSFM_TILE, 0, st>>>(d);
-    ba_k_camfin<<<h->cam_blocks, 256, 0, st>>>(d, h->red + (long long)h->lin_blocks * 8);
-    k_sum_partials<<<1, 1024, 0, st>>>(h->red, h->lin_blocks * 8 + h->cam_blocks, d.scal + SC_GNORM2);
-    count_launch(h, 5);
+    if (!sharded(h)) {
+      ba_k_camfin<<<h->cam_blocks, 256, 0, st>>>(d, h->red + (long long)h->lin_blocks * 8, nullptr);
+      k_sum_partials<<<1, 1024, 0, st>>>(h->red, h->lin_blocks * 8 + h->cam_blocks, d.scal + SC_GNORM2);
+      count_launch(h, 5);
+    } else {
+      // camera blocks: local tile sums -> exchange -> identical Bc / gcam on every rank;
+      // |g|^2 = sum over ranks of the point part + the (replicated) camera part
+      k_cam_tilesum<<<h->cam_blocks, 256, 0, st>>>(d.topo, d.tilebuf, CAM_V, h->camsum);
+      int rc = allreduce(h, h->camsum, (long long)CAM_V * d.bp.C, AR_SUM, st);
+      if (rc) return rc;
+      ba_k_camfin<<<h->cam_blocks, 256, 0, st>>>(d, h->red + (long long)h->lin_blocks * 8, h->camsum);
+      k_sum_partials<<<1, 1024, 0, st>>>(h->red, h->lin_blocks * 8, h->ar_tmp + 1);
+      if ((rc = allreduce(h, h->ar_tmp + 1, 1, AR_SUM, st))) return rc;
+      k_sum_partials<<<1, 1024, 0, st>>>(h->red + (long long)h->lin_blocks * 8, h->cam_blocks, h->ar_tmp + 2);
+      k_add2<<<1, 1, 0, st>>>(h->ar_tmp + 1, h->ar_tmp + 2, d.scal + SC_GNORM2);
+      if ((rc = allreduce(h, d.scal + SC_GMAX, 1, AR_MAX, st))) return rc;
+      count_launch(h, 8);
+    }
   } else {
     int rc = gp_launch_linearize(h->gp, theta, r_out, J_out, h->red, h->lin_blocks, h->cam_blocks, st);
     if (rc) return set_err(SSFM_CUDA_ERROR, "gp linearize launch");
@@ -646,11 +708,11 @@ static int launch_pcg(ssfm_handle* h, double lam, const ssfm_lm_config* cfg, cud
   void* args[11];
   if (h->kind == 0) {
     BADev& d = h->ba;
-    void* a[12];
+    void* a[13];
     CGCtl* ctl = &h->misc->ctl;
-    a[0] = &d; a[1] = &h->fz; a[2] = &lam; a[3] = &max_it; a[4] = &tol;
-    a[5] = &h->x; a[6] = &h->r; a[7] = &h->z; a[8] = &h->p; a[9] = &h->q;
-    a[10] = &h->part; a[11] = &ctl;
+    a[0] = &d; a[1] = &h->fz; a[2] = &h->cm; a[3] = &lam; a[4] = &max_it; a[5] = &tol;
+    a[6] = &h->x; a[7] = &h->r; a[8] = &h->z; a[9] = &h->p; a[10] = &h->q;
+    a[11] = &h->part; a[12] = &ctl;
     CU(cudaLaunchCooperativeKernel(h->pcg_fn, dim3(h->pcg_grid), dim3(h->pcg_threads), a, h->pcg_smem, st));
   } else {
     GPDev& g = h->gp;
@@ -673,7 +735,15 @@ static int launch_solve(ssfm_handle* h, double lam, const ssfm_lm_config* cfg, c
     BADev& d = h->ba;
     ba_k_ptinv<<<nblk(d.bp.P, 256), 256, 0, st>>>(d, lam);
     if (d.topo.nt) ba_k_precond<<<d.topo.nt, SSFM_TILE, 0, st>>>(d);
-    ba_k_camprec<<<nblk(d.bp.C, 64), 64, 0, st>>>(d, lam);
+    const double* cs = nullptr;
+    if (sharded(h)) {
+      k_cam_tilesum<<<h->cam_blocks, 256, 0, st>>>(d.topo, d.tilebuf, CAM_V, h->camsum);
+      int rc = allreduce(h, h->camsum, (long long)CAM_V * d.bp.C, AR_SUM, st);
+      if (rc) return rc;
+      cs = h->camsum;
+      count_launch(h);
+    }
+    ba_k_camprec<<<nblk(d.bp.C, 64), 64, 0, st>>>(d, lam, cs);
     count_launch(h, 3);
   } else {
     int rc = gp_launch_elim(h->gp, lam, h->cam_blocks, st);
@@ -721,6 +791,7 @@ static int status_to_code(int s) {
     return SSFM_SINGULAR_BLOCK;
   if (s & (ST_CG_MAXITER | ST_CG_BREAKDOWN)) return SSFM_CG_STALL;
   if (s & ST_ZERO_QUAT) return SSFM_ZERO_QUATERNION;
+  if (s & (ST_COMM_TIMEOUT | ST_SCHEDULE)) return SSFM_COMM_ERROR;
   return SSFM_OK;
 }
 
@@ -738,6 +809,8 @@ static std::string status_msg(int s, const Misc& m) {
   }
   if (s & ST_CG_BREAKDOWN) return "CG broke down (p.q <= 0)";
   if (s & ST_ZERO_QUAT) return "quaternion norm below 1e-12 during renormalization";
+  if (s & ST_COMM_TIMEOUT) return "a peer rank did not reach the exchange within 60 s";
+  if (s & ST_SCHEDULE) return "fused operator schedule violated (internal error)";
   return "ok";
 }
 
@@ -804,6 +877,7 @@ extern "C" int ssfm_solve_normal(ssfm_handle* h, double lambda, const ssfm_lm_co
   int rc = launch_solve(h, lambda, cfg, st);
   if (rc) return rc;
   if (delta) CU(cudaMemcpyAsync(delta, h->delta, sizeof(double) * h->total_params, cudaMemcpyDeviceToDevice, st));
+  if ((rc = sync_status(h, st))) return rc;
   if ((rc = read_misc(h, st))) return rc;
   const Misc& m = *h->hmisc;
   if (cg_iters_host) *cg_iters_host = m.ctl.iters;
@@ -863,6 +937,7 @@ extern "C" int ssfm_lm_solve(ssfm_handle* h, double* theta_io, const ssfm_lm_con
     count_launch(h);
     if ((rc = launch_post_step(h, h->cand, st))) return rc;
     if ((rc = launch_cost(h, h->cand, st))) return rc;
+    if ((rc = sync_status(h, st))) return rc;
     CU(cudaEventRecord(h->ev1, st));
     if ((rc = read_misc(h, st))) return rc;
     const Misc m = *h->hmisc;
@@ -947,6 +1022,67 @@ extern "C" int ssfm_profile_get(const ssfm_handle* h, int32_t kind, double* ms, 
     if (launches) *launches = p.kernel_launches;
     if (bytes) *bytes = 0;
   }
+  return SSFM_OK;
+}
+
+extern "C" int ssfm_comm_init(ssfm_handle* h, int32_t rank, int32_t nranks, void* ipc_handle_out,
+                              void** region_out) {
+  if (!h) return set_err(SSFM_INVALID_ARGUMENT, "null argument");
+  if (h->kind != 0) return set_err(SSFM_INVALID_ARGUMENT, "point sharding: BA handles only in this build");
+  if (nranks < 1 || nranks > SSFM_MAX_RANKS || rank < 0 || rank >= nranks)
+    return set_err(SSFM_INVALID_ARGUMENT, "bad rank / nranks");
+  if (h->region) return set_err(SSFM_INVALID_ARGUMENT, "exchange region already initialised");
+  const int C = h->topo.C;
+  const long long cap = (long long)std::max(CAM_V, 8) * C + 64;
+  const size_t bytes = 256 + sizeof(double) * 2 * (size_t)cap;
+  CU(cudaMalloc(&h->region, bytes));
+  CU(cudaMemset(h->region, 0, bytes));
+  DALLOC(h->cm.epoch, 1);
+  CU(cudaMemset(h->cm.epoch, 0, sizeof(unsigned long long)));
+  DALLOC(h->camsum, (long long)CAM_V * C);
+  DALLOC(h->ar_tmp, 16);
+  CU(cudaDeviceSynchronize());
+  CommDev& cm = h->cm;
+  cm.rank = rank;
+  cm.cap = cap;
+  cm.flag[rank] = static_cast<unsigned long long*>(h->region);
+  cm.buf[rank] = reinterpret_cast<double*>(static_cast<char*>(h->region) + 256);
+  cm.status = &h->misc->status;
+  cm.nranks = 1;   // becomes nranks on connect
+  h->comm_nranks = nranks;
+  if (ipc_handle_out) {
+    cudaIpcMemHandle_t ih;
+    CU(cudaIpcGetMemHandle(&ih, h->region));
+    memcpy(ipc_handle_out, &ih, sizeof(ih));
+  }
+  if (region_out) *region_out = h->region;
+  return SSFM_OK;
+}
+
+extern "C" int ssfm_comm_connect(ssfm_handle* h, const void* ipc_handles, void* const* regions) {
+  if (!h || !h->region) return set_err(SSFM_INVALID_ARGUMENT, "ssfm_comm_connect before ssfm_comm_init");
+  if (!ipc_handles && !regions) return set_err(SSFM_INVALID_ARGUMENT, "need IPC handles or region pointers");
+  CommDev& cm = h->cm;
+  const int R = h->comm_nranks;
+  for (int r = 0; r < R; ++r) {
+    if (r == cm.rank) continue;
+    void* ptr = nullptr;
+    if (regions && regions[r]) {
+      ptr = regions[r];
+    } else if (ipc_handles) {
+      cudaIpcMemHandle_t ih;
+      memcpy(&ih, static_cast<const char*>(ipc_handles) + sizeof(ih) * r, sizeof(ih));
+      cudaError_t e = cudaIpcOpenMemHandle(&ptr, ih, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess)
+        return set_err(SSFM_COMM_ERROR, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+      h->ipc_opened.push_back(ptr);
+    } else {
+      return set_err(SSFM_INVALID_ARGUMENT, "missing peer region");
+    }
+    cm.flag[r] = static_cast<unsigned long long*>(ptr);
+    cm.buf[r] = reinterpret_cast<double*>(static_cast<char*>(ptr) + 256);
+  }
+  cm.nranks = R;
   return SSFM_OK;
 }
 

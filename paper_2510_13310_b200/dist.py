@@ -1,0 +1,189 @@
+"""Point-sharded multi-GPU bundle adjustment.
+
+One process per GPU (torchrun), or several handles in one process on one
+device (tests). The observations are sharded by point ownership:
+
+* points are split into `world` contiguous ranges balanced by observation
+  count (`shard_ranges`); rank r owns its points and every observation of
+  them, so point elimination, point back-substitution and the point half of
+  the gradient are local;
+* camera parameters (poses, focals) and the camera-space PCG vectors are
+  replicated; the camera-side sums (J^T J camera blocks, J^T r, Schur
+  preconditioner blocks and, every CG iteration, the camera half of S*p) and
+  the scalar reductions (cost, |g|^2, max|g|, status) are exchanged through
+  peer memory by the native library (csrc/comm.cuh) -- in-kernel for S*p.
+
+Replicated values are combined in rank order on every rank, so every rank
+holds bitwise-identical camera parameters and takes the same LM decisions;
+the LM report is identical on all ranks. Results differ from a single-GPU
+solve only by summation order (bitwise stable per GPU count).
+
+The reference (sparsesfm) has no multi-GPU path; this module extends its
+`BAProblem` / `lm_solve` API (ba.py:35-36, lm.py:727-728) without changing it:
+a `ShardedBAProblem` is a `BAProblem` over the rank's shard, `lm_solve` is
+called on every rank with the rank's local theta.
+"""
+
+from __future__ import annotations
+
+import ctypes as ct
+
+import numpy as np
+
+from . import _native
+from .ba import BAProblem
+from .scene import SceneArrays, as_arrays
+
+
+def shard_ranges(pt_idx, num_points: int, world: int):
+    """Contiguous point ranges [(p0, p1)] per rank, balanced by observation
+    count: rank r ends at the first point whose prefix observation count
+    reaches r+1 / world of the total. Deterministic, empty ranges allowed."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    counts = np.bincount(np.asarray(pt_idx, dtype=np.int64), minlength=num_points)
+    csum = np.concatenate([[0], np.cumsum(counts)])
+    total = int(csum[-1])
+    bounds = [0]
+    for r in range(1, world):
+        target = (r * total) // world
+        p = int(np.searchsorted(csum, target, side="left"))
+        bounds.append(min(max(p, bounds[-1]), num_points))
+    bounds.append(num_points)
+    return [(bounds[r], bounds[r + 1]) for r in range(world)]
+
+
+def shard_arrays(arr: SceneArrays, rank: int, world: int):
+    """(local SceneArrays, (p0, p1), observation indices) of one rank: every
+    camera, points [p0, p1) renumbered from 0, their observations in the
+    original observation order."""
+    p0, p1 = shard_ranges(arr.pt_idx, arr.num_points, world)[rank]
+    pt = np.asarray(arr.pt_idx, dtype=np.int64)
+    obs = np.nonzero((pt >= p0) & (pt < p1))[0]
+    local = SceneArrays(arr.quats, arr.centers, arr.focals, arr.pps, arr.dists, arr.model_tag,
+                        arr.points[p0:p1], np.asarray(arr.cam_idx)[obs], pt[obs] - p0,
+                        arr.pixels[obs], None if arr.depths is None else arr.depths[obs])
+    return local, (p0, p1), obs
+
+
+class ShardedBAProblem(BAProblem):
+    """BAProblem over this rank's point shard (see module docstring).
+
+    comm="torch": ranks are torch.distributed ranks (one process per GPU);
+    the exchange regions are connected on first use via CUDA IPC handles
+    all-gathered over `group`. comm="local": several shards in one process
+    on one device; call `connect_local(problems)` before solving.
+    Every computing call (cost, linearize, lm_solve) is collective.
+    """
+
+    def __init__(self, scene, loss=None, optimize_focal: bool = True, shared_focal: bool = False,
+                 rank: int | None = None, world: int | None = None, group=None, comm: str = "torch"):
+        arr = as_arrays(scene)
+        if rank is None or world is None:
+            import torch.distributed as dist
+            rank, world = dist.get_rank(group), dist.get_world_size(group)
+        if shared_focal and optimize_focal:
+            raise ValueError("shared_focal is not supported by the sharded solver")
+        local, (p0, p1), obs = shard_arrays(arr, rank, world)
+        if local.num_observations == 0:
+            raise ValueError(f"rank {rank} owns no observations (world {world} too large for this scene)")
+        super().__init__(local, loss, optimize_focal, shared_focal)
+        self.global_arr = arr
+        self.rank, self.world, self.group, self.comm = rank, world, group, comm
+        self.point_range = (p0, p1)
+        self.obs_index = obs
+        self._connected = world == 1
+
+    def _create(self):
+        h = super()._create()
+        self._native_ptr = h
+        if self.world > 1 and self.comm == "torch":
+            import torch.distributed as dist
+            lib = _native.load()
+            ih = (ct.c_char * 64)()
+            _native.check(lib.ssfm_comm_init(ct.c_void_p(h.ptr), self.rank, self.world, ih, None))
+            handles = [None] * self.world
+            dist.all_gather_object(handles, bytes(ih), group=self.group)
+            blob = b"".join(handles)
+            _native.check(lib.ssfm_comm_connect(ct.c_void_p(h.ptr), ct.c_char_p(blob), None))
+            self._connected = True
+        return h
+
+    def _native_handle(self):
+        h = super()._native_handle()
+        if not self._connected:
+            raise RuntimeError("sharded problem not connected: call connect_local(problems) first")
+        return h
+
+    # -- theta between the global layout and this rank's shard ---------------
+    def scatter_theta(self, theta_global) -> np.ndarray:
+        """This rank's local theta [7C | 3 P_local | focals] from a global one."""
+        th = np.asarray(theta_global, dtype=np.float64)
+        c, P = self.num_cameras, self.global_arr.num_points
+        p0, p1 = self.point_range
+        parts = [th[:7 * c], th[7 * c + 3 * p0:7 * c + 3 * p1]]
+        if self.optimize_focal:
+            parts.append(th[7 * c + 3 * P:])
+        return np.concatenate(parts)
+
+    def gather_theta(self, theta_local, shards=None) -> np.ndarray:
+        """Global theta from every rank's local theta (collective for
+        comm="torch"; for comm="local" pass `shards` = [(problem, theta)])."""
+        if not isinstance(theta_local, np.ndarray):
+            theta_local = theta_local.detach().cpu().numpy()
+        c = self.num_cameras
+        if shards is None:
+            if self.world == 1:
+                shards_pts = [theta_local[7 * c:7 * c + 3 * self.num_points]]
+            else:
+                import torch.distributed as dist
+                mine = theta_local[7 * c:7 * c + 3 * self.num_points]
+                shards_pts = [None] * self.world
+                dist.all_gather_object(shards_pts, mine, group=self.group)
+        else:
+            shards_pts = []
+            for p, th in sorted(shards, key=lambda s: s[0].rank):
+                th = th if isinstance(th, np.ndarray) else th.detach().cpu().numpy()
+                shards_pts.append(th[7 * c:7 * c + 3 * p.num_points])
+        parts = [theta_local[:7 * c], *shards_pts]
+        if self.optimize_focal:
+            parts.append(theta_local[7 * c + 3 * self.num_points:])
+        return np.concatenate(parts)
+
+    def encode_global(self) -> np.ndarray:
+        return BAProblem(self.global_arr, self.loss, self.optimize_focal, self.shared_focal).encode()
+
+
+def connect_local(problems) -> None:
+    """Connect several ShardedBAProblem (ranks 0..R-1 of one scene) living in
+    this process on the current device: exchange regions are plain device
+    pointers. Their collective calls must then run concurrently (one host
+    thread per problem) and their PCG grids must fit the device together
+    (set SSFM_PCG_SMS before the handles are created)."""
+    lib = _native.load()
+    world = len(problems)
+    regions = (ct.c_void_p * world)()
+    for p in problems:
+        if p.world != world or p.comm != "local":
+            raise ValueError("connect_local needs comm='local' problems of one world")
+        h = BAProblem._native_handle(p)
+        reg = ct.c_void_p(0)
+        _native.check(lib.ssfm_comm_init(ct.c_void_p(h.ptr), p.rank, world, None, ct.byref(reg)))
+        regions[p.rank] = reg.value
+    for p in problems:
+        h = BAProblem._native_handle(p)
+        _native.check(lib.ssfm_comm_connect(ct.c_void_p(h.ptr), None, regions))
+        p._connected = True
+
+
+def run_ba_sharded(scene, loss=None, config=None, optimize_focal: bool = True, group=None):
+    """run_ba (ba.py:264-271) over the torch.distributed ranks: every rank
+    returns the full solved scene (decoded from the gathered theta) and the
+    (identical) SolveReport."""
+    from .lm import lm_solve
+    prob = ShardedBAProblem(scene, loss, optimize_focal, group=group)
+    th0 = prob.encode()
+    th, rep = lm_solve(prob, th0, config)
+    full = prob.gather_theta(th)
+    g = BAProblem(prob.global_arr, prob.loss, optimize_focal)
+    return g.decode(full), rep

@@ -1,0 +1,147 @@
+"""GPU: the point-sharded solver (paper_2510_13310_b200.dist, csrc/comm.cuh).
+
+Only one GPU is available to the tests, so the shards of one scene run as
+several handles on cuda:0:
+* in one process (comm="local": exchange regions are device pointers; one
+  host thread and one stream per shard, PCG grids capped with SSFM_PCG_SMS so
+  the persistent kernels of all shards are co-resident);
+* in two processes (comm="torch": gloo process group, CUDA IPC handles,
+  exactly the one-process-per-GPU code path minus NVLink).
+
+Checks: all shards report bitwise-identical LM trajectories and camera
+parameters (replicated values are combined in rank order on every rank);
+the sharded solve follows the single-GPU solve (same accept sequence, costs
+within 1e-7 relative: only the summation order differs, so
+each damped step agrees with the single-GPU one to the CG tolerance 1e-8 and
+the cost after it to about that, relative).
+"""
+import os
+import subprocess
+import sys
+import threading
+
+import numpy as np
+import pytest
+
+import paper_2510_13310_b200 as b2
+from paper_2510_13310_b200 import dist as bd
+from paper_2510_13310_b200 import synth
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def scene(cams=40, pts=3000, k=5, seed=0):
+    _, obs = synth.generate_arrays(synth.SynthConfig(num_cameras=cams, num_points=pts, visibility_fraction=k / cams,
+                                                     pixel_noise_sigma=1.0, seed=seed))
+    return synth.perturb_arrays(obs, rot_deg=1.0, center_frac=0.01, focal_frac=0.02, point_frac=0.005, seed=1)
+
+
+def solve_local_shards(gpu, st, world, cfg, fused="1"):
+    os.environ["SSFM_PCG_SMS"] = str(140 // world)
+    os.environ["SSFM_FUSED"] = fused
+    try:
+        probs = [bd.ShardedBAProblem(st, b2.RobustLoss("huber", 1.0), rank=r, world=world, comm="local")
+                 for r in range(world)]
+        bd.connect_local(probs)
+    finally:
+        os.environ.pop("SSFM_PCG_SMS")
+        os.environ.pop("SSFM_FUSED")
+    out = [None] * world
+    errs = []
+
+    def work(r):
+        try:
+            with gpu.cuda.stream(gpu.cuda.Stream()):
+                p = probs[r]
+                out[r] = b2.lm_solve(p, p.encode(), cfg)
+        except Exception as e:   # noqa: BLE001
+            errs.append(e)
+
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=300)
+    assert not errs, errs
+    return probs, out
+
+
+@pytest.mark.parametrize("world,fused", [(2, "1"), (3, "1"), (2, "0")])
+def test_local_shards_match_single_gpu(gpu, world, fused):
+    st = scene()
+    cfg = b2.LMConfig(max_iterations=15)
+    os.environ["SSFM_FUSED"] = fused          # the same operator as the shards
+    try:
+        single = b2.BAProblem(st, b2.RobustLoss("huber", 1.0))
+        single._native_handle()
+    finally:
+        os.environ.pop("SSFM_FUSED")
+    th1, rep1 = b2.lm_solve(single, single.encode(), cfg)
+    probs, out = solve_local_shards(gpu, st, world, cfg, fused)
+    reps = [o[1] for o in out]
+    # identical on every shard (bitwise)
+    for rep in reps[1:]:
+        assert [(i.cost_after, i.step_accepted, i.cg_iters, i.lam) for i in rep.iterations] == \
+               [(i.cost_after, i.step_accepted, i.cg_iters, i.lam) for i in reps[0].iterations]
+    cams = [o[0][:7 * st.num_cameras] for o in out]
+    for c in cams[1:]:
+        assert np.array_equal(c, cams[0])
+    # follows the single-GPU solve
+    assert [i.step_accepted for i in reps[0].iterations] == [i.step_accepted for i in rep1.iterations]
+    for a, b in zip(reps[0].iterations, rep1.iterations):
+        assert a.cost_after == pytest.approx(b.cost_after, rel=1e-7)
+    full = probs[0].gather_theta(out[0][0], shards=[(p, o[0]) for p, o in zip(probs, out)])
+    assert full.shape == th1.shape
+    assert np.abs(full - th1).max() <= 1e-6 * max(1.0, np.abs(th1).max())
+
+
+def test_sharded_cost_and_gradient_are_global(gpu):
+    st = scene(cams=12, pts=400, k=4, seed=3)
+    single = b2.BAProblem(st, b2.RobustLoss("huber", 1.0))
+    th = single.encode()
+    c1 = single.cost(th)
+    g1 = single.gradient(th)
+    os.environ["SSFM_PCG_SMS"] = "64"
+    try:
+        probs = [bd.ShardedBAProblem(st, b2.RobustLoss("huber", 1.0), rank=r, world=2, comm="local") for r in range(2)]
+        bd.connect_local(probs)
+    finally:
+        os.environ.pop("SSFM_PCG_SMS")
+    res = [None, None]
+
+    def work(r):
+        with gpu.cuda.stream(gpu.cuda.Stream()):
+            p = probs[r]
+            res[r] = (p.cost(p.encode()), p.gradient(p.encode()))
+
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(2)]
+    [t.start() for t in ts]
+    [t.join(timeout=120) for t in ts]
+    assert res[0][0] == res[1][0] == pytest.approx(c1, rel=1e-13)
+    C = st.num_cameras
+    # camera part of the gradient is the global one on every rank; point parts are local
+    for r in range(2):
+        g = res[r][1]
+        assert np.allclose(g[:7 * C], g1[:7 * C], rtol=1e-11, atol=1e-9)
+        p0, p1 = probs[r].point_range
+        assert np.allclose(g[7 * C:7 * C + 3 * (p1 - p0)], g1[7 * C + 3 * p0:7 * C + 3 * p1], rtol=1e-12, atol=1e-12)
+
+
+def test_two_processes_ipc(gpu, tmp_path):
+    """comm='torch': two processes on cuda:0, gloo for the handle exchange,
+    CUDA IPC for the exchange regions (the one-process-per-GPU path)."""
+    out = tmp_path / "res"
+    env = dict(os.environ, SSFM_PCG_SMS="64", PYTHONPATH=ROOT)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29517", os.path.join(ROOT, "tests", "dist_worker.py"),
+           str(out)]
+    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+    r0, r1 = np.load(str(out) + ".0.npz"), np.load(str(out) + ".1.npz")
+    assert np.array_equal(r0["costs"], r1["costs"])
+    assert np.array_equal(r0["theta"], r1["theta"])
+    st = scene(cams=20, pts=1500, k=4, seed=2)
+    single = b2.BAProblem(st, b2.RobustLoss("huber", 1.0))
+    _, rep = b2.lm_solve(single, single.encode(), b2.LMConfig(max_iterations=8))
+    assert r0["costs"] == pytest.approx(np.array([i.cost_after for i in rep.iterations]), rel=1e-7)
