@@ -36,13 +36,16 @@ struct BADev {
   double* yv;             // [4P] (padded for 32-byte gathers)
   double* Minv;           // [64C]
   double* bred;           // [8C]
+  double* fterm;          // [2C] shared focal: per-camera shares (operator row / precond)
+  double* fpt;            // [3P] shared focal: a_j = sum_o Jp_o^T jf_o (nullptr otherwise)
+  double* fwpart;         // [ptinv blocks] shared focal: sum_j a_j^T Cinv_j a_j partials
   unsigned char* pinned;  // [C] bitmask of pinned retained slots
   double* scal;           // scalars: [0] gmax bits, [1] gnorm2, [2] cost, ...
   double* partials;       // [max(nb, blocks)] reduction scratch
   int* status;
 };
 
-enum { SC_GMAX = 0, SC_GNORM2 = 1, SC_COST = 2, SC_LAMBDA = 3 };
+enum { SC_GMAX = 0, SC_GNORM2 = 1, SC_COST = 2, SC_LAMBDA = 3, SC_GFOCAL = 4 };
 
 // ---------------------------------------------------------------------------
 // camera cache from theta (quat_to_matrix_many per camera, ba.py:111-116)
@@ -104,7 +107,7 @@ __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
 // Writes Jpm (coalesced), Jcm/rcm (camera-major scatter), Cpt, gpt, and the
 // optional reference-layout exports (r_out [2N], J_out [22N] in observation order).
 // ---------------------------------------------------------------------------
-#define LIN_V 9
+#define LIN_V 12   // Jp^T Jp (6), Jp^T r (3), Jp^T jf (3, shared focal only)
 __global__ void __launch_bounds__(256) ba_k_linearize(BADev d, const double* __restrict__ theta,
                                                       double* r_out, double* J_out, double* gpt_norm_part) {
   __shared__ double sm[8][SSFM_BATCH][LIN_V];
@@ -156,6 +159,9 @@ __global__ void __launch_bounds__(256) ba_k_linearize(BADev d, const double* __r
         val[6] = jp[0] * r[0] + jp[3] * r[1];
         val[7] = jp[1] * r[0] + jp[4] * r[1];
         val[8] = jp[2] * r[0] + jp[5] * r[1];
+        val[9] = jp[0] * J[14] + jp[3] * J[15];
+        val[10] = jp[1] * J[14] + jp[4] * J[15];
+        val[11] = jp[2] * J[14] + jp[5] * J[15];
         if (r_out) {
           const int o = d.topo.pm_obs[i];
           r_out[2ll * o] = r[0];
@@ -190,6 +196,10 @@ __global__ void __launch_bounds__(256) ba_k_linearize(BADev d, const double* __r
       __syncwarp();
     }
     if (my_pt < pb1) {
+      if (d.fpt) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) d.fpt[3ll * my_pt + k] = acc[9 + k];
+      }
       double* C6 = d.Cpt + 6ll * my_pt;
 #pragma unroll
       for (int k = 0; k < 6; ++k) C6[k] = acc[k];
@@ -291,11 +301,14 @@ __global__ void ba_k_camfin(BADev d, double* cam_norm_part, const double* camsum
 #pragma unroll
       for (int q = p; q < 8; ++q) { B[8 * p + q] = s[idx]; B[8 * q + p] = s[idx]; ++idx; }
     double* g = d.gcam + 8ll * c;
+    const int nown = d.bp.focal_mode == 2 ? 7 : 8;   // shared focal: summed over cameras later
 #pragma unroll
     for (int p = 0; p < 8; ++p) {
       g[p] = s[36 + p];
-      gn2 += s[36 + p] * s[36 + p];
-      gmax = fmax(gmax, fabs(s[36 + p]));
+      if (p < nown) {
+        gn2 += s[36 + p] * s[36 + p];
+        gmax = fmax(gmax, fabs(s[36 + p]));
+      }
     }
   }
   double v[1] = {gn2};
@@ -326,37 +339,56 @@ __device__ __forceinline__ bool inv_sym3(const double* m, double* inv, double& d
   return true;
 }
 
+__device__ __forceinline__ void ptinv_focal_part(const BADev& d, int j, const double* inv) {
+  // shared focal: a_j^T Cinv_j a_j, block partials in block order (fixed tree)
+  __shared__ double sm[32];
+  double v[1] = {0.0};
+  if (j < d.bp.P) {
+    const double* a = d.fpt + 3ll * j;
+    double w[3];
+    sym3_matvec(inv, a, w);
+    v[0] = a[0] * w[0] + a[1] * w[1] + a[2] * w[2];
+  }
+  block_reduce<1>(v, sm);
+  if (threadIdx.x == 0) d.fwpart[blockIdx.x] = v[0];
+}
+
 __global__ void ba_k_ptinv(BADev d, double lam) {
-  int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= d.bp.P) return;
-  double m[6];
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  double inv[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  if (j < d.bp.P) {
+    double m[6];
 #pragma unroll
-  for (int k = 0; k < 6; ++k) m[k] = d.Cpt[6ll * j + k];
-  const double s = 1.0 + lam;
-  m[0] *= s; m[3] *= s; m[5] *= s;
-  double b[3];
+    for (int k = 0; k < 6; ++k) m[k] = d.Cpt[6ll * j + k];
+    const double s = 1.0 + lam;
+    m[0] *= s; m[3] *= s; m[5] *= s;
+    double b[3];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) b[k] = -d.gpt[3ll * j + k];
-  const int di[3] = {0, 3, 5};
+    for (int k = 0; k < 3; ++k) b[k] = -d.gpt[3ll * j + k];
+    const int di[3] = {0, 3, 5};
 #pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    if (m[di[k]] == 0.0) {
-      if (b[k] != 0.0) atomicOr(d.status, ST_PIN_POINT);
-      m[di[k]] = 1.0;
+    for (int k = 0; k < 3; ++k) {
+      if (m[di[k]] == 0.0) {
+        if (b[k] != 0.0) atomicOr(d.status, ST_PIN_POINT);
+        m[di[k]] = 1.0;
+      }
     }
+    double det;
+    if (!inv_sym3(m, inv, det)) {
+      atomicOr(d.status, ST_SINGULAR_POINT);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) inv[k] = 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 6; ++k) d.Cinv[6ll * j + k] = inv[k];
+    double y[3];
+    sym3_matvec(inv, b, y);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) d.y0[3ll * j + k] = y[k];
   }
-  double inv[6], det;
-  if (!inv_sym3(m, inv, det)) {
-    atomicOr(d.status, ST_SINGULAR_POINT);
-#pragma unroll
-    for (int k = 0; k < 6; ++k) inv[k] = 0.0;
-  }
-#pragma unroll
-  for (int k = 0; k < 6; ++k) d.Cinv[6ll * j + k] = inv[k];
-  double y[3];
-  sym3_matvec(inv, b, y);
-#pragma unroll
-  for (int k = 0; k < 3; ++k) d.y0[3ll * j + k] = y[k];
+  // every thread of the block, one code path (the reduction uses full-warp
+  // shuffles and __syncthreads)
+  if (d.fpt) ptinv_focal_part(d, j, inv);
 }
 
 // ---------------------------------------------------------------------------
@@ -475,12 +507,21 @@ __global__ void ba_k_camprec(BADev d, double lam, const double* camsum) {
   for (int p = 0; p < 8; ++p) br[p] = -d.gcam[8ll * c + p] - s[36 + p];
   unsigned pin = 0;
   for (int p = 0; p < 8; ++p) {
+    if (p == 7 && d.bp.focal_mode == 2) continue;   // shared focal: decided over all cameras
     if (S[9 * p] == 0.0) {
       // a zero diagonal of a PSD matrix implies a zero row: pin it (lm.py:628-635)
       if (br[p] != 0.0) atomicOr(d.status, ST_PIN_RETAINED);
       pin |= 1u << p;
       S[9 * p] = 1.0;
     }
+  }
+  if (d.bp.focal_mode == 2) {
+    // shared focal: this camera's share of the 1x1 focal block and of its rhs;
+    // ba_k_shared_focal_prec sums the shares and decides the pin
+    d.fterm[2ll * c] = B[63] * (1.0 + lam);   // the point terms are not per camera:
+    d.fterm[2ll * c + 1] = br[7];             // a_j couples every camera of point j
+    pin = (pin & 0x7fu) | 0x80u;
+    br[7] = 0.0;
   }
   d.pinned[c] = (unsigned char)pin;
   for (int p = 0; p < 8; ++p) d.bred[8ll * c + p] = (pin >> p & 1u) ? 0.0 : br[p];
@@ -492,10 +533,64 @@ __global__ void ba_k_camprec(BADev d, double lam, const double* camsum) {
   if (!ok) atomicOr(d.status, ST_SINGULAR_PRECOND);
   for (int p = 0; p < 8; ++p)
     for (int q = 0; q < 8; ++q) M[8 * p + q] = (p < 7 && q < 7 && ok) ? I7[7 * p + q] : 0.0;
+  if (d.bp.focal_mode == 2) { M[63] = 1.0; return; }
   const double s77 = S[63];
   const double f = 1.0 / s77;
   if (!isfinite(f)) atomicOr(d.status, ST_SINGULAR_PRECOND);
   M[63] = f;
+}
+
+// Shared focal (ba.py:49, 61): one retained scalar coupled to every camera.
+// Its damped Schur diagonal is the sum of the cameras' damped focal diagonals
+// minus sum_j a_j^T Cinv_j a_j (a_j = sum over ALL observations of point j of
+// Jp^T jf: the cross terms between cameras are part of it); its reduced rhs is
+// the sum of the cameras' shares. Summed in fixed order (one block); pinned if
+// the diagonal is exactly zero
+// (lm.py:628-635), and set its 1x1 block-Jacobi factor (lm.py:516-527).
+__global__ void ba_k_shared_focal_prec(BADev d, int nwpart) {
+  __shared__ double sm[96];
+  double v[3] = {0.0, 0.0, 0.0};
+  const int C = d.bp.C;
+  const int per = (C + blockDim.x - 1) / blockDim.x;
+  const int a = threadIdx.x * per, b = min(C, a + per);
+  for (int c = a; c < b; ++c) { v[0] += d.fterm[2ll * c]; v[1] += d.fterm[2ll * c + 1]; }
+  const int perw = (nwpart + blockDim.x - 1) / blockDim.x;
+  const int aw = threadIdx.x * perw, bw = min(nwpart, aw + perw);
+  for (int k = aw; k < bw; ++k) v[2] += d.fwpart[k];
+  block_reduce<3>(v, sm);
+  if (threadIdx.x == 0) {
+    // S_ff = A_ff (1 + lam) - sum_j a_j^T Cinv_j a_j  (lm.py:608-626 for the focal row)
+    const double sff = v[0] - v[2], bf = v[1];
+    if (sff == 0.0) {
+      if (bf != 0.0) atomicOr(d.status, ST_PIN_RETAINED);
+      d.pinned[0] |= 0x80;
+      d.bred[7] = 0.0;
+      d.Minv[63] = 1.0;
+    } else {
+      d.pinned[0] &= 0x7f;
+      d.bred[7] = bf;
+      const double f = 1.0 / sff;
+      if (!isfinite(f)) atomicOr(d.status, ST_SINGULAR_PRECOND);
+      d.Minv[63] = f;
+    }
+  }
+}
+
+// Shared focal gradient: sum of the cameras' focal entries (camera order);
+// adds it to |g|^2 and max|g| (camfin left it out).
+__global__ void ba_k_shared_focal_grad(BADev d) {
+  __shared__ double sm[32];
+  double v[1] = {0.0};
+  const int C = d.bp.C;
+  const int per = (C + blockDim.x - 1) / blockDim.x;
+  const int a = threadIdx.x * per, b = min(C, a + per);
+  for (int c = a; c < b; ++c) v[0] += d.gcam[8ll * c + 7];
+  block_reduce<1>(v, sm);
+  if (threadIdx.x == 0) {
+    d.scal[SC_GFOCAL] = v[0];
+    d.scal[SC_GNORM2] += v[0] * v[0];
+    atomic_max_nonneg(d.scal + SC_GMAX, fabs(v[0]));
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -527,6 +622,7 @@ __global__ void __launch_bounds__(256) ba_k_backsub(BADev d, const double* __res
         double pc[8];
         ld_v4(x + 8ll * c, pc);
         ld_v4(x + 8ll * c + 4, pc + 4);
+        if (d.bp.focal_mode == 2) pc[7] = x[7];
         double t[2];
         ba_jc_mul(J, pc, t);
         ba_jpt_mul(J, t, val);
@@ -559,6 +655,7 @@ __global__ void ba_k_camdelta(BADev d, const double* __restrict__ x, double* del
 #pragma unroll
   for (int k = 0; k < 7; ++k) delta[7ll * c + k] = x[8ll * c + k];
   if (d.bp.focal_mode == 1) delta[d.bp.off_foc + c] = x[8ll * c + 7];
+  if (d.bp.focal_mode == 2 && c == 0) delta[d.bp.off_foc] = x[7];
 }
 
 // candidate = theta + delta (lm.py:770)

@@ -72,6 +72,7 @@ __device__ __forceinline__ void ba_point_pass(const BADev& d, const double* v, d
         double pc[8];
         ld_v4(v + 8ll * c, pc);
         ld_v4(v + 8ll * c + 4, pc + 4);
+        if (d.bp.focal_mode == 2) pc[7] = v[7];   // shared focal (camera 0, slot 7)
         double t[2];
         ba_jc_mul(J, pc, t);
         ba_jpt_mul(J, t, val);
@@ -195,6 +196,7 @@ __device__ __forceinline__ void ba_fused_pass(const BADev& d, const FusedTopo& f
         double pc[8];
         ld_v4(v + 8ll * c, pc);
         ld_v4(v + 8ll * c + 4, pc + 4);
+        if (d.bp.focal_mode == 2) pc[7] = v[7];   // shared focal (camera 0, slot 7)
         double t[2];
         ba_jc_mul(J, pc, t);
         ba_jpt_mul(J, t, val);
@@ -320,6 +322,8 @@ ba_k_pcg(BADev d, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg
     return a;
   };
   unsigned long long ep = cm.nranks > 1 ? *cm.epoch : 0ull;
+  const bool shared = d.bp.focal_mode == 2;
+  double qf = 0.0;
 
   // ---- init: x = 0, r = b_red, z = M r, p = z
   {
@@ -348,6 +352,7 @@ ba_k_pcg(BADev d, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg
   const double tol = cg_tol * fmax(gn, 1e-300);
   double rr = cta_partials_sum(part, NP, 2, 0, &smb[0]);
   double rho = cta_partials_sum(part, NP, 2, 1, &smb[1]);
+  double pf = shared ? p[7] : 0.0;
   double rn = sqrt(rr);
   int iters = 0;
   int flag = 0;
@@ -383,10 +388,13 @@ ba_k_pcg(BADev d, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg
           const bool ok = s < S;
           const int c = ok ? s >> 3 : 0, k = s & 7;
           const double pk = ok ? p[s] : 0.0;
+          // shared focal: the focal slot of every camera reads the one shared
+          // unknown, stored in camera 0's slot 7 (the others are pinned zeros)
+          const double pkt = (shared && k == 7) ? pf : pk;
           double bp = 0.0;
 #pragma unroll
           for (int m = 0; m < 8; ++m) {
-            const double pm = grp8_get(pk, m);
+            const double pm = grp8_get(pkt, m);
             if (ok) bp += d.Bc[64ll * c + 8 * k + m] * pm;
           }
           if (ok) {
@@ -398,17 +406,27 @@ ba_k_pcg(BADev d, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg
             } else {
               acc = local_cam(s);
             }
-            double qk = bp + lam * d.Bc[64ll * c + 9 * k] * pk - acc;
-            if ((d.pinned[c] >> k) & 1) qk = pk;
-            q[s] = qk;
-            v[0] += pk * qk;
+            if (shared && k == 7) {
+              // camera c's share of the shared-focal row; summed below
+              d.fterm[c] = bp + lam * d.Bc[64ll * c + 63] * pf - acc;
+              if (c) q[s] = 0.0;
+            } else {
+              double qk = bp + lam * d.Bc[64ll * c + 9 * k] * pk - acc;
+              if ((d.pinned[c] >> k) & 1) qk = pk;
+              q[s] = qk;
+              v[0] += pk * qk;
+            }
           }
         }
         block_reduce<1>(v, smred);
         if (threadIdx.x == 0) part[2ll * blockIdx.x] = v[0];
       }
       grid.sync();
-      const double pq = cta_partials_sum(part, NP, 2, 0, &smb[0]);
+      double pq = cta_partials_sum(part, NP, 2, 0, &smb[0]);
+      if (shared) {   // every CTA sums the cameras' shares in the same order
+        qf = (d.pinned[0] >> 7 & 1) ? pf : cta_partials_sum(d.fterm, d.bp.C, 1, 0, &smb[2]);
+        pq += pf * qf;
+      }
       if (!isfinite(pq) || pq <= 0.0) { flag = ST_CG_BREAKDOWN; break; }
       const double alpha = rho / pq;
       // P4: x += a p, r -= a q, z = M r; partials r.r, r.z
@@ -422,7 +440,7 @@ ba_k_pcg(BADev d, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg
           double rk = 0.0;
           if (ok) {
             x[s] += alpha * p[s];
-            rk = r[s] - alpha * q[s];
+            rk = r[s] - alpha * ((shared && s == 7) ? qf : q[s]);
             r[s] = rk;
           }
           double zk = 0.0;
@@ -449,6 +467,7 @@ ba_k_pcg(BADev d, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg
       // P5: p = z + beta p
       for (int s = gid; s < S; s += stride) p[s] = z[s] + beta * p[s];
       grid.sync();
+      if (shared) pf = p[7];   // every thread tracks the shared focal of p
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {

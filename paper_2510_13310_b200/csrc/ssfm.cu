@@ -343,8 +343,6 @@ extern "C" int ssfm_create_ba(const ssfm_ba_desc* desc, void* stream, ssfm_handl
   if (desc->num_obs <= 0) return set_err(SSFM_EMPTY_PROBLEM, "scene has no observations");
   if (desc->num_obs >= (1ll << 31) - 64) return set_err(SSFM_INVALID_ARGUMENT, "too many observations for int32 indexing");
   if (desc->num_cameras <= 0 || desc->num_points < 0) return set_err(SSFM_INVALID_ARGUMENT, "bad camera/point counts");
-  if (desc->shared_focal && desc->optimize_focal)
-    return set_err(SSFM_INVALID_ARGUMENT, "shared_focal: not supported by this build");
   cudaStream_t st = (cudaStream_t)stream;
   ssfm_handle* h = new ssfm_handle();
   CU(cudaGetDevice(&h->device));
@@ -401,6 +399,13 @@ extern "C" int ssfm_create_ba(const ssfm_ba_desc* desc, void* stream, ssfm_handl
   if ((rc = dalloc(h, &d.yv, 4ll * P))) return fail(rc);   // padded: 32-byte gathers
   if ((rc = dalloc(h, &d.Minv, 64ll * C))) return fail(rc);
   if ((rc = dalloc(h, &d.bred, 8ll * C))) return fail(rc);
+  if ((rc = dalloc(h, &d.fterm, 2ll * C))) return fail(rc);
+  d.fpt = nullptr;
+  d.fwpart = nullptr;
+  if (d.bp.focal_mode == 2) {
+    if ((rc = dalloc(h, &d.fpt, 3ll * P))) return fail(rc);
+    if ((rc = dalloc(h, &d.fwpart, nblk(P, 256) + 1))) return fail(rc);
+  }
   if ((rc = dalloc(h, &d.pinned, C))) return fail(rc);
   if ((rc = common_alloc(h, 8 * C, C))) return fail(rc);
   d.scal = h->misc->scal;
@@ -678,6 +683,7 @@ static int launch_linearize(ssfm_handle* h, const double* theta, double* r_out, 
       ba_k_camfin<<<h->cam_blocks, 256, 0, st>>>(d, h->red + (long long)h->lin_blocks * 8, nullptr);
       k_sum_partials<<<1, 1024, 0, st>>>(h->red, h->lin_blocks * 8 + h->cam_blocks, d.scal + SC_GNORM2);
       count_launch(h, 5);
+      if (d.bp.focal_mode == 2) { ba_k_shared_focal_grad<<<1, 256, 0, st>>>(d); count_launch(h); }
     } else {
       // camera blocks: local tile sums -> exchange -> identical Bc / gcam on every rank;
       // |g|^2 = sum over ranks of the point part + the (replicated) camera part
@@ -745,6 +751,10 @@ static int launch_solve(ssfm_handle* h, double lam, const ssfm_lm_config* cfg, c
     }
     ba_k_camprec<<<nblk(d.bp.C, 64), 64, 0, st>>>(d, lam, cs);
     count_launch(h, 3);
+    if (d.bp.focal_mode == 2) {
+      ba_k_shared_focal_prec<<<1, 256, 0, st>>>(d, nblk(d.bp.P, 256));
+      count_launch(h);
+    }
   } else {
     int rc = gp_launch_elim(h->gp, lam, h->cam_blocks, st);
     if (rc) return set_err(SSFM_CUDA_ERROR, "gp elimination launch");
@@ -848,6 +858,8 @@ __global__ void k_export_grad_ba(BADev d, double* grad) {
     grad[i] = d.gpt[i - 7ll * C];
   } else if (d.bp.focal_mode == 1 && i < d.bp.off_foc + C) {
     grad[i] = d.gcam[8 * (i - d.bp.off_foc) + 7];
+  } else if (d.bp.focal_mode == 2 && i == d.bp.off_foc) {
+    grad[i] = d.scal[SC_GFOCAL];
   }
   (void)P;
 }
@@ -1029,6 +1041,7 @@ extern "C" int ssfm_comm_init(ssfm_handle* h, int32_t rank, int32_t nranks, void
                               void** region_out) {
   if (!h) return set_err(SSFM_INVALID_ARGUMENT, "null argument");
   if (h->kind != 0) return set_err(SSFM_INVALID_ARGUMENT, "point sharding: BA handles only in this build");
+  if (h->ba.bp.focal_mode == 2) return set_err(SSFM_INVALID_ARGUMENT, "point sharding: shared focal not supported");
   if (nranks < 1 || nranks > SSFM_MAX_RANKS || rank < 0 || rank >= nranks)
     return set_err(SSFM_INVALID_ARGUMENT, "bad rank / nranks");
   if (h->region) return set_err(SSFM_INVALID_ARGUMENT, "exchange region already initialised");

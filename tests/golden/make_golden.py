@@ -130,7 +130,19 @@ def digest(arrs):
     return h.hexdigest()
 
 
+def shared_focal_fixture():
+    """BA with ONE focal shared by every camera (ba.py:49, 61, 77, 89)."""
+    truth, obs = rsm.generate(rsm.SynthConfig(num_cameras=8, num_points=120, visibility_fraction=0.5,
+                                              pixel_noise_sigma=1.0, seed=3))
+    start = rsm.perturb(obs, rot_deg=1.0, center_frac=0.01, focal_frac=0.02, point_frac=0.005, seed=1)
+    ba_fixture("ba_shared.npz", start, ref.RobustLoss("huber", 1.0), shared_focal=True)
+
+
 def main():
+    if "shared" in sys.argv[1:]:
+        shared_focal_fixture()
+        return
+    shared_focal_fixture()
     # --- BA fixtures
     truth, obs = rsm.generate(rsm.SynthConfig(num_cameras=8, num_points=120, visibility_fraction=0.5,
                                               pixel_noise_sigma=1.0, seed=3))

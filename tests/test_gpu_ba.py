@@ -337,3 +337,32 @@ def test_large_problem_properties(gpu):
     th2, _ = b2.lm_solve(p, th0, b2.LMConfig(max_iterations=6))
     assert np.array_equal(th, th2)
     assert synth.reproj_rmse(p.decode(th)) < synth.reproj_rmse(p.decode(th0))
+
+
+def test_shared_focal_vs_reference(gpu):          # test_ba.py:225-230 + the shared-focal golden
+    """One focal shared by every camera (ba.py:49, 61, 77, 89): layout, cost,
+    residuals, Jacobian, gradient, damped step and LM trajectory vs the
+    reference run (tests/golden/ba_shared.npz)."""
+    z = golden("ba_shared.npz")
+    p = problem_from_golden(z)
+    assert p.layout.num_param_blocks == len(z["quats"]) + len(z["points"]) + 1
+    th = z["theta0"]
+    assert p.cost(th) == pytest.approx(float(z["cost0"]), rel=1e-13)
+    r, jac = p.linearize(th)
+    assert jac.num_entries == 3 * len(z["cam"])
+    assert rel(r, z["r0"]) < 1e-13
+    assert rel(jac.data, z["J0"]) < 1e-12
+    assert rel(p.gradient(th), z["grad0"]) < 1e-11
+    d, it = solve_normal_native(gpu, p, 1e-3, b2.LMConfig())
+    assert rel(d, z["delta_lam1e3"]) < 1e-7
+    assert abs(it - int(z["cg_lam1e3"])) <= 2
+    th_f, rep = b2.lm_solve(p, th, b2.LMConfig(max_iterations=30))
+    ref = z["records"]
+    assert rep.termination == str(z["termination"])
+    assert [i.step_accepted for i in rep.iterations] == [bool(x) for x in ref[:, 4]]
+    assert cg_counts_match([i.cg_iters for i in rep.iterations], [int(x) for x in ref[:, 5]])
+    assert rep.iterations[-1].cost_after == pytest.approx(ref[-1, 2], rel=1e-10)
+    est, tru = p.decode(th_f), p.decode(z["theta_final"])
+    assert np.all(est.focals == est.focals[0])
+    _, al = synth.align(est, tru, "sim3")
+    assert np.abs(al.points - tru.points).max() < 1e-8 * synth.scene_diameter(tru)

@@ -13,7 +13,7 @@ def rel(a, b):
     return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
 
 
-@pytest.mark.parametrize("name", ["ba_small.npz", "ba_nofocal.npz", "ba_bal.npz"])
+@pytest.mark.parametrize("name", ["ba_small.npz", "ba_nofocal.npz", "ba_bal.npz", "ba_shared.npz"])
 def test_ba_cost_residual_jacobian_gradient(name):
     z = golden(name)
     prob = ba_prob_from_golden(z)
@@ -26,8 +26,9 @@ def test_ba_cost_residual_jacobian_gradient(name):
     assert rel(Jd.T @ r, z["grad0"]) < 1e-11
 
 
-def test_ba_solve_normal_matches_reference():
-    z = golden("ba_small.npz")
+@pytest.mark.parametrize("name", ["ba_small.npz", "ba_shared.npz"])
+def test_ba_solve_normal_matches_reference(name):
+    z = golden(name)
     prob = ba_prob_from_golden(z)
     r, J = orc.ba_linearize(prob, z["theta0"])
     Jd = orc.ba_dense_jacobian(prob, J)
@@ -36,7 +37,7 @@ def test_ba_solve_normal_matches_reference():
     assert abs(it - int(z["cg_lam1e3"])) <= 2
 
 
-@pytest.mark.parametrize("name", ["ba_small.npz", "ba_nofocal.npz", "ba_bal.npz"])
+@pytest.mark.parametrize("name", ["ba_small.npz", "ba_nofocal.npz", "ba_bal.npz", "ba_shared.npz"])
 def test_ba_lm_solve_matches_reference(name):
     z = golden(name)
     prob = ba_prob_from_golden(z)
