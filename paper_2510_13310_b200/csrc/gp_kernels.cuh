@@ -17,6 +17,7 @@
 //   C'_j  = (1+lam) sum a^2 I   - sum inv_o a^2 g g^T
 #pragma once
 #include "ba_kernels.cuh"
+#include "comm.cuh"
 #include <cooperative_groups.h>
 
 #define GP_JREC 4
@@ -231,14 +232,19 @@ __global__ void __launch_bounds__(SSFM_TILE) gp_k_camred(GPDev g) {
   }
 }
 
-__global__ void gp_k_camfin(GPDev g, double* norm_part) {
+__global__ void gp_k_camfin(GPDev g, double* norm_part, const double* camsum) {
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   double gn2 = 0.0, gmax = 0.0;
   if (c < g.gp.C) {
     double s[GPC_V] = {0.0, 0.0, 0.0, 0.0};
-    for (int t = g.topo.cam_tile[c]; t < g.topo.cam_tile[c + 1]; ++t)
+    if (camsum) {   // per-camera sums already reduced over the ranks
 #pragma unroll
-      for (int k = 0; k < GPC_V; ++k) s[k] += g.tilebuf[(long long)GPC_V * t + k];
+      for (int k = 0; k < GPC_V; ++k) s[k] = camsum[(long long)GPC_V * c + k];
+    } else {
+      for (int t = g.topo.cam_tile[c]; t < g.topo.cam_tile[c + 1]; ++t)
+#pragma unroll
+        for (int k = 0; k < GPC_V; ++k) s[k] += g.tilebuf[(long long)GPC_V * t + k];
+    }
     g.Acam[c] = s[0];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -416,15 +422,16 @@ __global__ void __launch_bounds__(SSFM_TILE) gp_k_cam_elim(GPDev g, double lam) 
   }
 }
 
-__global__ void gp_k_camprec(GPDev g, double lam) {
+__global__ void gp_k_camprec(GPDev g, double lam, const double* camsum) {
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= g.gp.C) return;
   double s[GPE_V];
 #pragma unroll
-  for (int k = 0; k < GPE_V; ++k) s[k] = 0.0;
-  for (int t = g.topo.cam_tile[c]; t < g.topo.cam_tile[c + 1]; ++t)
+  for (int k = 0; k < GPE_V; ++k) s[k] = camsum ? camsum[(long long)GPE_V * c + k] : 0.0;
+  if (!camsum)
+    for (int t = g.topo.cam_tile[c]; t < g.topo.cam_tile[c + 1]; ++t)
 #pragma unroll
-    for (int k = 0; k < GPE_V; ++k) s[k] += g.tilebuf[(long long)GPE_V * t + k];
+      for (int k = 0; k < GPE_V; ++k) s[k] += g.tilebuf[(long long)GPE_V * t + k];
   const double A = g.Acam[c] * (1.0 + lam);
   double Bp[6] = {A - s[0], -s[1], -s[2], A - s[3], -s[4], A - s[5]};
 #pragma unroll
@@ -548,7 +555,7 @@ __device__ __forceinline__ void gp_camera_pass(const GPDev& g, const double* y, 
   }
 }
 
-__global__ void __launch_bounds__(PCG_THREADS) gp_k_pcg(GPDev g, double lam, int max_iters,
+__global__ void __launch_bounds__(PCG_THREADS) gp_k_pcg(GPDev g, CommDev cm, double lam, int max_iters,
                                                         double cg_tol, double* x, double* r,
                                                         double* z, double* p, double* q,
                                                         double* part, CGCtl* ctl) {
@@ -562,6 +569,13 @@ __global__ void __launch_bounds__(PCG_THREADS) gp_k_pcg(GPDev g, double lam, int
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   double* tile4 = g.tilebuf;
   const int NP = gridDim.x;
+  auto local_cam = [&](int s) -> double {   // local camera half of S*p, slot s = 4c + k
+    const int c = s >> 2, k = s & 3;
+    double a = 0.0;
+    for (int t = g.topo.cam_tile[c]; t < g.topo.cam_tile[c + 1]; ++t) a += tile4[4ll * t + k];
+    return a;
+  };
+  unsigned long long ep = cm.nranks > 1 ? *cm.epoch : 0ull;
   {
     double v[2] = {0.0, 0.0};
     for (int base = 0; base < S; base += stride) {
@@ -598,6 +612,14 @@ __global__ void __launch_bounds__(PCG_THREADS) gp_k_pcg(GPDev g, double lam, int
       grid.sync();
       gp_camera_pass(g, g.yv, tile4, smred);
       grid.sync();
+      if (cm.nranks > 1) {   // exchange the camera half of S*p with the peers (comm.cuh)
+        ++ep;
+        double* mine = cm.buf[cm.rank] + (long long)(ep & 1) * cm.cap;
+        for (int s = gid; s < S; s += stride) mine[s] = local_cam(s);
+        grid.sync();
+        if (blockIdx.x == 0 && threadIdx.x == 0) comm_signal_wait(cm, ep);
+        grid.sync();
+      }
       {
         double v[1] = {0.0};
         for (int base = 0; base < S; base += stride) {
@@ -612,8 +634,14 @@ __global__ void __launch_bounds__(PCG_THREADS) gp_k_pcg(GPDev g, double lam, int
             if (k < 3) {
               const double* B = g.Bp + 6ll * c;
               const double row[3][3] = {{B[0], B[1], B[2]}, {B[1], B[3], B[4]}, {B[2], B[4], B[5]}};
-              double acc = 0.0;
-              for (int t = g.topo.cam_tile[c]; t < g.topo.cam_tile[c + 1]; ++t) acc += tile4[4ll * t + k];
+              double acc;
+              if (cm.nranks > 1) {
+                const long long off = (long long)(ep & 1) * cm.cap + s;
+                acc = comm_peer_load(cm.buf[0] + off);
+                for (int rk = 1; rk < cm.nranks; ++rk) acc += comm_peer_load(cm.buf[rk] + off);
+              } else {
+                acc = local_cam(s);
+              }
               qk = row[k][0] * p0 + row[k][1] * p1 + row[k][2] * p2 - acc;
             }
             if ((g.pinned[c] >> k) & 1) qk = pk;
@@ -663,6 +691,7 @@ __global__ void __launch_bounds__(PCG_THREADS) gp_k_pcg(GPDev g, double lam, int
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (cm.nranks > 1) *cm.epoch = ep;
     ctl->tol = tol; ctl->rho = rho; ctl->rn = rn; ctl->iters = iters; ctl->flag = flag;
     if (flag) atomicOr(g.status, flag);
   }
@@ -764,7 +793,8 @@ __global__ void gp_k_scale_sum(GPDev g, const double* __restrict__ theta, double
   if (threadIdx.x == 0) part[blockIdx.x] = v[0];
 }
 
-__global__ void gp_k_gauge_prep(GPDev g, const double* __restrict__ part, int n, const double* __restrict__ theta) {
+__global__ void gp_k_gauge_prep(GPDev g, const double* __restrict__ part, int n, const double* __restrict__ theta,
+                                double* sum_cnt) {
   __shared__ double sm[32];
   double v[1] = {0.0};
   int per = (n + blockDim.x - 1) / blockDim.x;
@@ -772,10 +802,17 @@ __global__ void gp_k_gauge_prep(GPDev g, const double* __restrict__ part, int n,
   for (int k = a; k < b; ++k) v[0] += part[k];
   block_reduce<1>(v, sm);
   if (threadIdx.x == 0) {
-    g.scal[4] = v[0] / (double)g.topo.N;   // mean
+    if (sum_cnt) {   // sharded: (sum, count) for the allreduce, mean in gp_k_gauge_mean
+      sum_cnt[0] = v[0];
+      sum_cnt[1] = (double)g.topo.N;
+    } else {
+      g.scal[4] = v[0] / (double)g.topo.N;   // mean
+    }
     g.scal[5] = theta[0]; g.scal[6] = theta[1]; g.scal[7] = theta[2];   // t0 copy
   }
 }
+
+__global__ void gp_k_gauge_mean(GPDev g, const double* sum_cnt) { g.scal[4] = sum_cnt[0] / sum_cnt[1]; }
 
 __global__ void gp_k_gauge_apply(GPDev g, double* theta, long long n) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -810,7 +847,7 @@ static int gp_launch_linearize(GPDev& g, const double* theta, double* r_out, dou
   gp_k_linearize<<<lin_blocks, 256, 0, st>>>(g, theta, r_out, J_out, red);
   if (g.topo.nt) gp_k_camred<<<g.topo.nt, SSFM_TILE, 0, st>>>(g);
   const long long off = (long long)lin_blocks * 8;
-  gp_k_camfin<<<cam_blocks, 256, 0, st>>>(g, red + off);
+  gp_k_camfin<<<cam_blocks, 256, 0, st>>>(g, red + off, nullptr);
   const int sb = gp_nblk(g.topo.N, 256);
   gp_k_scale_norm<<<sb, 256, 0, st>>>(g, red + off + cam_blocks);
   k_sum_partials<<<1, 1024, 0, st>>>(red, (int)(off + cam_blocks + sb), g.scal + SC_GNORM2);
@@ -822,7 +859,7 @@ static int gp_launch_elim(GPDev& g, double lam, int cam_blocks, cudaStream_t st)
   const int lin_blocks = std::max(1, gp_nblk(g.topo.nb, 8));
   gp_k_pt_elim<<<std::min(lin_blocks, 148 * 16), 256, 0, st>>>(g, lam);
   if (g.topo.nt) gp_k_cam_elim<<<g.topo.nt, SSFM_TILE, 0, st>>>(g, lam);
-  gp_k_camprec<<<gp_nblk(g.gp.C, 64), 64, 0, st>>>(g, lam);
+  gp_k_camprec<<<gp_nblk(g.gp.C, 64), 64, 0, st>>>(g, lam, nullptr);
   (void)cam_blocks;
   return cudaGetLastError() != cudaSuccess;
 }
@@ -838,7 +875,7 @@ static int gp_launch_post_step(GPDev& g, double* theta, double* red, cudaStream_
   if (g.gp.depth_mode) return 0;
   const int sb = gp_nblk(g.topo.N, 256);
   gp_k_scale_sum<<<sb, 256, 0, st>>>(g, theta, red);
-  gp_k_gauge_prep<<<1, 1024, 0, st>>>(g, red, sb, theta);
+  gp_k_gauge_prep<<<1, 1024, 0, st>>>(g, red, sb, theta, nullptr);
   const long long n = g.gp.off_sc + g.topo.N;
   gp_k_gauge_apply<<<gp_nblk(n, 256), 256, 0, st>>>(g, theta, n);
   return cudaGetLastError() != cudaSuccess;

@@ -229,6 +229,16 @@ static int common_alloc(ssfm_handle* h, int S_slots, int C) {
   return SSFM_OK;
 }
 
+// SSFM_PCG_SMS caps the SMs of the persistent PCG grid (several sharded
+// handles on one device must be co-resident: their kernels wait on each other)
+static int pcg_sms_of(const ssfm_handle* h) {
+  if (const char* e = getenv("SSFM_PCG_SMS")) {
+    const int v = atoi(e);
+    if (v > 0 && v < h->num_sms) return v;
+  }
+  return h->num_sms;
+}
+
 // Choose the BA PCG operator and its launch geometry; build the fused schedule.
 template <int SL>
 static int try_fused_ba(ssfm_handle* h, int* ok) {
@@ -263,11 +273,7 @@ static int setup_ba_pcg(ssfm_handle* h, cudaStream_t st) {
   const Topo& T = h->topo;
   // SSFM_PCG_SMS caps the SMs of the persistent PCG grid (several sharded
   // handles on one device must be co-resident: their kernels wait on each other)
-  h->pcg_sms = h->num_sms;
-  if (const char* e = getenv("SSFM_PCG_SMS")) {
-    const int v = atoi(e);
-    if (v > 0 && v < h->num_sms) h->pcg_sms = v;
-  }
+  h->pcg_sms = pcg_sms_of(h);
   const int C = h->ba.bp.C;
   const char* env = getenv("SSFM_FUSED");
   const bool want = !(env && env[0] == '0') && C < FZ_MAX_CAMERAS;
@@ -495,7 +501,8 @@ extern "C" int ssfm_create_gp(const ssfm_gp_desc* desc, void* stream, ssfm_handl
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gp_k_pcg, PCG_THREADS, 0) || occ < 1)
     return fail(set_err(SSFM_CUDA_ERROR, "occupancy query for the PCG kernel failed"));
-  h->pcg_grid = occ * h->num_sms;
+  h->pcg_sms = pcg_sms_of(h);
+  h->pcg_grid = occ * h->pcg_sms;
   h->lin_blocks = std::max(1, std::min(nblk(T.nb, 8), h->num_sms * 16));
   h->cost_blocks = nblk(N, 256);
   h->cam_blocks = nblk(C, 256);
@@ -665,6 +672,8 @@ static int launch_cost(ssfm_handle* h, const double* theta, cudaStream_t st) {
     gp_k_cost<<<h->cost_blocks, 256, 0, st>>>(g, theta, h->red);
     k_sum_partials<<<1, 1024, 0, st>>>(h->red, h->cost_blocks, g.scal + SC_COST);
     count_launch(h, 2);
+    int rc = allreduce(h, g.scal + SC_COST, 1, AR_SUM, st);
+    if (rc) return rc;
   }
   CU(cudaGetLastError());
   return SSFM_OK;
@@ -699,9 +708,31 @@ static int launch_linearize(ssfm_handle* h, const double* theta, double* r_out, 
       count_launch(h, 8);
     }
   } else {
-    int rc = gp_launch_linearize(h->gp, theta, r_out, J_out, h->red, h->lin_blocks, h->cam_blocks, st);
-    if (rc) return set_err(SSFM_CUDA_ERROR, "gp linearize launch");
-    count_launch(h, 5);
+    GPDev& g = h->gp;
+    if (!sharded(h)) {
+      int rc = gp_launch_linearize(g, theta, r_out, J_out, h->red, h->lin_blocks, h->cam_blocks, st);
+      if (rc) return set_err(SSFM_CUDA_ERROR, "gp linearize launch");
+      count_launch(h, 5);
+    } else {
+      // camera sums exchanged; |g|^2 = (points + scales: summed over ranks) + cameras
+      gp_k_linearize<<<h->lin_blocks, 256, 0, st>>>(g, theta, r_out, J_out, h->red);
+      if (g.topo.nt) gp_k_camred<<<g.topo.nt, SSFM_TILE, 0, st>>>(g);
+      k_cam_tilesum<<<h->cam_blocks, 256, 0, st>>>(g.topo, g.tilebuf, GPC_V, h->camsum);
+      int rc = allreduce(h, h->camsum, (long long)GPC_V * g.gp.C, AR_SUM, st);
+      if (rc) return rc;
+      const long long off = (long long)h->lin_blocks * 8;
+      gp_k_camfin<<<h->cam_blocks, 256, 0, st>>>(g, h->red + off, h->camsum);
+      const int sb = nblk(g.topo.N, 256);
+      gp_k_scale_norm<<<sb, 256, 0, st>>>(g, h->red + off + h->cam_blocks);
+      k_sum_partials<<<1, 1024, 0, st>>>(h->red, (int)off, h->ar_tmp + 1);
+      k_sum_partials<<<1, 1024, 0, st>>>(h->red + off + h->cam_blocks, sb, h->ar_tmp + 3);
+      k_add2<<<1, 1, 0, st>>>(h->ar_tmp + 1, h->ar_tmp + 3, h->ar_tmp + 1);
+      if ((rc = allreduce(h, h->ar_tmp + 1, 1, AR_SUM, st))) return rc;
+      k_sum_partials<<<1, 1024, 0, st>>>(h->red + off, h->cam_blocks, h->ar_tmp + 2);
+      k_add2<<<1, 1, 0, st>>>(h->ar_tmp + 1, h->ar_tmp + 2, g.scal + SC_GNORM2);
+      if ((rc = allreduce(h, g.scal + SC_GMAX, 1, AR_MAX, st))) return rc;
+      count_launch(h, 11);
+    }
   }
   CU(cudaGetLastError());
   h->linearized = true;
@@ -722,12 +753,12 @@ static int launch_pcg(ssfm_handle* h, double lam, const ssfm_lm_config* cfg, cud
     CU(cudaLaunchCooperativeKernel(h->pcg_fn, dim3(h->pcg_grid), dim3(h->pcg_threads), a, h->pcg_smem, st));
   } else {
     GPDev& g = h->gp;
-    args[0] = &g; args[1] = &lam; args[2] = &max_it; args[3] = &tol;
-    args[4] = &h->x; args[5] = &h->r; args[6] = &h->z; args[7] = &h->p; args[8] = &h->q;
-    args[9] = &h->part;
+    void* a[12];
     CGCtl* ctl = &h->misc->ctl;
-    args[10] = &ctl;
-    CU(cudaLaunchCooperativeKernel((void*)gp_k_pcg, dim3(h->pcg_grid), dim3(PCG_THREADS), args, 0, st));
+    a[0] = &g; a[1] = &h->cm; a[2] = &lam; a[3] = &max_it; a[4] = &tol;
+    a[5] = &h->x; a[6] = &h->r; a[7] = &h->z; a[8] = &h->p; a[9] = &h->q;
+    a[10] = &h->part; a[11] = &ctl;
+    CU(cudaLaunchCooperativeKernel((void*)gp_k_pcg, dim3(h->pcg_grid), dim3(PCG_THREADS), a, 0, st));
   }
   count_launch(h);
   return SSFM_OK;
@@ -756,9 +787,22 @@ static int launch_solve(ssfm_handle* h, double lam, const ssfm_lm_config* cfg, c
       count_launch(h);
     }
   } else {
-    int rc = gp_launch_elim(h->gp, lam, h->cam_blocks, st);
-    if (rc) return set_err(SSFM_CUDA_ERROR, "gp elimination launch");
-    count_launch(h, 4);
+    GPDev& g = h->gp;
+    if (!sharded(h)) {
+      int rc = gp_launch_elim(g, lam, h->cam_blocks, st);
+      if (rc) return set_err(SSFM_CUDA_ERROR, "gp elimination launch");
+      count_launch(h, 4);
+    } else {
+      g.lam = lam;
+      const int lb = std::max(1, nblk(g.topo.nb, 8));
+      gp_k_pt_elim<<<std::min(lb, 148 * 16), 256, 0, st>>>(g, lam);
+      if (g.topo.nt) gp_k_cam_elim<<<g.topo.nt, SSFM_TILE, 0, st>>>(g, lam);
+      k_cam_tilesum<<<h->cam_blocks, 256, 0, st>>>(g.topo, g.tilebuf, GPE_V, h->camsum);
+      int rc = allreduce(h, h->camsum, (long long)GPE_V * g.gp.C, AR_SUM, st);
+      if (rc) return rc;
+      gp_k_camprec<<<nblk(g.gp.C, 64), 64, 0, st>>>(g, lam, h->camsum);
+      count_launch(h, 4);
+    }
   }
   CU(cudaGetLastError());
   if (h->prof.on) CU(cudaEventRecord(h->ev2, st));
@@ -783,8 +827,22 @@ static int launch_post_step(ssfm_handle* h, double* theta, cudaStream_t st) {
     ba_k_renorm<<<h->cam_blocks, 256, 0, st>>>(h->ba.bp.C, theta, &h->misc->status);
     count_launch(h);
   } else {
-    gp_launch_post_step(h->gp, theta, h->red, st);
-    count_launch(h, 3);
+    GPDev& g = h->gp;
+    if (!sharded(h) || g.gp.depth_mode) {
+      gp_launch_post_step(g, theta, h->red, st);
+      count_launch(h, 3);
+    } else {
+      // mean scale over every rank's observations (gp.py:137-139)
+      const int sb = nblk(g.topo.N, 256);
+      gp_k_scale_sum<<<sb, 256, 0, st>>>(g, theta, h->red);
+      gp_k_gauge_prep<<<1, 1024, 0, st>>>(g, h->red, sb, theta, h->ar_tmp + 4);
+      int rc = allreduce(h, h->ar_tmp + 4, 2, AR_SUM, st);
+      if (rc) return rc;
+      gp_k_gauge_mean<<<1, 1, 0, st>>>(g, h->ar_tmp + 4);
+      const long long n = g.gp.off_sc + g.topo.N;
+      gp_k_gauge_apply<<<nblk(n, 256), 256, 0, st>>>(g, theta, n);
+      count_launch(h, 4);
+    }
   }
   CU(cudaGetLastError());
   return SSFM_OK;
@@ -1040,19 +1098,20 @@ extern "C" int ssfm_profile_get(const ssfm_handle* h, int32_t kind, double* ms, 
 extern "C" int ssfm_comm_init(ssfm_handle* h, int32_t rank, int32_t nranks, void* ipc_handle_out,
                               void** region_out) {
   if (!h) return set_err(SSFM_INVALID_ARGUMENT, "null argument");
-  if (h->kind != 0) return set_err(SSFM_INVALID_ARGUMENT, "point sharding: BA handles only in this build");
-  if (h->ba.bp.focal_mode == 2) return set_err(SSFM_INVALID_ARGUMENT, "point sharding: shared focal not supported");
+  if (h->kind == 0 && h->ba.bp.focal_mode == 2)
+    return set_err(SSFM_INVALID_ARGUMENT, "point sharding: shared focal not supported");
   if (nranks < 1 || nranks > SSFM_MAX_RANKS || rank < 0 || rank >= nranks)
     return set_err(SSFM_INVALID_ARGUMENT, "bad rank / nranks");
   if (h->region) return set_err(SSFM_INVALID_ARGUMENT, "exchange region already initialised");
   const int C = h->topo.C;
-  const long long cap = (long long)std::max(CAM_V, 8) * C + 64;
+  const int per_cam = h->kind == 0 ? std::max(CAM_V, 8) : std::max(GPE_V, 4);
+  const long long cap = (long long)per_cam * C + 64;
   const size_t bytes = 256 + sizeof(double) * 2 * (size_t)cap;
   CU(cudaMalloc(&h->region, bytes));
   CU(cudaMemset(h->region, 0, bytes));
   DALLOC(h->cm.epoch, 1);
   CU(cudaMemset(h->cm.epoch, 0, sizeof(unsigned long long)));
-  DALLOC(h->camsum, (long long)CAM_V * C);
+  DALLOC(h->camsum, (long long)per_cam * C);
   DALLOC(h->ar_tmp, 16);
   CU(cudaDeviceSynchronize());
   CommDev& cm = h->cm;

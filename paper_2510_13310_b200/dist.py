@@ -19,9 +19,10 @@ the LM report is identical on all ranks. Results differ from a single-GPU
 solve only by summation order (bitwise stable per GPU count).
 
 The reference (sparsesfm) has no multi-GPU path; this module extends its
-`BAProblem` / `lm_solve` API (ba.py:35-36, lm.py:727-728) without changing it:
-a `ShardedBAProblem` is a `BAProblem` over the rank's shard, `lm_solve` is
-called on every rank with the rank's local theta.
+`BAProblem` / `GPProblem` / `lm_solve` API (ba.py:35-36, gp.py:33-35,
+lm.py:727-728) without changing it: a `ShardedBAProblem` / `ShardedGPProblem`
+is a problem over the rank's shard, `lm_solve` is called on every rank with
+the rank's local theta.
 """
 
 from __future__ import annotations
@@ -31,7 +32,8 @@ import ctypes as ct
 import numpy as np
 
 from . import _native
-from .ba import BAProblem
+from .ba import BAProblem, _DeviceProblem
+from .gp import GPProblem
 from .scene import SceneArrays, as_arrays
 
 
@@ -66,7 +68,55 @@ def shard_arrays(arr: SceneArrays, rank: int, world: int):
     return local, (p0, p1), obs
 
 
-class ShardedBAProblem(BAProblem):
+class _Sharded:
+    """Connection plumbing shared by the sharded BA and GP problems."""
+
+    def _init_shard(self, rank, world, group, comm):
+        if rank is None or world is None:
+            import torch.distributed as dist
+            rank, world = dist.get_rank(group), dist.get_world_size(group)
+        self.rank, self.world, self.group, self.comm = rank, world, group, comm
+        self._connected = world == 1
+        return rank, world
+
+    def _connect_torch(self, h):
+        if self.world > 1 and self.comm == "torch":
+            import torch.distributed as dist
+            lib = _native.load()
+            ih = (ct.c_char * 64)()
+            _native.check(lib.ssfm_comm_init(ct.c_void_p(h.ptr), self.rank, self.world, ih, None))
+            handles = [None] * self.world
+            dist.all_gather_object(handles, bytes(ih), group=self.group)
+            _native.check(lib.ssfm_comm_connect(ct.c_void_p(h.ptr), ct.c_char_p(b"".join(handles)), None))
+            self._connected = True
+
+    def _create(self):
+        h = super()._create()
+        self._native_ptr = h
+        self._connect_torch(h)
+        return h
+
+    def _native_handle(self):
+        h = super()._native_handle()
+        if not self._connected:
+            raise RuntimeError("sharded problem not connected: call connect_local(problems) first")
+        return h
+
+    def _all_gather(self, obj, shards, pick):
+        """every rank's `pick(problem, theta)` in rank order: torch collective,
+        or from `shards` = [(problem, theta)] for comm='local'."""
+        if shards is not None:
+            return [pick(p, th if isinstance(th, np.ndarray) else th.detach().cpu().numpy())
+                    for p, th in sorted(shards, key=lambda t: t[0].rank)]
+        if self.world == 1:
+            return [obj]
+        import torch.distributed as dist
+        out = [None] * self.world
+        dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+
+class ShardedBAProblem(_Sharded, BAProblem):
     """BAProblem over this rank's point shard (see module docstring).
 
     comm="torch": ranks are torch.distributed ranks (one process per GPU);
@@ -79,41 +129,17 @@ class ShardedBAProblem(BAProblem):
     def __init__(self, scene, loss=None, optimize_focal: bool = True, shared_focal: bool = False,
                  rank: int | None = None, world: int | None = None, group=None, comm: str = "torch"):
         arr = as_arrays(scene)
-        if rank is None or world is None:
-            import torch.distributed as dist
-            rank, world = dist.get_rank(group), dist.get_world_size(group)
+        rank, world = self._init_shard(rank, world, group, comm)
         if shared_focal and optimize_focal:
             raise ValueError("shared_focal is not supported by the sharded solver")
         local, (p0, p1), obs = shard_arrays(arr, rank, world)
         if local.num_observations == 0:
             raise ValueError(f"rank {rank} owns no observations (world {world} too large for this scene)")
-        super().__init__(local, loss, optimize_focal, shared_focal)
+        BAProblem.__init__(self, local, loss, optimize_focal, shared_focal)
+        self._connected = world == 1
         self.global_arr = arr
-        self.rank, self.world, self.group, self.comm = rank, world, group, comm
         self.point_range = (p0, p1)
         self.obs_index = obs
-        self._connected = world == 1
-
-    def _create(self):
-        h = super()._create()
-        self._native_ptr = h
-        if self.world > 1 and self.comm == "torch":
-            import torch.distributed as dist
-            lib = _native.load()
-            ih = (ct.c_char * 64)()
-            _native.check(lib.ssfm_comm_init(ct.c_void_p(h.ptr), self.rank, self.world, ih, None))
-            handles = [None] * self.world
-            dist.all_gather_object(handles, bytes(ih), group=self.group)
-            blob = b"".join(handles)
-            _native.check(lib.ssfm_comm_connect(ct.c_void_p(h.ptr), ct.c_char_p(blob), None))
-            self._connected = True
-        return h
-
-    def _native_handle(self):
-        h = super()._native_handle()
-        if not self._connected:
-            raise RuntimeError("sharded problem not connected: call connect_local(problems) first")
-        return h
 
     # -- theta between the global layout and this rank's shard ---------------
     def scatter_theta(self, theta_global) -> np.ndarray:
@@ -132,20 +158,8 @@ class ShardedBAProblem(BAProblem):
         if not isinstance(theta_local, np.ndarray):
             theta_local = theta_local.detach().cpu().numpy()
         c = self.num_cameras
-        if shards is None:
-            if self.world == 1:
-                shards_pts = [theta_local[7 * c:7 * c + 3 * self.num_points]]
-            else:
-                import torch.distributed as dist
-                mine = theta_local[7 * c:7 * c + 3 * self.num_points]
-                shards_pts = [None] * self.world
-                dist.all_gather_object(shards_pts, mine, group=self.group)
-        else:
-            shards_pts = []
-            for p, th in sorted(shards, key=lambda s: s[0].rank):
-                th = th if isinstance(th, np.ndarray) else th.detach().cpu().numpy()
-                shards_pts.append(th[7 * c:7 * c + 3 * p.num_points])
-        parts = [theta_local[:7 * c], *shards_pts]
+        pts = lambda p, th: th[7 * c:7 * c + 3 * p.num_points]  # noqa: E731
+        parts = [theta_local[:7 * c], *self._all_gather(pts(self, theta_local), shards, pts)]
         if self.optimize_focal:
             parts.append(theta_local[7 * c + 3 * self.num_points:])
         return np.concatenate(parts)
@@ -154,8 +168,60 @@ class ShardedBAProblem(BAProblem):
         return BAProblem(self.global_arr, self.loss, self.optimize_focal, self.shared_focal).encode()
 
 
+class ShardedGPProblem(_Sharded, GPProblem):
+    """GPProblem over this rank's point shard: every camera (replicated
+    centres, camera-0 gauge), points [p0, p1) renumbered, their observations
+    and per-observation scales. The mean-scale gauge of post_step
+    (gp.py:130-147) is taken over every rank's scales (one exchange of
+    (sum, count))."""
+
+    def __init__(self, base: GPProblem, rank: int | None = None, world: int | None = None, group=None,
+                 comm: str = "torch"):
+        rank, world = self._init_shard(rank, world, group, comm)
+        p0, p1 = shard_ranges(base.pt_idx, base.num_points, world)[rank]
+        obs = np.nonzero((base.pt_idx >= p0) & (base.pt_idx < p1))[0]
+        if len(obs) == 0:
+            raise ValueError(f"rank {rank} owns no observations (world {world} too large for this problem)")
+        GPProblem.__init__(self, base.rays[obs], base.fixed_rotations, base.cam_idx[obs], base.pt_idx[obs] - p0,
+                           p1 - p0, base.loss, base.depth_mode,
+                           None if base.depths is None else base.depths[obs], base.seed)
+        self._connected = world == 1
+        self._gauge_fixed = base.gauge_fixed
+        self.base = base
+        self.point_range = (p0, p1)
+        self.obs_index = obs
+
+    def scatter_theta(self, theta_global) -> np.ndarray:
+        th = np.asarray(theta_global, dtype=np.float64)
+        c, P = self.num_cameras, self.base.num_points
+        p0, p1 = self.point_range
+        parts = [th[:3 * c], th[3 * c + 3 * p0:3 * c + 3 * p1]]
+        if not self.depth_mode:
+            parts.append(th[3 * (c + P):][self.obs_index])
+        return np.concatenate(parts)
+
+    def initial_theta(self) -> np.ndarray:
+        """The base problem's seeded initial theta (gp.py:71-80), this rank's part."""
+        return self.scatter_theta(self.base.initial_theta())
+
+    def gather_theta(self, theta_local, shards=None) -> np.ndarray:
+        if not isinstance(theta_local, np.ndarray):
+            theta_local = theta_local.detach().cpu().numpy()
+        c, P, N = self.num_cameras, self.base.num_points, self.base.num_obs
+        pick = lambda p, th: (th[3 * c:3 * (c + p.num_points)],  # noqa: E731
+                              None if p.depth_mode else (p.obs_index, th[3 * (c + p.num_points):]))
+        got = self._all_gather(pick(self, theta_local), shards, pick)
+        parts = [theta_local[:3 * c], *[g[0] for g in got]]
+        if not self.depth_mode:
+            sc = np.empty(N)
+            for _, (idx, vals) in got:
+                sc[idx] = vals
+            parts.append(sc)
+        return np.concatenate(parts)
+
+
 def connect_local(problems) -> None:
-    """Connect several ShardedBAProblem (ranks 0..R-1 of one scene) living in
+    """Connect several sharded problems (ranks 0..R-1 of one problem) living in
     this process on the current device: exchange regions are plain device
     pointers. Their collective calls must then run concurrently (one host
     thread per problem) and their PCG grids must fit the device together
@@ -166,12 +232,12 @@ def connect_local(problems) -> None:
     for p in problems:
         if p.world != world or p.comm != "local":
             raise ValueError("connect_local needs comm='local' problems of one world")
-        h = BAProblem._native_handle(p)
+        h = _DeviceProblem._native_handle(p)
         reg = ct.c_void_p(0)
         _native.check(lib.ssfm_comm_init(ct.c_void_p(h.ptr), p.rank, world, None, ct.byref(reg)))
         regions[p.rank] = reg.value
     for p in problems:
-        h = BAProblem._native_handle(p)
+        h = _DeviceProblem._native_handle(p)
         _native.check(lib.ssfm_comm_connect(ct.c_void_p(h.ptr), None, regions))
         p._connected = True
 
@@ -187,3 +253,14 @@ def run_ba_sharded(scene, loss=None, config=None, optimize_focal: bool = True, g
     full = prob.gather_theta(th)
     g = BAProblem(prob.global_arr, prob.loss, optimize_focal)
     return g.decode(full), rep
+
+
+def run_gp_sharded(scene, depth_mode: bool = False, loss=None, config=None, seed: int = 0, group=None):
+    """run_gp (gp.py:204-218) over the torch.distributed ranks: every rank
+    returns the gathered global theta and the (identical) SolveReport."""
+    from .gp import fix_gauge, make_rays
+    from .lm import lm_solve
+    base = fix_gauge(make_rays(scene, depth_mode, loss, seed))
+    prob = ShardedGPProblem(base, group=group)
+    th, rep = lm_solve(prob, prob.initial_theta(), config)
+    return prob.gather_theta(th), rep

@@ -93,6 +93,14 @@ def _worker(rank, world, port, q):
         th_l = p.scatter_theta(th_g)
         assert np.array_equal(th_l, p.encode())                  # local layout == local encode
         assert np.array_equal(p.gather_theta(th_l), th_g)        # gloo round trip
+        # GP: scatter / gather of centres, points and per-observation scales
+        import paper_2510_13310_b200 as b2
+        base = b2.fix_gauge(b2.make_rays(st, depth_mode=False, seed=0))
+        gp = bd.ShardedGPProblem(base, rank=rank, world=world)
+        g0 = base.initial_theta()
+        g0[-base.num_obs:] = np.arange(base.num_obs) + 1.0     # distinct scales
+        assert np.array_equal(gp.gather_theta(gp.scatter_theta(g0)), g0)
+        assert np.array_equal(gp.initial_theta(), gp.scatter_theta(base.initial_theta()))
         loc, _, _ = bd.shard_arrays(st, rank, world)
         S, br = camera_schur(prob_of(loc), th_l, 1e-3)
         t = torch.from_numpy(np.concatenate([S.ravel(), br]))

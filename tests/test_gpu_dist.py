@@ -145,3 +145,36 @@ def test_two_processes_ipc(gpu, tmp_path):
     single = b2.BAProblem(st, b2.RobustLoss("huber", 1.0))
     _, rep = b2.lm_solve(single, single.encode(), b2.LMConfig(max_iterations=8))
     assert r0["costs"] == pytest.approx(np.array([i.cost_after for i in rep.iterations]), rel=1e-7)
+
+
+def test_local_gp_shards_match_single_gpu(gpu):
+    """GP (gp.py) sharded by point: scales follow their observations, centres
+    are replicated, the mean-scale gauge is taken over every rank."""
+    _, obs = synth.generate_arrays(synth.SynthConfig(num_cameras=30, num_points=2000, visibility_fraction=5 / 30,
+                                                     pixel_noise_sigma=0.5, seed=2))
+    base = b2.fix_gauge(b2.make_rays(obs, depth_mode=False, loss=b2.RobustLoss("huber", 0.1), seed=0))
+    cfg = b2.LMConfig(max_iterations=15)
+    th1, rep1 = b2.lm_solve(base, base.initial_theta(), cfg)
+    os.environ["SSFM_PCG_SMS"] = "70"
+    try:
+        probs = [bd.ShardedGPProblem(base, rank=r, world=2, comm="local") for r in range(2)]
+        bd.connect_local(probs)
+    finally:
+        os.environ.pop("SSFM_PCG_SMS")
+    out = [None, None]
+
+    def work(r):
+        with gpu.cuda.stream(gpu.cuda.Stream()):
+            out[r] = b2.lm_solve(probs[r], probs[r].initial_theta(), cfg)
+
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(2)]
+    [t.start() for t in ts]
+    [t.join(timeout=300) for t in ts]
+    ra, rb = out[0][1], out[1][1]
+    assert [(i.cost_after, i.cg_iters) for i in ra.iterations] == [(i.cost_after, i.cg_iters) for i in rb.iterations]
+    assert [i.step_accepted for i in ra.iterations] == [i.step_accepted for i in rep1.iterations]
+    for a, b in zip(ra.iterations, rep1.iterations):
+        assert a.cost_after == pytest.approx(b.cost_after, rel=1e-7)
+    full = probs[0].gather_theta(out[0][0], shards=[(p, o[0]) for p, o in zip(probs, out)])
+    C, P = base.num_cameras, base.num_points
+    assert np.abs(full[:3 * (C + P)] - th1[:3 * (C + P)]).max() < 1e-6
