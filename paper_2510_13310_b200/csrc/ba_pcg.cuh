@@ -50,6 +50,7 @@ __device__ __forceinline__ double cta_partials_sum(const double* part, int n, in
 // P1 for a camera vector v -> y (per point): y_j = Cinv_j sum_o Jp^T (Jc v_c)
 __device__ __forceinline__ void ba_point_pass(const BADev& d, const double* v, double* y,
                                               double (*sm)[SSFM_BATCH][3]) {
+  const unsigned long long pstream = pol_evict_first(), pkeep = pol_evict_last();
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -67,8 +68,8 @@ __device__ __forceinline__ void ba_point_pass(const BADev& d, const double* v, d
       if (i < ob1) {
         double J[BA_JREC];
 #pragma unroll
-        for (int k = 0; k < BA_JREC; ++k) J[k] = __ldg(d.Jpm + k * Np + i);
-        const int c = __ldg(d.topo.pm_cam + i);
+        for (int k = 0; k < BA_JREC; ++k) J[k] = ldg_stream(d.Jpm + k * Np + i, pstream);
+        const int c = ldg_stream_i(d.topo.pm_cam + i, pstream);
         double pc[8];
         ld_v4(v + 8ll * c, pc);
         ld_v4(v + 8ll * c + 4, pc + 4);
@@ -93,7 +94,7 @@ __device__ __forceinline__ void ba_point_pass(const BADev& d, const double* v, d
       for (int k = 0; k < 6; ++k) ci[k] = __ldg(d.Cinv + 6ll * my_pt + k);
       sym3_matvec(ci, acc, w);
 #pragma unroll
-      for (int k = 0; k < 3; ++k) y[4ll * my_pt + k] = w[k];
+      for (int k = 0; k < 3; ++k) st_hint(y + 4ll * my_pt + k, w[k], pkeep);
     }
   }
 }
@@ -101,6 +102,7 @@ __device__ __forceinline__ void ba_point_pass(const BADev& d, const double* v, d
 // P2: per camera tile, sum Jc^T (Jp y_j) -> tile8[t][8]
 __device__ __forceinline__ void ba_camera_pass(const BADev& d, const double* y, double* tile8,
                                                double* smred) {
+  const unsigned long long pstream = pol_evict_first(), pkeep = pol_evict_last();
   const long long Np = d.Npad;
   for (int t = blockIdx.x; t < d.topo.nt; t += gridDim.x) {
     const int o0 = __ldg(d.topo.tile_obs + t), o1 = __ldg(d.topo.tile_obs + t + 1);
@@ -111,10 +113,10 @@ __device__ __forceinline__ void ba_camera_pass(const BADev& d, const double* y, 
     if (i < o1) {
       double J[BA_JREC];
 #pragma unroll
-      for (int k = 0; k < BA_JREC; ++k) J[k] = __ldg(d.Jcm + k * Np + i);
-      const int j = __ldg(d.topo.cm_pt + i);
+      for (int k = 0; k < BA_JREC; ++k) J[k] = ldg_stream(d.Jcm + k * Np + i, pstream);
+      const int j = ldg_stream_i(d.topo.cm_pt + i, pstream);
       double yj[4];
-      ld_v4(y + 4ll * j, yj);
+      ld_v4_hint(y + 4ll * j, yj, pkeep);
       double tt[2];
       ba_jp_mul(J, yj, tt);
       ba_jct_mul(J, tt, o);
@@ -141,6 +143,7 @@ __device__ __forceinline__ void ba_fused_pass(const BADev& d, const FusedTopo& f
                                               double (*smy)[SSFM_BATCH][3],
                                               int (*smown)[SSFM_BATCH]) {
   constexpr int G = 8 / SL;
+  const unsigned long long pstream = pol_evict_first();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = blockIdx.x % G, grp = blockIdx.x / G, ngrp = gridDim.x / G;
   const int C = d.bp.C;
@@ -191,7 +194,7 @@ __device__ __forceinline__ void ba_fused_pass(const BADev& d, const FusedTopo& f
       if (i < ob1) {
         c = __ldg(d.topo.pm_cam + i);
 #pragma unroll
-        for (int k = 0; k < BA_JREC; ++k) J[k] = __ldg(d.Jpm + k * Np + i);
+        for (int k = 0; k < BA_JREC; ++k) J[k] = ldg_stream(d.Jpm + k * Np + i, pstream);
         tk = __ldg(fz.tick + i);
         double pc[8];
         ld_v4(v + 8ll * c, pc);
@@ -230,7 +233,7 @@ __device__ __forceinline__ void ba_fused_pass(const BADev& d, const FusedTopo& f
       if (have) {
         if (rounds > 1) {   // a single point with > 32 observations: reload its round
 #pragma unroll
-          for (int k = 0; k < BA_JREC; ++k) J[k] = __ldg(d.Jpm + k * Np + i);
+          for (int k = 0; k < BA_JREC; ++k) J[k] = ldg_stream(d.Jpm + k * Np + i, pstream);
           c = __ldg(d.topo.pm_cam + i);
           tk = __ldg(fz.tick + i);
         }

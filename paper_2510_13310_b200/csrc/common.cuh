@@ -90,6 +90,38 @@ __device__ __forceinline__ void ld_v4(const double* a, double* x) {
                : "=d"(x[0]), "=d"(x[1]), "=d"(x[2]), "=d"(x[3]) : "l"(a));
 }
 
+// L2 eviction policies (createpolicy): the per-observation Jacobian streams
+// through L2 once per pass (evict_first, and no L1 allocation: it lives in
+// registers), while the small per-point / per-camera vectors that are
+// gathered at random (y, p) should survive the stream (evict_last).
+__device__ __forceinline__ unsigned long long pol_evict_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long pol_evict_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double ldg_stream(const double* a, unsigned long long pol) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int ldg_stream_i(const int* a, unsigned long long pol) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void ld_v4_hint(const double* a, double* x, unsigned long long pol) {
+  asm volatile("ld.global.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+               : "=d"(x[0]), "=d"(x[1]), "=d"(x[2]), "=d"(x[3]) : "l"(a), "l"(pol));
+}
+__device__ __forceinline__ void st_hint(double* a, double v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
+}
+
 // Symmetric 3x3 stored as upper triangle {00,01,02,11,12,22}.
 __device__ __forceinline__ void sym3_matvec(const double* m, const double* x, double* y) {
   y[0] = m[0] * x[0] + m[1] * x[1] + m[2] * x[2];

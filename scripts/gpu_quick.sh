@@ -1,2 +1,2 @@
 #!/usr/bin/env bash
-timeout 300 python scripts/dev_shared.py 2>&1 | tail -20
+SSFM_FUSED=0 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct --clock-control none -k regex:ba_k_pcg -c 1 --csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline 2>/dev/null | grep -E "dram__|gpu__time|lts__" 
