@@ -210,6 +210,11 @@ int ssfm_comm_init(ssfm_handle* h, int32_t rank, int32_t nranks, void* ipc_handl
                    void** region_out);
 int ssfm_comm_connect(ssfm_handle* h, const void* ipc_handles, void* const* regions);
 
+/* Diagnostic (BA): number of Jacobian entries where the camera-major copy
+ * (written by the camera-tile linearize pass) differs bitwise from the
+ * point-major copy, after ssfm_linearize. Expected 0. */
+int ssfm_check_jacobian(ssfm_handle* h, int64_t* mismatches, void* stream);
+
 /* Which Schur operator the PCG kernel of this handle runs (no reference
  * counterpart; it replaces the dense S@p of lm.py:656). *slot_groups = 0: the
  * two-pass operator (point-major then camera-major Jacobian reads); >= 1: the

@@ -18,6 +18,7 @@ struct BADev {
   BAParams bp;
   Topo topo;
   const double* pix_pm;   // [2N] interleaved, point-major
+  const double* pix_cm;   // [2N] interleaved, camera-major
   const double* pps;      // [2C]
   const double* dists;    // [2C]
   const double* focals;   // [C] fixed focals (focal_mode 0)
@@ -101,6 +102,20 @@ __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
   atomicMax(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)__double_as_longlong(v));
 }
 
+// One observation's weighted residual, robust cost term and compact Jacobian
+// record. The point-major and camera-major copies of the Jacobian are computed
+// by two kernels from the same inputs with this one expression tree (same
+// rounding and contraction), so they are bit-identical; ssfm_check_jacobian
+// verifies it on the device (tests/test_gpu_ba.py).
+__device__ __forceinline__ void ba_obs_eval(const BAParams& bp, const BACam* __restrict__ cam, const double* X,
+                                         const double* pix, double* r, double* J, double* cost_term) {
+  const BACam cc = *cam;
+  BAProj pr;
+  double sw;
+  ba_residual(bp, cc, X, pix, pr, r, sw, *cost_term);
+  ba_jacobian(bp, cc, pr, sw, J);
+}
+
 // ---------------------------------------------------------------------------
 // linearize (ba.py:140-194) fused with the point side of jtj/jtr
 // (_core.pyx:18-97 for point keys): one warp per point batch.
@@ -133,21 +148,11 @@ __global__ void __launch_bounds__(256) ba_k_linearize(BADev d, const double* __r
       for (int k = 0; k < LIN_V; ++k) val[k] = 0.0;
       if (i < ob1) {
         const int c = d.topo.pm_cam[i], j = d.topo.pm_pt[i];
-        const BACam cc = d.cams[c];
         const double* X = theta + d.bp.off_pts + 3ll * j;
-        BAProj pr;
-        double r[2], sw, ct;
-        ba_residual(d.bp, cc, X, d.pix_pm + 2ll * i, pr, r, sw, ct);
-        double J[BA_JREC];
-        ba_jacobian(d.bp, cc, pr, sw, J);
-        const int ic = d.topo.pm_to_cm[i];
+        double r[2], J[BA_JREC], ct;
+        ba_obs_eval(d.bp, d.cams + c, X, d.pix_pm + 2ll * i, r, J, &ct);
 #pragma unroll
-        for (int k = 0; k < BA_JREC; ++k) {
-          d.Jpm[k * Np + i] = J[k];
-          d.Jcm[k * Np + ic] = J[k];
-        }
-        d.rcm[ic] = r[0];
-        d.rcm[Np + ic] = r[1];
+        for (int k = 0; k < BA_JREC; ++k) d.Jpm[k * Np + i] = J[k];
         // point-side products: Jp^T Jp (upper 6) and Jp^T r
         const double* jp = J + 8;
         val[0] = jp[0] * jp[0] + jp[3] * jp[3];
@@ -222,33 +227,43 @@ __global__ void __launch_bounds__(256) ba_k_linearize(BADev d, const double* __r
 }
 
 // ---------------------------------------------------------------------------
-// camera side of jtj/jtr: per camera tile, sum Jc^T Jc (36 upper) and Jc^T r (8)
+// camera side of linearize + jtj/jtr: per camera tile (one CTA, <= 256
+// observations of one camera, camera-major order) evaluate the observations
+// again with the same compiled body (ba_obs_eval), write the camera-major
+// Jacobian copy and residual coalesced, and reduce the tile's Jc^T Jc (36
+// upper) and Jc^T r (8). Recomputing costs ~2x the linearize flops but
+// replaces 16 scattered 8-byte stores per observation (sector read-modify-
+// write: ~8x the bytes) by coalesced ones.
 // ---------------------------------------------------------------------------
 #define CAM_V 44
-__global__ void __launch_bounds__(SSFM_TILE) ba_k_camred(BADev d) {
+__global__ void __launch_bounds__(SSFM_TILE) ba_k_linearize_cm(BADev d, const double* __restrict__ theta) {
   __shared__ double sm[(SSFM_TILE / 32) * CAM_V];
   const int t = blockIdx.x;
   const int o0 = d.topo.tile_obs[t], o1 = d.topo.tile_obs[t + 1];
+  const int c = d.topo.tile_cam[t];
   const int i = o0 + threadIdx.x;
   double v[CAM_V];
 #pragma unroll
   for (int k = 0; k < CAM_V; ++k) v[k] = 0.0;
   if (i < o1) {
     const long long Np = d.Npad;
-    double J[BA_JREC];
+    const int j = d.topo.cm_pt[i];
+    double r[2], J[BA_JREC], ct;
+    ba_obs_eval(d.bp, d.cams + c, theta + d.bp.off_pts + 3ll * j, d.pix_cm + 2ll * i, r, J, &ct);
 #pragma unroll
-    for (int k = 0; k < BA_JREC; ++k) J[k] = d.Jcm[k * Np + i];
+    for (int k = 0; k < BA_JREC; ++k) d.Jcm[k * Np + i] = J[k];
+    d.rcm[i] = r[0];
+    d.rcm[Np + i] = r[1];
     double a[8], b[8];
     ba_jc_row(J, 0, a);
     ba_jc_row(J, 1, b);
-    const double r0 = d.rcm[i], r1 = d.rcm[Np + i];
     int idx = 0;
 #pragma unroll
     for (int p = 0; p < 8; ++p)
 #pragma unroll
       for (int q = p; q < 8; ++q) v[idx++] = a[p] * a[q] + b[p] * b[q];
 #pragma unroll
-    for (int p = 0; p < 8; ++p) v[36 + p] = a[p] * r0 + b[p] * r1;
+    for (int p = 0; p < 8; ++p) v[36 + p] = a[p] * r[0] + b[p] * r[1];
   }
   block_reduce<CAM_V>(v, sm);
   if (threadIdx.x == 0) {
@@ -258,7 +273,6 @@ __global__ void __launch_bounds__(SSFM_TILE) ba_k_camred(BADev d) {
   }
 }
 
-// per camera: sum tile partials in tile order -> Bc (full 8x8), gcam
 // per camera: sum of its tile partials in tile order (the local part of a
 // camera block when the observations are sharded over ranks)
 __global__ void k_cam_tilesum(const Topo T, const double* __restrict__ tilebuf, int V, double* camsum) {
@@ -674,4 +688,16 @@ __global__ void ba_k_renorm(int C, double* theta, int* status) {
   if (n < 1e-12) { atomicOr(status, ST_ZERO_QUAT); return; }
 #pragma unroll
   for (int k = 0; k < 4; ++k) q[k] = DIV(q[k], n);
+}
+
+// diagnostic: count (observation, entry) pairs where the camera-major copy of
+// the Jacobian differs from the point-major one (bitwise)
+__global__ void k_check_jcopies(BADev d, unsigned long long* mism) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= d.topo.N) return;
+  const int ic = d.topo.pm_to_cm[i];
+  int bad = 0;
+  for (int k = 0; k < BA_JREC; ++k)
+    bad += __double_as_longlong(d.Jpm[k * d.Npad + i]) != __double_as_longlong(d.Jcm[k * d.Npad + ic]);
+  if (bad) atomicAdd(mism, (unsigned long long)bad);
 }

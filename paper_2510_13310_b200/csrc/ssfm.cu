@@ -381,6 +381,10 @@ extern "C" int ssfm_create_ba(const ssfm_ba_desc* desc, void* stream, ssfm_handl
   if ((rc = dalloc(h, &dists, 2 * C))) return fail(rc);
   if ((rc = dalloc(h, &focals, C))) return fail(rc);
   k_gather_rows<<<nblk(N, 256), 256, 0, st>>>(desc->pixels, T.pm_obs, N, 2, pix_pm);
+  double* pix_cm;
+  if ((rc = dalloc(h, &pix_cm, 2 * N))) return fail(rc);
+  k_gather_rows<<<nblk(N, 256), 256, 0, st>>>(desc->pixels, T.cm_obs, N, 2, pix_cm);
+  d.pix_cm = pix_cm;
   if (cudaMemcpyAsync(pps, desc->pps, sizeof(double) * 2 * C, cudaMemcpyDeviceToDevice, st) ||
       cudaMemcpyAsync(dists, desc->dists, sizeof(double) * 2 * C, cudaMemcpyDeviceToDevice, st))
     return fail(set_err(SSFM_CUDA_ERROR, "copy camera intrinsics"));
@@ -687,7 +691,7 @@ static int launch_linearize(ssfm_handle* h, const double* theta, double* r_out, 
     BADev& d = h->ba;
     ba_k_prep<<<h->cam_blocks, 256, 0, st>>>(d, theta);
     ba_k_linearize<<<h->lin_blocks, 256, 0, st>>>(d, theta, r_out, J_out, h->red);
-    if (d.topo.nt) ba_k_camred<<<d.topo.nt, SSFM_TILE, 0, st>>>(d);
+    if (d.topo.nt) ba_k_linearize_cm<<<d.topo.nt, SSFM_TILE, 0, st>>>(d, theta);
     if (!sharded(h)) {
       ba_k_camfin<<<h->cam_blocks, 256, 0, st>>>(d, h->red + (long long)h->lin_blocks * 8, nullptr);
       k_sum_partials<<<1, 1024, 0, st>>>(h->red, h->lin_blocks * 8 + h->cam_blocks, d.scal + SC_GNORM2);
@@ -1155,6 +1159,24 @@ extern "C" int ssfm_comm_connect(ssfm_handle* h, const void* ipc_handles, void* 
     cm.buf[r] = reinterpret_cast<double*>(static_cast<char*>(ptr) + 256);
   }
   cm.nranks = R;
+  return SSFM_OK;
+}
+
+extern "C" int ssfm_check_jacobian(ssfm_handle* h, int64_t* mismatches, void* stream) {
+  if (!h || !mismatches) return set_err(SSFM_INVALID_ARGUMENT, "null argument");
+  if (h->kind != 0) return set_err(SSFM_INVALID_ARGUMENT, "BA handles only");
+  if (!h->linearized) return set_err(SSFM_INVALID_ARGUMENT, "ssfm_check_jacobian before ssfm_linearize");
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long* dm = nullptr;
+  CU(cudaMalloc(&dm, sizeof(unsigned long long)));
+  CU(cudaMemsetAsync(dm, 0, sizeof(unsigned long long), st));
+  k_check_jcopies<<<nblk(h->topo.N, 256), 256, 0, st>>>(h->ba, dm);
+  unsigned long long hm = 0;
+  cudaMemcpyAsync(&hm, dm, sizeof(hm), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  cudaFree(dm);
+  CU(cudaGetLastError());
+  *mismatches = (int64_t)hm;
   return SSFM_OK;
 }
 

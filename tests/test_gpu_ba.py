@@ -366,3 +366,16 @@ def test_shared_focal_vs_reference(gpu):          # test_ba.py:225-230 + the sha
     assert np.all(est.focals == est.focals[0])
     _, al = synth.align(est, tru, "sim3")
     assert np.abs(al.points - tru.points).max() < 1e-8 * synth.scene_diameter(tru)
+
+
+@pytest.mark.parametrize("name", BA_GOLDENS + ["ba_shared.npz"])
+def test_jacobian_copies_bitwise_identical(gpu, name):
+    """The camera-major Jacobian copy (camera-tile linearize pass) equals the
+    point-major one bit for bit: one expression tree, same inputs."""
+    z = golden(name)
+    p = problem_from_golden(z)
+    p.gradient(z["theta0"] * (1 + 1e-3 * np.sin(np.arange(len(z["theta0"])))))
+    m = ct.c_int64(-1)
+    _native.check(_native.load().ssfm_check_jacobian(ct.c_void_p(p._native_handle().ptr), ct.byref(m),
+                                                     ct.c_void_p(gpu.cuda.current_stream().cuda_stream)))
+    assert m.value == 0
