@@ -47,7 +47,11 @@ CONFIGS = {
     "c3": (1700, 150000, 5, 1.0, 1.0, "synthetic BA 1.7k cams / 150k pts / 750k obs (C3 shape)"),
     "c4ba": (1000, 500000, 8, 1.0, 1.0, "synthetic BA 1k cams / 500k pts / 4M obs (C4 BA stage)"),
     "c5": (5000, 2000000, 10, 1.0, 1.0, "synthetic large-scale BA 5000 cams / 2M pts / 20M obs (C5)"),
+    # global positioning (gp.py): rays from the observed scene, Huber 0.1, seeded init
+    "c2gp": (200, 50000, 6, 0.5, 0.1, "synthetic GP 200 cams / 50k pts / 300k obs, per-observation scales (C2)"),
+    "c4gp": (1000, 500000, 8, 1.0, 0.1, "synthetic GP 1k cams / 500k pts / 4M obs (C4 GP stage)"),
 }
+GP_CONFIGS = {"c2gp", "c4gp"}
 # bounded CPU sample of the C5 shape for the reference (same k = 10 views per point)
 REF_SAMPLE = (1000, 40000, 10)
 METRIC = "BA/GP LM iteration time and observations/sec at 1/2/4/8 B200 vs CPU ref"
@@ -183,14 +187,23 @@ def run_b200(args, ws, rank, local):
     # cameras replicated, camera sums exchanged through peer memory (dist.py)
     from paper_2510_13310_b200 import dist as bdist
 
+    is_gp = args.config in GP_CONFIGS
+    gp_base = b2.fix_gauge(b2.make_rays(arr, depth_mode=False, loss=loss, seed=0)) if is_gp else None
+
     def make_problem():
+        if is_gp:
+            return bdist.ShardedGPProblem(gp_base, rank=rank, world=ws) if ws > 1 else \
+                b2.fix_gauge(b2.make_rays(arr, depth_mode=False, loss=loss, seed=0))
         if ws > 1:
             return bdist.ShardedBAProblem(arr, loss, rank=rank, world=ws)
         return b2.BAProblem(arr, loss)
 
+    def theta_start(p):
+        return p.initial_theta() if is_gp else p.encode()
+
     problem = make_problem()
     Nl, Pl = problem.num_obs, problem.num_points
-    theta0 = torch.as_tensor(problem.encode()).cuda()
+    theta0 = torch.as_tensor(theta_start(problem)).cuda()
     h = problem._native_handle()
     lib = _native.load()
     t_setup = time.time()
@@ -250,13 +263,15 @@ def run_b200(args, ws, rank, local):
 
     # roofline of the dominant kernel: the PCG solve (ba_k_pcg), S*p dominated
     peak, peak_kind = peaks()
-    bytes_per_cg = 136.0 * Nl + 72.0 * Pl + 128.0 * C        # SURVEY.md 8(d), S*p per CG iteration (this rank)
+    # SURVEY.md 8(d), S*p per CG iteration (this rank)
+    bytes_per_cg = (40.0 * Nl + 72.0 * Pl + 48.0 * C) if is_gp else (136.0 * Nl + 72.0 * Pl + 128.0 * C)
     roof = None
     if pms.value > 0 and cgit.value > 0:
         ach = bytes_per_cg * cgit.value / (pms.value / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "traffic": None, "peak_source": peak_kind,
-                "kernel": "ba_k_pcg", "launches": int(pl.value), "cg_iters": int(cgit.value),
+                "kernel": "gp_k_pcg" if is_gp else "ba_k_pcg", "launches": int(pl.value),
+                "cg_iters": int(cgit.value),
                 "kernel_ms": round(pms.value, 3),
                 "algorithmic_bytes_per_cg_iter": bytes_per_cg,
                 "kernel_share_of_step": round(pms.value / max(ms_total, 1e-9), 4)}
@@ -265,7 +280,7 @@ def run_b200(args, ws, rank, local):
     # ---- end to end through the public API from host arrays
     e2e = None
     if not args.no_e2e:
-        theta_host = problem.encode()
+        theta_host = theta_start(problem)
         barrier()
         t_a = time.perf_counter()
         e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -281,7 +296,7 @@ def run_b200(args, ws, rank, local):
             t = torch.tensor([wall], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             wall = float(t.item())
-        h2d = (Nl * (4 + 4 + 16) + C * (16 + 16 + 8) + theta_host.nbytes)
+        h2d = (Nl * (4 + 4 + (24 if is_gp else 16)) + C * (16 + 16 + 8) + theta_host.nbytes)
         e2e = {"value": N * its / wall, "unit": "obs/s",
                "h2d_bytes_per_step": int(h2d / its), "d2h_bytes_per_step": int(theta_host.nbytes / its),
                "iterations": its, "wall_s": round(wall, 3), "device_ms": round(e_ms, 1),
@@ -293,6 +308,7 @@ def run_b200(args, ws, rank, local):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": label, "cameras": C, "points": P, "observations": N,
                    "views_per_point": k, "loss": f"huber({delta})", "lm": "LMConfig() defaults",
+                   "problem": "gp" if is_gp else "ba",
                    "parallelism": f"points sharded over {ws} GPUs" if ws > 1 else "single",
                    "observations_per_rank": Nl,
                    "l2": "inputs larger than L2 (J 2x2.56 GB)" if N >= 10**6 else "small (latency bound)"},
@@ -300,7 +316,7 @@ def run_b200(args, ws, rank, local):
         "lm_ms_per_iteration": [round(i.device_ms, 3) for i in rep_t.iterations],
         "roofline": roof, "e2e": e2e, "clocks": clocks, "gpu_launches": int(launches.value),
     }
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline and not is_gp:
         result["cpu_baseline"] = cpu_baseline_sample(max_iterations=4)
     if dist is not None:
         dist.barrier()

@@ -38,6 +38,8 @@ struct GPDev {
   Topo topo;
   const double* ray_pm;   // [3N] point-major rays
   const double* dep_pm;   // [N] point-major ray depths (depth mode)
+  const double* ray_cm;   // [3N] camera-major rays
+  const double* dep_cm;   // [N] camera-major ray depths (depth mode)
   double* Jpm;            // [4 * Npad]
   double* Jcm;            // [4 * Npad]
   double* rcm;            // [3 * Npad]
@@ -73,15 +75,15 @@ __device__ __forceinline__ double gp_inv(double lam, const double* rec) {
   return D == 0.0 ? 0.0 : 1.0 / D;
 }
 
-// residual block of one observation (gp.py:96-107), numpy operation order
-__device__ __forceinline__ void gp_residual(const GPDev& g, long long i, const double* __restrict__ theta,
-                                            double span[3], double blk[3], double& dsc, double& s) {
-  const int c = g.topo.pm_cam[i], j = g.topo.pm_pt[i];
+// residual block of one observation (gp.py:96-107), numpy operation order;
+// camera c, point j, original observation o, its ray v and depth
+__device__ __forceinline__ void gp_residual_at(const GPDev& g, int c, int j, int o, const double* v, double dep,
+                                               const double* __restrict__ theta, double span[3], double blk[3],
+                                               double& dsc, double& s) {
   const double* X = theta + g.gp.off_pts + 3ll * j;
   const double* t = theta + 3ll * c;
-  if (g.gp.depth_mode) dsc = DIV(1.0, g.dep_pm[i]);
-  else dsc = theta[g.gp.off_sc + g.topo.pm_obs[i]];
-  const double* v = g.ray_pm + 3 * i;
+  if (g.gp.depth_mode) dsc = DIV(1.0, dep);
+  else dsc = theta[g.gp.off_sc + o];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     span[k] = SUB(X[k], t[k]);
@@ -89,6 +91,31 @@ __device__ __forceinline__ void gp_residual(const GPDev& g, long long i, const d
   }
   // np.einsum("ni,ni->n") evaluates (b0 b0 + b2 b2) + b1 b1 for 3 terms
   s = ADD(ADD(MUL(blk[0], blk[0]), MUL(blk[2], blk[2])), MUL(blk[1], blk[1]));
+}
+
+// point-major observation i
+__device__ __forceinline__ void gp_residual(const GPDev& g, long long i, const double* __restrict__ theta,
+                                            double span[3], double blk[3], double& dsc, double& s) {
+  gp_residual_at(g, g.topo.pm_cam[i], g.topo.pm_pt[i], g.topo.pm_obs[i], g.ray_pm + 3 * i,
+                 g.gp.depth_mode ? g.dep_pm[i] : 0.0, theta, span, blk, dsc, s);
+}
+
+// compact record {a, g}, weighted residual and b_o = -(g . r) of one
+// observation (gp.py:109-128); shared by the point-major and camera-major
+// linearize passes (one expression tree -> bit-identical copies)
+__device__ __forceinline__ void gp_record(const GPDev& g, int c, const double span[3], const double blk[3],
+                                          double d, double s, double rec[4], double r[3], double& bo) {
+  double cst, w;
+  robust(g.gp.loss_kind, g.gp.delta, s, cst, w);
+  const double sw = __dsqrt_rn(w);
+  rec[0] = d * sw;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    rec[1 + k] = g.gp.depth_mode ? 0.0 : -span[k] * sw;
+    r[k] = MUL(blk[k], sw);
+  }
+  bo = -(rec[1] * r[0] + rec[2] * r[1] + rec[3] * r[2]);
+  (void)c;
 }
 
 __global__ void gp_k_cost(GPDev g, const double* __restrict__ theta, double* partials) {
@@ -126,32 +153,16 @@ __global__ void __launch_bounds__(256) gp_k_linearize(GPDev g, const double* __r
       const int i = base + lane;
       double val[GPL_V] = {0.0, 0.0, 0.0, 0.0};
       if (i < ob1) {
-        double span[3], blk[3], d, s, cst, w;
+        double span[3], blk[3], d, s;
         gp_residual(g, i, theta, span, blk, d, s);
-        robust(g.gp.loss_kind, g.gp.delta, s, cst, w);
-        const double sw = __dsqrt_rn(w);
         const int c = g.topo.pm_cam[i];
-        const double a = d * sw;
+        double rec[4], r[3], bo;
+        gp_record(g, c, span, blk, d, s, rec, r, bo);
+        const double a = rec[0];
         const double at = gp_at(g, c, a);
-        double rec[4];
-        rec[0] = a;
-        double r[3];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          rec[1 + k] = g.gp.depth_mode ? 0.0 : -span[k] * sw;
-          r[k] = MUL(blk[k], sw);
-        }
-        const double bo = -(rec[1] * r[0] + rec[2] * r[1] + rec[3] * r[2]);
-        const int ic = g.topo.pm_to_cm[i];
-#pragma unroll
-        for (int k = 0; k < GP_JREC; ++k) {
-          g.Jpm[k * Np + i] = rec[k];
-          g.Jcm[k * Np + ic] = rec[k];
-        }
-#pragma unroll
-        for (int k = 0; k < 3; ++k) g.rcm[k * Np + ic] = r[k];
+        for (int k = 0; k < GP_JREC; ++k) g.Jpm[k * Np + i] = rec[k];
         g.bo_pm[i] = bo;
-        g.bo_cm[ic] = bo;
         const int o = g.topo.pm_obs[i];
         if (!g.gp.depth_mode) {
           g.gsc[o] = -bo;    // squared norm summed by gp_k_scale_norm
@@ -209,9 +220,12 @@ __global__ void __launch_bounds__(256) gp_k_linearize(GPDev g, const double* __r
   }
 }
 
-// camera side at linearize: sum a_t^2 and sum a_t r (J^T r camera part)
+// camera side at linearize, per camera tile (camera-major): evaluate the
+// observations again with the same expressions, write the camera-major
+// record / residual / b_o copies coalesced, and reduce sum a_t^2 and
+// sum a_t r (J^T r camera part). Replaces scattered 8-byte stores.
 #define GPC_V 4
-__global__ void __launch_bounds__(SSFM_TILE) gp_k_camred(GPDev g) {
+__global__ void __launch_bounds__(SSFM_TILE) gp_k_linearize_cm(GPDev g, const double* __restrict__ theta) {
   __shared__ double sm[(SSFM_TILE / 32) * GPC_V];
   const int t = blockIdx.x;
   const int o0 = g.topo.tile_obs[t], o1 = g.topo.tile_obs[t + 1];
@@ -220,10 +234,20 @@ __global__ void __launch_bounds__(SSFM_TILE) gp_k_camred(GPDev g) {
   double v[GPC_V] = {0.0, 0.0, 0.0, 0.0};
   if (i < o1) {
     const long long Np = g.Npad;
-    const double at = gp_at(g, c, g.Jcm[i]);
+    double span[3], blk[3], d, s;
+    gp_residual_at(g, c, g.topo.cm_pt[i], g.topo.cm_obs[i], g.ray_cm + 3ll * i,
+                   g.gp.depth_mode ? g.dep_cm[i] : 0.0, theta, span, blk, d, s);
+    double rec[4], r[3], bo;
+    gp_record(g, c, span, blk, d, s, rec, r, bo);
+#pragma unroll
+    for (int k = 0; k < GP_JREC; ++k) g.Jcm[k * Np + i] = rec[k];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) g.rcm[k * Np + i] = r[k];
+    g.bo_cm[i] = bo;
+    const double at = gp_at(g, c, rec[0]);
     v[0] = at * at;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) v[1 + k] = at * g.rcm[k * Np + i];
+    for (int k = 0; k < 3; ++k) v[1 + k] = at * r[k];
   }
   block_reduce<GPC_V>(v, sm);
   if (threadIdx.x == 0) {
@@ -845,7 +869,7 @@ static inline int gp_nblk(long long n, int t) { return (int)((n + t - 1) / t); }
 static int gp_launch_linearize(GPDev& g, const double* theta, double* r_out, double* J_out,
                                double* red, int lin_blocks, int cam_blocks, cudaStream_t st) {
   gp_k_linearize<<<lin_blocks, 256, 0, st>>>(g, theta, r_out, J_out, red);
-  if (g.topo.nt) gp_k_camred<<<g.topo.nt, SSFM_TILE, 0, st>>>(g);
+  if (g.topo.nt) gp_k_linearize_cm<<<g.topo.nt, SSFM_TILE, 0, st>>>(g, theta);
   const long long off = (long long)lin_blocks * 8;
   gp_k_camfin<<<cam_blocks, 256, 0, st>>>(g, red + off, nullptr);
   const int sb = gp_nblk(g.topo.N, 256);

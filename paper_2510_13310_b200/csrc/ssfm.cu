@@ -481,6 +481,14 @@ extern "C" int ssfm_create_gp(const ssfm_gp_desc* desc, void* stream, ssfm_handl
     k_gather_rows<<<nblk(N, 256), 256, 0, st>>>(desc->depths, T.pm_obs, N, 1, dep_pm);
   }
   g.ray_pm = ray_pm; g.dep_pm = dep_pm;
+  double *ray_cm, *dep_cm = nullptr;
+  if ((rc = dalloc(h, &ray_cm, 3 * N))) return fail(rc);
+  k_gather_rows<<<nblk(N, 256), 256, 0, st>>>(desc->rays, T.cm_obs, N, 3, ray_cm);
+  if (desc->depth_mode) {
+    if ((rc = dalloc(h, &dep_cm, N))) return fail(rc);
+    k_gather_rows<<<nblk(N, 256), 256, 0, st>>>(desc->depths, T.cm_obs, N, 1, dep_cm);
+  }
+  g.ray_cm = ray_cm; g.dep_cm = dep_cm;
   if ((rc = dalloc(h, &g.Jpm, GP_JREC * g.Npad))) return fail(rc);
   if ((rc = dalloc(h, &g.Jcm, GP_JREC * g.Npad))) return fail(rc);
   if ((rc = dalloc(h, &g.rcm, 3 * g.Npad))) return fail(rc);
@@ -720,7 +728,7 @@ static int launch_linearize(ssfm_handle* h, const double* theta, double* r_out, 
     } else {
       // camera sums exchanged; |g|^2 = (points + scales: summed over ranks) + cameras
       gp_k_linearize<<<h->lin_blocks, 256, 0, st>>>(g, theta, r_out, J_out, h->red);
-      if (g.topo.nt) gp_k_camred<<<g.topo.nt, SSFM_TILE, 0, st>>>(g);
+      if (g.topo.nt) gp_k_linearize_cm<<<g.topo.nt, SSFM_TILE, 0, st>>>(g, theta);
       k_cam_tilesum<<<h->cam_blocks, 256, 0, st>>>(g.topo, g.tilebuf, GPC_V, h->camsum);
       int rc = allreduce(h, h->camsum, (long long)GPC_V * g.gp.C, AR_SUM, st);
       if (rc) return rc;
