@@ -215,6 +215,12 @@ int ssfm_comm_connect(ssfm_handle* h, const void* ipc_handles, void* const* regi
  * point-major copy, after ssfm_linearize. Expected 0. */
 int ssfm_check_jacobian(ssfm_handle* h, int64_t* mismatches, void* stream);
 
+/* Diagnostic (BA): mean time (ms) of one standalone launch of a pass of the
+ * two-pass Schur operator over the current linearization, reps launches after
+ * warm-up. which: 0 = point pass (Jpm, p gather -> y), 1 = camera pass (Jcm,
+ * y gather -> tile sums). Call after ssfm_solve_normal. */
+int ssfm_bench_operator(ssfm_handle* h, int32_t which, int32_t reps, double* ms_out, void* stream);
+
 /* Which Schur operator the PCG kernel of this handle runs (no reference
  * counterpart; it replaces the dense S@p of lm.py:656). *slot_groups = 0: the
  * two-pass operator (point-major then camera-major Jacobian reads); >= 1: the

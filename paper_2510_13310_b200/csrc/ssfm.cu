@@ -1188,6 +1188,32 @@ extern "C" int ssfm_check_jacobian(ssfm_handle* h, int64_t* mismatches, void* st
   return SSFM_OK;
 }
 
+extern "C" int ssfm_bench_operator(ssfm_handle* h, int32_t which, int32_t reps, double* ms_out, void* stream) {
+  if (!h || !ms_out || reps < 1) return set_err(SSFM_INVALID_ARGUMENT, "bad argument");
+  if (h->kind != 0) return set_err(SSFM_INVALID_ARGUMENT, "BA handles only");
+  cudaStream_t st = (cudaStream_t)stream;
+  int occ = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, which == 0 ? (const void*)k_op_point : (const void*)k_op_camera,
+                                                   PCG_THREADS, 0));
+  const int grid = std::max(1, occ) * h->num_sms;
+  BADev& d = h->ba;
+  for (int w = 0; w < 2; ++w) {   // warm-up
+    if (which == 0) k_op_point<<<grid, PCG_THREADS, 0, st>>>(d, h->p, d.yv);
+    else k_op_camera<<<grid, PCG_THREADS, 0, st>>>(d, d.yv, d.tilebuf);
+  }
+  CU(cudaEventRecord(h->ev0, st));
+  for (int k = 0; k < reps; ++k) {
+    if (which == 0) k_op_point<<<grid, PCG_THREADS, 0, st>>>(d, h->p, d.yv);
+    else k_op_camera<<<grid, PCG_THREADS, 0, st>>>(d, d.yv, d.tilebuf);
+  }
+  CU(cudaEventRecord(h->ev1, st));
+  CU(cudaEventSynchronize(h->ev1));
+  float ms = 0.f;
+  CU(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  *ms_out = ms / reps;
+  return SSFM_OK;
+}
+
 extern "C" int ssfm_operator_info(const ssfm_handle* h, int32_t* slot_groups, int32_t* grid,
                                   int32_t* threads, int64_t* smem_bytes) {
   if (!h) return set_err(SSFM_INVALID_ARGUMENT, "null argument");
