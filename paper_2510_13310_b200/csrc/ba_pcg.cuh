@@ -483,3 +483,14 @@ ba_k_pcg(BADev d, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg
     if (flag) atomicOr(d.status, flag);
   }
 }
+
+// Diagnostic wrappers: the two passes of the two-pass operator as standalone
+// kernels (per-pass timing and roofline, ssfm_bench_operator).
+__global__ void __launch_bounds__(PCG_THREADS, 4) k_op_point(BADev d, const double* v, double* y) {
+  __shared__ double smp[PCG_THREADS / 32][SSFM_BATCH][3];
+  ba_point_pass(d, v, y, smp);
+}
+__global__ void __launch_bounds__(PCG_THREADS, 4) k_op_camera(BADev d, const double* y, double* tile8) {
+  __shared__ double smred[(PCG_THREADS / 32) * 8];
+  ba_camera_pass(d, y, tile8, smred);
+}
