@@ -210,6 +210,11 @@ int ssfm_comm_init(ssfm_handle* h, int32_t rank, int32_t nranks, void* ipc_handl
                    void** region_out);
 int ssfm_comm_connect(ssfm_handle* h, const void* ipc_handles, void* const* regions);
 
+/* reproj_rmse statistics (synth_metrics.py:312-325) on the device: sum of
+ * squared (unweighted) pixel errors and the number of observations in front of
+ * their camera, for theta (device). rmse = sqrt(*sum_sq / *count). BA only. */
+int ssfm_reproj_stats(ssfm_handle* h, const double* theta, double* sum_sq, int64_t* count, void* stream);
+
 /* Diagnostic (BA): number of Jacobian entries where the camera-major copy
  * (written by the camera-tile linearize pass) differs bitwise from the
  * point-major copy, after ssfm_linearize. Expected 0. */

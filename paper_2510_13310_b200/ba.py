@@ -99,6 +99,15 @@ class _DeviceProblem:
             self._jac = BlockSparseJacobian.allocate(self.layout, self._res_ids(), self._param_ids())
         return self._jac
 
+    def release(self) -> None:
+        """Free the device arena now (instead of at garbage collection), e.g.
+        between the GP and BA stages of the pipeline."""
+        h = self._native_ptr
+        self._native_ptr = None
+        if h is not None and h.ptr:
+            _native.load().ssfm_destroy(ct.c_void_p(h.ptr))
+            h.ptr = 0
+
     def device_bytes(self) -> int:
         return int(_native.load().ssfm_device_bytes(ct.c_void_p(self._native_handle().ptr)))
 

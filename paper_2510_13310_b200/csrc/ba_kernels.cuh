@@ -85,6 +85,28 @@ __global__ void ba_k_cost(BADev d, const double* __restrict__ theta, double* par
   if (threadIdx.x == 0) partials[blockIdx.x] = v[0];
 }
 
+// reproj_rmse statistics (synth_metrics.py:312-325): unweighted squared
+// pixel error and count over observations in front of their camera; block
+// partials [2 * block] summed in fixed order by the host entry point.
+__global__ void ba_k_reproj(BADev d, const double* __restrict__ theta, double* partials) {
+  __shared__ double sm[64];
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  double v[2] = {0.0, 0.0};
+  if (i < d.topo.N) {
+    const int c = d.topo.pm_cam[i], j = d.topo.pm_pt[i];
+    const BACam cc = d.cams[c];
+    BAProj pr;
+    ba_project(cc, theta + d.bp.off_pts + 3ll * j, d.bp.model, pr);
+    if (pr.mask) {
+      const double d0 = SUB(pr.uv[0], d.pix_pm[2 * i]), d1 = SUB(pr.uv[1], d.pix_pm[2 * i + 1]);
+      v[0] = ADD(MUL(d0, d0), MUL(d1, d1));
+      v[1] = 1.0;
+    }
+  }
+  block_reduce<2>(v, sm);
+  if (threadIdx.x == 0) { partials[2ll * blockIdx.x] = v[0]; partials[2ll * blockIdx.x + 1] = v[1]; }
+}
+
 // Sum n partials in fixed order with one block (deterministic).
 __global__ void k_sum_partials(const double* __restrict__ partials, int n, double* out) {
   __shared__ double sm[32];

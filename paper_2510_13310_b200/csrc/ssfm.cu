@@ -1214,6 +1214,38 @@ extern "C" int ssfm_bench_operator(ssfm_handle* h, int32_t which, int32_t reps, 
   return SSFM_OK;
 }
 
+__global__ void k_sum_pairs(const double* __restrict__ part, int n, double* out) {
+  __shared__ double sm[64];
+  double v[2] = {0.0, 0.0};
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int a = threadIdx.x * per, b = min(n, a + per);
+  for (int k = a; k < b; ++k) { v[0] += part[2ll * k]; v[1] += part[2ll * k + 1]; }
+  block_reduce<2>(v, sm);
+  if (threadIdx.x == 0) { out[0] = v[0]; out[1] = v[1]; }
+}
+
+extern "C" int ssfm_reproj_stats(ssfm_handle* h, const double* theta, double* sum_sq, int64_t* count,
+                                 void* stream) {
+  if (!h || !theta) return set_err(SSFM_INVALID_ARGUMENT, "null argument");
+  if (h->kind != 0) return set_err(SSFM_INVALID_ARGUMENT, "BA handles only");
+  cudaStream_t st = (cudaStream_t)stream;
+  BADev& d = h->ba;
+  const int nb = nblk(h->topo.N, 256);
+  double* part = nullptr;
+  CU(cudaMalloc(&part, sizeof(double) * (2ll * nb + 2)));
+  ba_k_prep<<<h->cam_blocks, 256, 0, st>>>(d, theta);
+  ba_k_reproj<<<nb, 256, 0, st>>>(d, theta, part);
+  k_sum_pairs<<<1, 1024, 0, st>>>(part, nb, part + 2ll * nb);
+  double hv[2] = {0.0, 0.0};
+  cudaMemcpyAsync(hv, part + 2ll * nb, sizeof(hv), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  cudaFree(part);
+  CU(cudaGetLastError());
+  if (sum_sq) *sum_sq = hv[0];
+  if (count) *count = (int64_t)hv[1];
+  return SSFM_OK;
+}
+
 extern "C" int ssfm_operator_info(const ssfm_handle* h, int32_t* slot_groups, int32_t* grid,
                                   int32_t* threads, int64_t* smem_bytes) {
   if (!h) return set_err(SSFM_INVALID_ARGUMENT, "null argument");

@@ -1,0 +1,74 @@
+"""Global SfM solve stage: GP then BA on the device.
+
+The reference has no pipeline function; SPEC's global SfM loop runs global
+positioning (gp.py:204-218, rotations fixed) and then bundle adjustment
+(ba.py:264-271) on the GP output, sharing one workspace. Here both stages
+stay on the device: GP writes its centres and points into a copy of the scene
+(rotations and focals untouched, exactly run_gp), BA starts from it. The GP
+handle is released before the BA handle is created, so the two stages reuse
+the same HBM (the "unified memory pool" of PAPER.md:165).
+"""
+
+from __future__ import annotations
+
+import ctypes as ct
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .ba import BAProblem
+from .gp import fix_gauge, make_rays
+from .lm import LMConfig, SolveReport, _stream, _torch, lm_solve
+from .scene import RobustLoss, SceneArrays, as_arrays
+
+
+@dataclass
+class PipelineReport:
+    gp: SolveReport
+    ba: SolveReport
+    rmse_after_gp: float
+    rmse_after_ba: float
+
+
+def reproj_stats(problem: BAProblem, theta) -> tuple[float, int]:
+    """(sum of squared pixel errors, number of observations in front of their
+    camera) on the device (the numerator / denominator of synth_metrics
+    reproj_rmse, synth_metrics.py:312-325)."""
+    torch = _torch()
+    t = problem._theta_dev(torch, theta)
+    s, n = ct.c_double(0.0), ct.c_int64(0)
+    _native.check(_native.load().ssfm_reproj_stats(ct.c_void_p(problem._native_handle().ptr),
+                                                   ct.c_void_p(t.data_ptr()), ct.byref(s), ct.byref(n),
+                                                   _stream(torch)))
+    return float(s.value), int(n.value)
+
+
+def reproj_rmse_device(problem: BAProblem, theta) -> float:
+    s, n = reproj_stats(problem, theta)
+    return float(np.sqrt(s / n)) if n else float("nan")
+
+
+def run_global_sfm(scene, gp_loss: RobustLoss | None = None, ba_loss: RobustLoss | None = None,
+                   gp_config: LMConfig | None = None, ba_config: LMConfig | None = None, seed: int = 0,
+                   optimize_focal: bool = True):
+    """GP (Huber 0.1 by default, seeded init, gauge fixed) then BA (Huber 1.0)
+    on the GP output. Returns (scene, PipelineReport)."""
+    arr = as_arrays(scene)
+    gp_loss = gp_loss or RobustLoss("huber", 0.1)
+    ba_loss = ba_loss or RobustLoss("huber", 1.0)
+    gp = fix_gauge(make_rays(arr, depth_mode=False, loss=gp_loss, seed=seed))
+    th_gp, rep_gp = lm_solve(gp, gp.initial_theta(), gp_config or LMConfig(max_iterations=20))
+    centers, points, _ = gp.views(th_gp)
+    mid = arr.copy()
+    mid.centers = np.array(centers, dtype=np.float64)
+    mid.points = np.array(points, dtype=np.float64)
+    gp.release()
+    ba = BAProblem(mid, ba_loss, optimize_focal)
+    th0 = ba.encode()
+    rm0 = reproj_rmse_device(ba, th0)
+    th_ba, rep_ba = lm_solve(ba, th0, ba_config or LMConfig(max_iterations=10))
+    rm1 = reproj_rmse_device(ba, th_ba)
+    out = ba.decode(th_ba)
+    ba.release()
+    return (out if isinstance(scene, SceneArrays) else out), PipelineReport(rep_gp, rep_ba, rm0, rm1)

@@ -379,3 +379,27 @@ def test_jacobian_copies_bitwise_identical(gpu, name):
     _native.check(_native.load().ssfm_check_jacobian(ct.c_void_p(p._native_handle().ptr), ct.byref(m),
                                                      ct.c_void_p(gpu.cuda.current_stream().cuda_stream)))
     assert m.value == 0
+
+
+def test_reproj_rmse_device_matches_host(gpu):        # synth_metrics.py:312-325
+    _, obs = synth.generate_arrays(synth.SynthConfig(num_cameras=12, num_points=600, visibility_fraction=0.4,
+                                                     pixel_noise_sigma=1.0, seed=6))
+    st = synth.perturb_arrays(obs, rot_deg=1.0, center_frac=0.01, focal_frac=0.02, point_frac=0.005, seed=1)
+    p = b2.BAProblem(st, b2.RobustLoss("huber", 1.0))
+    assert b2.reproj_rmse_device(p, p.encode()) == pytest.approx(synth.reproj_rmse(st), rel=1e-12)
+
+
+def test_global_sfm_pipeline(gpu):                     # SURVEY.md 8(d) C4 recipe, small
+    _, obs = synth.generate_arrays(synth.SynthConfig(num_cameras=30, num_points=3000, visibility_fraction=8 / 30,
+                                                     pixel_noise_sigma=1.0, seed=0))
+    out, rep = b2.run_global_sfm(obs)
+    # the same two stages run by hand
+    mid, rg = b2.run_gp(obs, loss=b2.RobustLoss("huber", 0.1), config=b2.LMConfig(max_iterations=20))
+    ref, rb = b2.run_ba(mid, b2.RobustLoss("huber", 1.0), b2.LMConfig(max_iterations=10))
+    assert [i.cost_after for i in rep.gp.iterations] == [i.cost_after for i in rg.iterations]
+    assert [i.cost_after for i in rep.ba.iterations] == [i.cost_after for i in rb.iterations]
+    assert rep.rmse_after_gp == pytest.approx(synth.reproj_rmse(mid), rel=1e-12)
+    assert rep.rmse_after_ba == pytest.approx(synth.reproj_rmse(out), rel=1e-12)
+    # BA minimises the Huber cost, not the RMSE: the RMSE stays at the noise level
+    assert rep.ba.iterations[-1].cost_after < rep.ba.iterations[0].cost_before
+    assert rep.rmse_after_ba < 1.5
