@@ -276,6 +276,7 @@ def run_b200(args, ws, rank, local):
     # solve converges early, the next one restarts from theta0 (same workload)
     ms_total, steps, iters = 0.0, 0, []
     pms_sum, pl_sum, cg_sum, launch_sum = 0.0, 0, 0.0, 0
+    phase_sum = [0.0] * 5
     theta_cur, lam_cur = theta_w, lam
     barrier()
     while steps < args.steps:
@@ -292,6 +293,10 @@ def run_b200(args, ws, rank, local):
         ams, launches, _ = ct.c_double(0), ct.c_int64(0), ct.c_double(0)
         lib.ssfm_profile_get(ct.c_void_p(h.ptr), 2, ct.byref(ams), ct.byref(launches), ct.byref(_))
         pms_sum += pms.value; pl_sum += pl.value; cg_sum += cgit.value; launch_sum += launches.value
+        for kk in range(5):
+            phm = ct.c_double(0)
+            lib.ssfm_profile_get(ct.c_void_p(h.ptr), 3 + kk, ct.byref(phm), None, None)
+            phase_sum[kk] += phm.value
         iters += rep_t.iterations
         steps += len(rep_t.iterations)
         if rep_t.termination != "max_iter" or not rep_t.iterations:
@@ -330,6 +335,9 @@ def run_b200(args, ws, rank, local):
                 "kernel_ms": round(pms.value, 3),
                 "algorithmic_bytes_per_cg_iter": bytes_per_cg,
                 "kernel_share_of_step": round(pms.value / max(ms_total, 1e-9), 4)}
+        if not is_gp and sum(phase_sum) > 0:
+            names = ["point_or_fused_pass", "camera_pass", "q_and_pq", "x_r_z_update", "p_update"]
+            roof["phase_ms_per_cg_iter"] = {n: round(v / cgit.value, 4) for n, v in zip(names, phase_sum)}
     del theta_t
 
     # ---- end to end through the public API from host arrays

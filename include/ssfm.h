@@ -184,7 +184,9 @@ int ssfm_export_pattern(ssfm_handle* h, int32_t* obs_pt_order,
 
 /* Timing hooks for bench.py: per-kernel-class accumulated device time of the
  * last lm_solve (ms) and launch counts. kind: 0 = PCG operator (S*p), 1 =
- * linearize, 2 = all. */
+ * linearize, 2 = all, 3..7 = BA PCG phases measured inside the persistent
+ * kernel by block 0 (point or fused pass, camera pass, q = S p, x/r/z update,
+ * p update; each including its grid barrier). */
 int ssfm_profile_get(const ssfm_handle* h, int32_t kind, double* ms,
                      int64_t* launches, double* bytes);
 int ssfm_profile_enable(ssfm_handle* h, int32_t on);

@@ -27,7 +27,17 @@ struct CGCtl {
   int iters;
   int flag;     // 0 running/converged, ST_CG_* on failure
   int pad[2];
+  // per-phase time of block 0 (ns, %globaltimer), accumulated over CG
+  // iterations: [0] point / fused pass, [1] camera pass, [2] q = S p + p.q,
+  // [3] x, r, z + r.r, r.z, [4] p update; each includes its grid barrier
+  unsigned long long phase_ns[5];
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 #define PCG_THREADS 256
 
@@ -325,6 +335,10 @@ ba_k_pcg(BADev d, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg
     return a;
   };
   unsigned long long ep = cm.nranks > 1 ? *cm.epoch : 0ull;
+  // phase timers of block 0 live in shared memory (no registers held across
+  // the passes)
+  __shared__ unsigned long long ph[5], pt0;
+  if (threadIdx.x == 0) { for (int k = 0; k < 5; ++k) ph[k] = 0ull; }
   const bool shared = d.bp.focal_mode == 2;
   double qf = 0.0;
 
@@ -362,16 +376,20 @@ ba_k_pcg(BADev d, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg
   if (rn > tol) {
     while (true) {
       if (iters >= max_iters) { flag = ST_CG_MAXITER; break; }
+      const bool tim = blockIdx.x == 0 && threadIdx.x == 0;
+      if (tim) pt0 = gtimer();
       if constexpr (SL == 0) {
         // P1: point pass
         ba_point_pass(d, p, d.yv, smp);
         grid.sync();
+        if (tim) { const unsigned long long t1 = gtimer(); ph[0] += t1 - pt0; pt0 = t1; }
         // P2: camera tiles
         ba_camera_pass(d, d.yv, tile8, smred);
       } else {
         ba_fused_pass<SL>(d, fz, p, dyn_acc, smp, smy, smown);
       }
       grid.sync();
+      if (tim) { const unsigned long long t1 = gtimer(); ph[SL == 0 ? 1 : 0] += t1 - pt0; pt0 = t1; }
       // P2x (sharded): exchange the local camera half of S*p with the peer
       // ranks inside the kernel (comm.cuh); P3 then sums the ranks in order.
       if (cm.nranks > 1) {
@@ -425,6 +443,7 @@ ba_k_pcg(BADev d, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg
         if (threadIdx.x == 0) part[2ll * blockIdx.x] = v[0];
       }
       grid.sync();
+      if (tim) { const unsigned long long t1 = gtimer(); ph[2] += t1 - pt0; pt0 = t1; }
       double pq = cta_partials_sum(part, NP, 2, 0, &smb[0]);
       if (shared) {   // every CTA sums the cameras' shares in the same order
         qf = (d.pinned[0] >> 7 & 1) ? pf : cta_partials_sum(d.fterm, d.bp.C, 1, 0, &smb[2]);
@@ -460,6 +479,7 @@ ba_k_pcg(BADev d, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg
         if (threadIdx.x == 0) { part[2ll * blockIdx.x] = v[0]; part[2ll * blockIdx.x + 1] = v[1]; }
       }
       grid.sync();
+      if (tim) { const unsigned long long t1 = gtimer(); ph[3] += t1 - pt0; pt0 = t1; }
       rr = cta_partials_sum(part, NP, 2, 0, &smb[0]);
       const double rz = cta_partials_sum(part, NP, 2, 1, &smb[1]);
       ++iters;
@@ -470,11 +490,13 @@ ba_k_pcg(BADev d, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg
       // P5: p = z + beta p
       for (int s = gid; s < S; s += stride) p[s] = z[s] + beta * p[s];
       grid.sync();
+      if (tim) ph[4] += gtimer() - pt0;
       if (shared) pf = p[7];   // every thread tracks the shared focal of p
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (cm.nranks > 1) *cm.epoch = ep;
+    for (int k = 0; k < 5; ++k) ctl->phase_ns[k] = ph[k];
     ctl->tol = tol;
     ctl->rho = rho;
     ctl->rn = rn;

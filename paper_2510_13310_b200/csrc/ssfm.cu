@@ -43,6 +43,7 @@ struct Misc {
 
 struct Profile {
   bool on = false;
+  double phase_ms[5] = {0, 0, 0, 0, 0};
   double pcg_ms = 0, lin_ms = 0, all_ms = 0;
   long long pcg_launches = 0, lin_launches = 0, all_launches = 0;
   long long cg_iters = 0;
@@ -1001,6 +1002,7 @@ extern "C" int ssfm_lm_solve(ssfm_handle* h, double* theta_io, const ssfm_lm_con
   h->prof.pcg_launches = h->prof.lin_launches = h->prof.all_launches = 0;
   h->prof.cg_iters = 0;
   h->prof.kernel_launches = 0;
+  for (int k = 0; k < 5; ++k) h->prof.phase_ms[k] = 0;
   int result = SSFM_OK;
   for (int it = 1; it <= cfg->max_iterations; ++it) {
     auto t0 = clk::now();
@@ -1031,6 +1033,7 @@ extern "C" int ssfm_lm_solve(ssfm_handle* h, double* theta_io, const ssfm_lm_con
       h->prof.pcg_ms += pms;
       h->prof.pcg_launches += 1;
       h->prof.cg_iters += m.ctl.iters;
+      for (int k = 0; k < 5; ++k) h->prof.phase_ms[k] += m.ctl.phase_ns[k] * 1e-6;
     }
     const int code = status_to_code(m.status);
     const bool pcg_done = !(m.status & (ST_SINGULAR_POINT | ST_PIN_POINT | ST_SINGULAR_PRECOND |
@@ -1098,6 +1101,10 @@ extern "C" int ssfm_profile_get(const ssfm_handle* h, int32_t kind, double* ms, 
   } else if (kind == 1) {
     if (ms) *ms = p.lin_ms;
     if (launches) *launches = p.lin_launches;
+    if (bytes) *bytes = 0;
+  } else if (kind >= 3 && kind <= 7) {
+    if (ms) *ms = p.phase_ms[kind - 3];
+    if (launches) *launches = p.pcg_launches;
     if (bytes) *bytes = 0;
   } else {
     if (ms) *ms = p.all_ms;

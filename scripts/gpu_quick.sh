@@ -1,4 +1,6 @@
 #!/usr/bin/env bash
-timeout 600 python -m pytest tests/test_gpu_ba.py -x -q -k "reproj or pipeline or shared or c1" 2>&1 | tail -3
-timeout 900 python bench.py --config c4 --steps 10 --warmup 3 > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err
-cut -c1-900 gpurun_out/bench_c4.json; tail -2 gpurun_out/bench_c4.err
+timeout 600 python -m pytest tests/test_gpu_ba.py tests/test_gpu_fused.py -x -q 2>&1 | tail -2
+timeout 600 python bench.py --no-cpu-baseline --no-e2e --steps 4 > gpurun_out/q_c5.json 2>/dev/null
+python -c "
+import json; b=json.load(open('gpurun_out/q_c5.json'))
+print('c5 ms/step', round(b['ms_per_step'],3), 'pcg ms/iter', round(b['roofline']['kernel_ms']/b['roofline']['cg_iters'],4), b['roofline'].get('phase_ms_per_cg_iter'))"
