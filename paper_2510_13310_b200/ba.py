@@ -26,6 +26,16 @@ def _torch():
     return t()
 
 
+def _index_dev(torch, idx):
+    """int32 device copy of an index array: integer inputs are copied as they
+    are and narrowed on the device (a host-side astype of 20M indices costs
+    more than moving the wider type)."""
+    x = np.asarray(idx)
+    if x.dtype.kind in "iu" and x.flags.c_contiguous:
+        return torch.from_numpy(x).to("cuda").to(torch.int32)
+    return torch.as_tensor(np.ascontiguousarray(x, dtype=np.int32)).to("cuda")
+
+
 class _DeviceProblem:
     """Common plumbing of the native problems: lazy handle creation on the
     current CUDA device, theta transfer, cost / linearize / post_step."""
@@ -181,8 +191,8 @@ class BAProblem(_DeviceProblem):
         from .lm import _stream
         a = self.arr
         dev = lambda x, dt: torch.as_tensor(np.ascontiguousarray(x, dtype=dt)).to("cuda")  # noqa: E731
-        cam = dev(a.cam_idx, np.int32)
-        pt = dev(a.pt_idx, np.int32)
+        cam = _index_dev(torch, a.cam_idx)
+        pt = _index_dev(torch, a.pt_idx)
         pix = dev(a.pixels, np.float64)
         pps = dev(a.pps, np.float64)
         dists = dev(a.dists, np.float64)

@@ -159,18 +159,14 @@ static int build_topo(ssfm_handle* h, const int* cam, const int* pt, int C, int 
   tmp_bytes = std::max(tmp_bytes, scan_bytes);
   void* tmp;
   DALLOC(*(char**)&tmp, tmp_bytes);
+  // stable sorts; segment offsets from the sorted keys (no atomics)
   if (N > 0) {
     CU(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, pt, keys_out, iota, perm_pm, (int)N, 0, nbits(P), st));
+    k_seg_from_sorted<<<nblk(N, TB), TB, 0, st>>>(keys_out, N, P, T.pt_seg);
     CU(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, cam, keys_out, iota, perm_cm, (int)N, 0, nbits(C), st));
+    k_seg_from_sorted<<<nblk(N, TB), TB, 0, st>>>(keys_out, N, C, T.cam_seg);
   }
-  // segments
   DALLOC(cnt, maxPC);
-  CU(cudaMemsetAsync(cnt, 0, sizeof(int) * maxPC, st));
-  if (N > 0) k_count<<<nblk(N, TB), TB, 0, st>>>(pt, N, cnt);
-  CU(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, T.pt_seg, P + 1, st));
-  CU(cudaMemsetAsync(cnt, 0, sizeof(int) * maxPC, st));
-  if (N > 0) k_count<<<nblk(N, TB), TB, 0, st>>>(cam, N, cnt);
-  CU(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, T.cam_seg, C + 1, st));
   if (N > 0) {
     k_perm_views<<<nblk(N, TB), TB, 0, st>>>(perm_pm, perm_cm, cam, pt, N, T.pm_pt, T.pm_cam, T.cm_pt, inv_cm);
     k_pm_to_cm<<<nblk(N, TB), TB, 0, st>>>(perm_pm, inv_cm, N, T.pm_to_cm);

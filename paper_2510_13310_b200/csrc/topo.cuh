@@ -63,6 +63,17 @@ __global__ void k_count(const int* __restrict__ key, long long n, int* counts) {
   if (i < n) atomicAdd(&counts[key[i]], 1);
 }
 
+// Segment offsets from sorted keys (no atomics): observation i opens the
+// segments of every key in (key[i-1], key[i]]; the last one closes the rest.
+__global__ void k_seg_from_sorted(const int* __restrict__ key, long long n, int nkeys, int* seg) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int prev = i == 0 ? -1 : key[i - 1];
+  for (int k = prev + 1; k <= key[i]; ++k) seg[k] = (int)i;
+  if (i == n - 1)
+    for (int k = key[i] + 1; k <= nkeys; ++k) seg[k] = (int)n;
+}
+
 // gather helpers for the permuted views
 __global__ void k_perm_views(const int* __restrict__ perm_pm, const int* __restrict__ perm_cm,
                              const int* __restrict__ cam, const int* __restrict__ pt, long long n,

@@ -27,10 +27,14 @@ _VALID_HEIGHTS = (2, 3)
 
 
 class BlockLayout:
-    """Ordered parameter / residual block structure (sparse_block.py:32-69)."""
+    """Ordered parameter / residual block structure (sparse_block.py:32-69).
 
-    __slots__ = ("kind_codes", "widths", "param_offsets", "residual_heights",
-                 "residual_offsets", "total_params", "total_residuals")
+    Layouts built from runs (every BA / GP problem) keep the runs and build
+    the per-block arrays (kind codes, widths, offsets; 20M residual blocks at
+    C5) only when something asks for them: the device solver never does."""
+
+    __slots__ = ("_kind_codes", "_widths", "_param_offsets", "_residual_heights",
+                 "_residual_offsets", "_runs", "_height", "_nres", "total_params", "total_residuals")
 
     def __init__(self, kinds, residual_heights):
         if isinstance(kinds, np.ndarray) and kinds.dtype.kind in "iu":
@@ -41,28 +45,79 @@ class BlockLayout:
         heights = np.asarray(residual_heights, dtype=np.int32)
         if heights.size and not np.isin(heights, _VALID_HEIGHTS).all():
             raise LayoutMismatch(f"residual heights must be in {_VALID_HEIGHTS}")
-        self.kind_codes = codes
-        self.widths = WIDTH_BY_CODE[codes.astype(np.int32)]
-        self.param_offsets = np.concatenate([[0], np.cumsum(self.widths, dtype=np.int64)])
-        self.residual_heights = heights
-        self.residual_offsets = np.concatenate([[0], np.cumsum(heights, dtype=np.int64)])
-        self.total_params = int(self.param_offsets[-1])
-        self.total_residuals = int(self.residual_offsets[-1])
+        self._runs = None
+        self._height = None
+        self._nres = len(heights)
+        self._set_param_arrays(codes)
+        self._residual_heights = heights
+        self._residual_offsets = np.concatenate([[0], np.cumsum(heights, dtype=np.int64)])
+        self.total_residuals = int(self._residual_offsets[-1])
+
+    def _set_param_arrays(self, codes):
+        self._kind_codes = codes
+        self._widths = WIDTH_BY_CODE[codes.astype(np.int32)]
+        self._param_offsets = np.concatenate([[0], np.cumsum(self._widths, dtype=np.int64)])
+        self.total_params = int(self._param_offsets[-1])
 
     @classmethod
     def from_runs(cls, runs, height: int, num_residual_blocks: int) -> "BlockLayout":
-        """Build from [(kind, count), ...] without per-block Python objects."""
-        codes = np.concatenate([np.full(int(n), KIND_CODE[k], dtype=np.int8) for k, n in runs]) \
-            if runs else np.zeros(0, np.int8)
-        return cls(codes, np.full(int(num_residual_blocks), height, dtype=np.int32))
+        """Build from [(kind, count), ...] without per-block arrays."""
+        if int(height) not in _VALID_HEIGHTS:
+            raise LayoutMismatch(f"residual heights must be in {_VALID_HEIGHTS}")
+        self = cls.__new__(cls)
+        self._runs = [(k, int(n)) for k, n in runs]
+        self._height = int(height)
+        self._nres = int(num_residual_blocks)
+        self._kind_codes = self._widths = self._param_offsets = None
+        self._residual_heights = self._residual_offsets = None
+        self.total_params = int(sum(int(WIDTH_BY_CODE[KIND_CODE[k]]) * n for k, n in self._runs))
+        self.total_residuals = self._height * self._nres
+        return self
+
+    def _param_from_runs(self):
+        codes = np.concatenate([np.full(n, KIND_CODE[k], dtype=np.int8) for k, n in self._runs]) \
+            if self._runs else np.zeros(0, np.int8)
+        self._set_param_arrays(codes)
+
+    @property
+    def kind_codes(self):
+        if self._kind_codes is None:
+            self._param_from_runs()
+        return self._kind_codes
+
+    @property
+    def widths(self):
+        if self._widths is None:
+            self._param_from_runs()
+        return self._widths
+
+    @property
+    def param_offsets(self):
+        if self._param_offsets is None:
+            self._param_from_runs()
+        return self._param_offsets
+
+    @property
+    def residual_heights(self):
+        if self._residual_heights is None:
+            self._residual_heights = np.full(self._nres, self._height, dtype=np.int32)
+        return self._residual_heights
+
+    @property
+    def residual_offsets(self):
+        if self._residual_offsets is None:
+            self._residual_offsets = np.arange(self._nres + 1, dtype=np.int64) * self._height
+        return self._residual_offsets
 
     @property
     def num_param_blocks(self) -> int:
+        if self._runs is not None:
+            return int(sum(n for _, n in self._runs))
         return len(self.kind_codes)
 
     @property
     def num_residual_blocks(self) -> int:
-        return len(self.residual_heights)
+        return self._nres
 
     def kind_name(self, block_id: int) -> str:
         return KINDS[self.kind_codes[block_id]]

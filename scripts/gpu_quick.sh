@@ -1,6 +1,5 @@
 #!/usr/bin/env bash
-timeout 600 python -m pytest tests/test_gpu_ba.py tests/test_gpu_fused.py -x -q 2>&1 | tail -2
-timeout 600 python bench.py --no-cpu-baseline --no-e2e --steps 4 > gpurun_out/q_c5.json 2>/dev/null
+timeout 900 python bench.py --no-cpu-baseline > gpurun_out/q_c5.json 2> gpurun_out/q_c5.err
 python -c "
 import json; b=json.load(open('gpurun_out/q_c5.json'))
-print('c5 ms/step', round(b['ms_per_step'],3), 'pcg ms/iter', round(b['roofline']['kernel_ms']/b['roofline']['cg_iters'],4), b['roofline'].get('phase_ms_per_cg_iter'))"
+print('value', round(b['value']/1e6,1), 'M obs/s; ms/step', round(b['ms_per_step'],2), 'e2e', round(b['e2e']['value']/1e6,1), 'M obs/s', b['e2e'])"
