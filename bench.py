@@ -361,11 +361,15 @@ def run_b200(args, ws, rank, local):
         e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e_a.record(stream)
         p2 = make_problem(arr_host)
+        t_c = time.perf_counter()
         th_out, rep_e = b2.lm_solve(p2, theta_host, b2.LMConfig(max_iterations=args.warmup + args.steps))
+        t_s = time.perf_counter()
         e_b.record(stream)
         barrier()
         wall = time.perf_counter() - t_a
         e_ms = e_a.elapsed_time(e_b)
+        log(f"[rank {rank}] e2e: problem {1e3 * (t_c - t_a):.0f} ms, lm_solve {1e3 * (t_s - t_c):.0f} ms "
+            f"({len(rep_e.iterations)} its, device {sum(i.device_ms for i in rep_e.iterations):.0f} ms)")
         its = max(len(rep_e.iterations), 1)
         if dist is not None:
             t = torch.tensor([wall], device="cuda")

@@ -1,0 +1,246 @@
+// ba_pcg_graph.cuh -- the block-Jacobi PCG (lm.py:637-672) as a CUDA graph:
+// one conditional WHILE node whose body is one CG iteration split into
+// kernels, each with the occupancy that suits it (no grid-wide barriers; the
+// kernel boundaries order the phases):
+//
+//   point pass (or fused pass) -> camera pass -> q = S p, p.q partials ->
+//   alpha, x, r, z, r.r / r.z partials -> beta, p update -> scalars + loop
+//   condition (one block, cudaGraphSetConditional)
+//
+// The same arithmetic, partial layout and summation order as ba_k_pcg, so
+// results are identical to the persistent kernel's (tests compare them
+// bitwise). lambda, the tolerance and the iteration cap live in device memory:
+// the instantiated graph is reused for every damped solve of the handle.
+// Sharded handles keep the persistent kernel (in-kernel exchange, comm.cuh).
+#pragma once
+#include "ba_pcg.cuh"
+
+#define CGV_BLOCKS 148   // vector-phase grid (partials per reduction)
+
+// device scalar state of the graph PCG
+struct CGGraphDev {
+  double* x; double* r; double* z; double* p; double* q;
+  double* partA;   // [2 * CGV_BLOCKS] p.q (and init r.r / r.z)
+  double* partB;   // [2 * CGV_BLOCKS] r.r / r.z
+  double* sc;      // [8]: 0 lam, 1 cg_tol, 2 tol, 3 rho, 4 rn, 5 rz (pending), 6 qf
+  int* ic;         // [4]: 0 max_iters, 1 iters, 2 flag, 3 done
+  CGCtl* ctl;
+  int fused;       // 0 two-pass (tile8), 1 fused (gpart, ngrp groups)
+  int ngrp;
+};
+
+// sum of n per-block partials component k in fixed order (warp 0), broadcast
+__device__ __forceinline__ double g_partials_sum(const double* part, int n, int k, double* smslot) {
+  return cta_partials_sum(part, n, 2, k, smslot);
+}
+
+// ---- init: x = 0, r = b_red, z = M r, p = z; partials r.r, r.z -> partA
+__global__ void __launch_bounds__(256) k_g_init(BADev d, CGGraphDev g) {
+  __shared__ double smred[64];
+  const int S = 8 * d.bp.C;
+  const int stride = gridDim.x * blockDim.x;
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  double v[2] = {0.0, 0.0};
+  for (int base = 0; base < S; base += stride) {
+    const int s = base + gid;
+    const bool ok = s < S;
+    if (base + (gid & ~31) >= S) continue;
+    const int c = ok ? s >> 3 : 0, k = s & 7;
+    const double rk = ok ? d.bred[s] : 0.0;
+    double zk = 0.0;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const double rm = grp8_get(rk, m);
+      if (ok) zk += d.Minv[64ll * c + 8 * k + m] * rm;
+    }
+    if (ok) { g.x[s] = 0.0; g.r[s] = rk; g.z[s] = zk; g.p[s] = zk; }
+    v[0] += rk * rk;
+    v[1] += rk * zk;
+  }
+  block_reduce<2>(v, smred);
+  if (threadIdx.x == 0) { g.partA[2ll * blockIdx.x] = v[0]; g.partA[2ll * blockIdx.x + 1] = v[1]; }
+}
+
+// init scalars: rho, tol, done (rn <= tol), iteration cap
+__global__ void k_g_init2(BADev d, CGGraphDev g, int nblk) {
+  __shared__ double smb[4];
+  const double rr = g_partials_sum(g.partA, nblk, 0, &smb[0]);
+  const double rho = g_partials_sum(g.partA, nblk, 1, &smb[1]);
+  if (threadIdx.x == 0) {
+    const double gn = sqrt(d.scal[SC_GNORM2]);
+    const double tol = g.sc[1] * fmax(gn, 1e-300);
+    const double rn = sqrt(rr);
+    g.sc[2] = tol; g.sc[3] = rho; g.sc[4] = rn;
+    g.ic[1] = 0;
+    int flag = 0, done = !(rn > tol);
+    if (!done && g.ic[0] <= 0) { flag = ST_CG_MAXITER; done = 1; }
+    g.ic[2] = flag;
+    g.ic[3] = done;
+  }
+}
+
+// ---- body kernels (each returns at once when the solve is done)
+__global__ void __launch_bounds__(PCG_THREADS, 4) k_g_point(BADev d, CGGraphDev g) {
+  if (*(volatile int*)(g.ic + 3)) return;
+  __shared__ double smp[PCG_THREADS / 32][SSFM_BATCH][3];
+  ba_point_pass(d, g.p, d.yv, smp);
+}
+
+__global__ void __launch_bounds__(PCG_THREADS, 4) k_g_camera(BADev d, CGGraphDev g) {
+  if (*(volatile int*)(g.ic + 3)) return;
+  __shared__ double smred[(PCG_THREADS / 32) * 8];
+  ba_camera_pass(d, d.yv, d.tilebuf, smred);
+}
+
+template <int SL>
+__global__ void __launch_bounds__(FZ_THREADS, 1) k_g_fused(BADev d, FusedTopo fz, CGGraphDev g) {
+  if (*(volatile int*)(g.ic + 3)) return;
+  __shared__ double smp[FZ_WARPS][SSFM_BATCH][3];
+  __shared__ double smy[FZ_WARPS][SSFM_BATCH][3];
+  __shared__ int smown[FZ_WARPS][SSFM_BATCH];
+  extern __shared__ double dyn_acc[];
+  ba_fused_pass<SL>(d, fz, g.p, dyn_acc, smp, smy, smown);
+}
+
+// q = S p per slot (P3 of ba_k_pcg), p.q partials -> partA, shared-focal shares
+__global__ void __launch_bounds__(256) k_g_q(BADev d, FusedTopo fz, CGGraphDev g) {
+  if (*(volatile int*)(g.ic + 3)) return;
+  __shared__ double smred[64];
+  const int S = 8 * d.bp.C;
+  const int stride = gridDim.x * blockDim.x;
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  const double lam = g.sc[0];
+  const bool shared = d.bp.focal_mode == 2;
+  const double pf = shared ? g.p[7] : 0.0;
+  double v[1] = {0.0};
+  for (int base = 0; base < S; base += stride) {
+    const int s = base + gid;
+    if (base + (gid & ~31) >= S) continue;
+    const bool ok = s < S;
+    const int c = ok ? s >> 3 : 0, k = s & 7;
+    const double pk = ok ? g.p[s] : 0.0;
+    const double pkt = (shared && k == 7) ? pf : pk;
+    double bp = 0.0;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const double pm = grp8_get(pkt, m);
+      if (ok) bp += d.Bc[64ll * c + 8 * k + m] * pm;
+    }
+    if (ok) {
+      double acc = 0.0;
+      if (!g.fused) {
+        const int t0 = d.topo.cam_tile[c], t1 = d.topo.cam_tile[c + 1];
+        for (int t = t0; t < t1; ++t) acc += d.tilebuf[8ll * t + k];
+      } else {
+        for (int gq = 0; gq < g.ngrp; ++gq) acc += fz.gpart[(long long)gq * S + s];
+      }
+      if (shared && k == 7) {
+        d.fterm[c] = bp + lam * d.Bc[64ll * c + 63] * pf - acc;
+        if (c) g.q[s] = 0.0;
+      } else {
+        double qk = bp + lam * d.Bc[64ll * c + 9 * k] * pk - acc;
+        if ((d.pinned[c] >> k) & 1) qk = pk;
+        g.q[s] = qk;
+        v[0] += pk * qk;
+      }
+    }
+  }
+  block_reduce<1>(v, smred);
+  if (threadIdx.x == 0) g.partA[2ll * blockIdx.x] = v[0];
+}
+
+// alpha = rho / p.q (every block, same order); x += a p, r -= a q, z = M r;
+// partials r.r, r.z -> partB
+__global__ void __launch_bounds__(256) k_g_update(BADev d, CGGraphDev g, int nblk) {
+  if (*(volatile int*)(g.ic + 3)) return;
+  __shared__ double smred[64];
+  __shared__ double smb[4];
+  const int S = 8 * d.bp.C;
+  const int stride = gridDim.x * blockDim.x;
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool shared = d.bp.focal_mode == 2;
+  double pq = g_partials_sum(g.partA, nblk, 0, &smb[0]);
+  double qf = 0.0;
+  if (shared) {
+    const double pf = g.p[7];
+    qf = (d.pinned[0] >> 7 & 1) ? pf : cta_partials_sum(d.fterm, d.bp.C, 1, 0, &smb[2]);
+    pq += pf * qf;
+  }
+  if (!isfinite(pq) || pq <= 0.0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) g.ic[2] = ST_CG_BREAKDOWN;
+    return;
+  }
+  const double alpha = g.sc[3] / pq;
+  double v[2] = {0.0, 0.0};
+  for (int base = 0; base < S; base += stride) {
+    const int s = base + gid;
+    if (base + (gid & ~31) >= S) continue;
+    const bool ok = s < S;
+    const int c = ok ? s >> 3 : 0, k = s & 7;
+    double rk = 0.0;
+    if (ok) {
+      g.x[s] += alpha * g.p[s];
+      rk = g.r[s] - alpha * ((shared && s == 7) ? qf : g.q[s]);
+      g.r[s] = rk;
+    }
+    double zk = 0.0;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const double rm = grp8_get(rk, m);
+      if (ok) zk += d.Minv[64ll * c + 8 * k + m] * rm;
+    }
+    if (ok) g.z[s] = zk;
+    v[0] += rk * rk;
+    v[1] += rk * zk;
+  }
+  block_reduce<2>(v, smred);
+  if (threadIdx.x == 0) { g.partB[2ll * blockIdx.x] = v[0]; g.partB[2ll * blockIdx.x + 1] = v[1]; }
+}
+
+// beta = r.z / rho (every block, same order); p = z + beta p
+__global__ void __launch_bounds__(256) k_g_pupdate(BADev d, CGGraphDev g, int nblk) {
+  if (*(volatile int*)(g.ic + 3) || *(volatile int*)(g.ic + 2)) return;
+  __shared__ double smb[4];
+  const double rr = g_partials_sum(g.partB, nblk, 0, &smb[0]);
+  const double rz = g_partials_sum(g.partB, nblk, 1, &smb[1]);
+  if (sqrt(rr) <= g.sc[2]) return;   // converged: the loop ends, p is not used again
+  const double beta = rz / g.sc[3];
+  const int S = 8 * d.bp.C;
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x)
+    g.p[s] = g.z[s] + beta * g.p[s];
+}
+
+// scalars of the iteration and the loop condition (one block)
+__global__ void k_g_scalars(BADev d, CGGraphDev g, int nblk, cudaGraphConditionalHandle hc) {
+  __shared__ double smb[4];
+  int done = *(volatile int*)(g.ic + 3);
+  if (!done) {
+    int flag = g.ic[2];
+    if (!flag) {
+      const double rr = g_partials_sum(g.partB, nblk, 0, &smb[0]);
+      const double rz = g_partials_sum(g.partB, nblk, 1, &smb[1]);
+      if (threadIdx.x == 0) {
+        const int iters = g.ic[1] + 1;
+        const double rn = sqrt(rr);
+        g.ic[1] = iters;
+        g.sc[4] = rn;
+        if (rn <= g.sc[2]) done = 1;
+        else if (iters >= g.ic[0]) { flag = ST_CG_MAXITER; done = 1; }
+        else g.sc[3] = rz;   // rho of the next iteration
+        g.ic[2] = flag;
+        g.ic[3] = done;
+      }
+    } else if (threadIdx.x == 0) {
+      g.ic[3] = done = 1;
+    }
+  }
+  if (threadIdx.x == 0) {
+    if (g.ic[3]) {
+      CGCtl* ctl = g.ctl;
+      ctl->tol = g.sc[2]; ctl->rho = g.sc[3]; ctl->rn = g.sc[4];
+      ctl->iters = g.ic[1]; ctl->flag = g.ic[2];
+      if (g.ic[2]) atomicOr(d.status, g.ic[2]);
+    }
+    cudaGraphSetConditional(hc, g.ic[3] ? 0u : 1u);
+  }
+}

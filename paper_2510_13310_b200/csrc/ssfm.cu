@@ -17,6 +17,7 @@
 
 #include "../../include/ssfm.h"
 #include "ba_pcg.cuh"
+#include "ba_pcg_graph.cuh"
 #include "gp_kernels.cuh"
 #include "pattern.cuh"
 
@@ -81,6 +82,11 @@ struct ssfm_handle {
   double* camsum = nullptr;     // [CAM_V * C] per-camera sums exchanged between ranks
   double* ar_tmp = nullptr;     // [16] scalar scratch
   int comm_nranks = 1;
+  // graph PCG (ba_pcg_graph.cuh): built on first use, reused for every solve
+  int graph_state = 0;          // 0 not built, 1 ready, -1 unavailable (persistent kernel)
+  cudaGraph_t pcg_graph = nullptr;
+  cudaGraphExec_t pcg_exec = nullptr;
+  CGGraphDev gdev{};
   int lin_blocks = 0;
   int cost_blocks = 0;
   int cam_blocks = 0;
@@ -114,6 +120,8 @@ static inline int nblk(long long n, int t) { return (int)((n + t - 1) / t); }
 static void free_handle(ssfm_handle* h) {
   if (!h) return;
   for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
+  if (h->pcg_exec) cudaGraphExecDestroy(h->pcg_exec);
+  if (h->pcg_graph) cudaGraphDestroy(h->pcg_graph);
   for (void* p : h->allocs) cudaFree(p);
   if (h->region) cudaFree(h->region);
   if (h->hmisc) cudaFreeHost(h->hmisc);
@@ -266,7 +274,18 @@ static int try_fused_ba(ssfm_handle* h, int* ok) {
   return SSFM_OK;
 }
 
+static int setup_ba_pcg_op(ssfm_handle* h, cudaStream_t st);
+
 static int setup_ba_pcg(ssfm_handle* h, cudaStream_t st) {
+  int rc = setup_ba_pcg_op(h, st);
+  if (rc) return rc;
+  const char* ge = getenv("SSFM_PCG_GRAPH");
+  const bool want = ge ? ge[0] == '1' : (h->fz.G == 0 && h->topo.N >= 1000000);
+  h->graph_state = want ? 0 : -1;
+  return SSFM_OK;
+}
+
+static int setup_ba_pcg_op(ssfm_handle* h, cudaStream_t st) {
   const Topo& T = h->topo;
   // SSFM_PCG_SMS caps the SMs of the persistent PCG grid (several sharded
   // handles on one device must be co-resident: their kernels wait on each other)
@@ -748,10 +767,124 @@ static int launch_linearize(ssfm_handle* h, const double* theta, double* r_out, 
   return SSFM_OK;
 }
 
+
+__global__ void k_g_setparams(CGGraphDev g, double lam, double cg_tol, int max_iters) {
+  g.sc[0] = lam; g.sc[1] = cg_tol; g.ic[0] = max_iters;
+}
+
+template <int SL>
+static cudaError_t prepare_fused() {
+  int optin = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, k_g_fused<SL>);
+  if (e) return e;
+  return cudaFuncSetAttribute(k_g_fused<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              optin - (int)fa.sharedSizeBytes);
+}
+
+template <int SL>
+static void capture_fused(ssfm_handle* h, cudaStream_t cs) {
+  k_g_fused<SL><<<h->pcg_grid, FZ_THREADS, h->pcg_smem, cs>>>(h->ba, h->fz, h->gdev);
+}
+
+// Build the graph PCG of a BA handle: one conditional WHILE node, body = one
+// CG iteration as kernels. Falls back to the persistent kernel (state -1) if
+// the runtime refuses (e.g. no conditional nodes).
+static int build_pcg_graph(ssfm_handle* h) {
+  CGGraphDev& g = h->gdev;
+  g.x = h->x; g.r = h->r; g.z = h->z; g.p = h->p; g.q = h->q;
+  DALLOC(g.partA, 2 * CGV_BLOCKS + 2);
+  DALLOC(g.partB, 2 * CGV_BLOCKS + 2);
+  DALLOC(g.sc, 8);
+  DALLOC(g.ic, 4);
+  g.ctl = &h->misc->ctl;
+  g.fused = h->fz.G > 0 ? 1 : 0;
+  g.ngrp = h->fz.ngrp;
+  cudaGraphConditionalHandle hc;
+  cudaGraphNodeParams cp = {};
+  cudaGraphNode_t cn;
+  cudaStream_t cs = nullptr;
+  auto unavailable = [&](cudaError_t e) {
+    cudaGetLastError();
+    if (cs) cudaStreamDestroy(cs);
+    h->pcg_graph = nullptr;   // left to the driver: a half-captured body is not destroyed here
+    h->graph_state = -1;
+    (void)e;
+    return SSFM_OK;
+  };
+  cudaError_t e;
+  if (g.fused) {   // before any capture: kernel attributes cannot be set while capturing
+    switch (h->fz.SL) {
+      case 8: e = prepare_fused<8>(); break;
+      case 4: e = prepare_fused<4>(); break;
+      case 2: e = prepare_fused<2>(); break;
+      default: e = prepare_fused<1>(); break;
+    }
+    if (e) return unavailable(e);
+  }
+  if ((e = cudaGraphCreate(&h->pcg_graph, 0))) return unavailable(e);
+  if ((e = cudaGraphConditionalHandleCreate(&hc, h->pcg_graph, 1, cudaGraphCondAssignDefault))) return unavailable(e);
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = hc;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  if ((e = cudaGraphAddNode(&cn, h->pcg_graph, nullptr, 0, &cp))) return unavailable(e);
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  if ((e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking))) return unavailable(e);
+  if ((e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed)))
+    return unavailable(e);
+  BADev& d = h->ba;
+  int occ_p = 0, occ_c = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, k_g_point, PCG_THREADS, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, k_g_camera, PCG_THREADS, 0);
+  if (g.fused) {
+    switch (h->fz.SL) {
+      case 8: capture_fused<8>(h, cs); break;
+      case 4: capture_fused<4>(h, cs); break;
+      case 2: capture_fused<2>(h, cs); break;
+      default: capture_fused<1>(h, cs); break;
+    }
+  } else {
+    k_g_point<<<std::max(1, occ_p) * h->num_sms, PCG_THREADS, 0, cs>>>(d, g);
+    if (d.topo.nt) k_g_camera<<<std::max(1, occ_c) * h->num_sms, PCG_THREADS, 0, cs>>>(d, g);
+  }
+  k_g_q<<<CGV_BLOCKS, 256, 0, cs>>>(d, h->fz, g);
+  k_g_update<<<CGV_BLOCKS, 256, 0, cs>>>(d, g, CGV_BLOCKS);
+  k_g_pupdate<<<CGV_BLOCKS, 256, 0, cs>>>(d, g, CGV_BLOCKS);
+  k_g_scalars<<<1, 32, 0, cs>>>(d, g, CGV_BLOCKS, hc);
+  if ((e = cudaStreamEndCapture(cs, &body))) return unavailable(e);
+  if ((e = cudaGraphInstantiate(&h->pcg_exec, h->pcg_graph, 0))) return unavailable(e);
+  cudaStreamDestroy(cs);
+  h->graph_state = 1;
+  return SSFM_OK;
+}
+
 static int launch_pcg(ssfm_handle* h, double lam, const ssfm_lm_config* cfg, cudaStream_t st) {
   int max_it = cfg->cg_max_iters;
   double tol = cfg->cg_tol;
   void* args[11];
+  // BA, one rank: the graph PCG for the two-pass operator on large problems,
+  // where each pass as its own kernel (own occupancy, no grid barrier) beats
+  // the persistent kernel (C5: 1.17 vs 1.29 ms per CG iteration); the
+  // persistent kernel stays faster for the fused operator and small problems
+  // (C4-BA fused 0.204 vs 0.229 ms, C1 0.025 vs 0.035 ms). SSFM_PCG_GRAPH=1/0
+  // forces either.
+  // (decided at handle creation, setup_ba_pcg; built here on first use)
+  if (h->kind == 0 && !sharded(h) && h->graph_state == 0) {
+    int rc = build_pcg_graph(h);
+    if (rc) return rc;
+  }
+  if (h->kind == 0 && !sharded(h) && h->graph_state == 1) {
+    CGGraphDev& g = h->gdev;
+    k_g_setparams<<<1, 1, 0, st>>>(g, lam, tol, max_it);
+    k_g_init<<<CGV_BLOCKS, 256, 0, st>>>(h->ba, g);
+    k_g_init2<<<1, 32, 0, st>>>(h->ba, g, CGV_BLOCKS);
+    CU(cudaGraphLaunch(h->pcg_exec, st));
+    count_launch(h, 3);
+    return SSFM_OK;
+  }
   if (h->kind == 0) {
     BADev& d = h->ba;
     void* a[13];

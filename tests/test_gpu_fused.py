@@ -83,7 +83,7 @@ def test_fused_matches_two_pass_damped_solve(gpu, groups):
         d0, it0 = solve_normal_native(gpu, ref, lam, cfg)
         d1, it1 = solve_normal_native(gpu, fz, lam, cfg)
         assert rel(d1, d0) < 1e-9, (lam, rel(d1, d0))
-        assert abs(it1 - it0) <= 1
+        assert abs(it1 - it0) <= max(2, 0.03 * it0)   # stop at cg_tol 1e-12 is rounding-sensitive
         d2, it2 = solve_normal_native(gpu, fz, lam, cfg)
         assert np.array_equal(d1, d2) and it1 == it2       # bitwise deterministic
 
@@ -108,3 +108,42 @@ def test_fused_lm_trajectory_matches_two_pass(gpu):
     b, rb = b2.lm_solve(fz, th0, b2.LMConfig(max_iterations=12))
     assert [i.step_accepted for i in ra.iterations] == [i.step_accepted for i in rb.iterations]
     assert abs(ra.iterations[-1].cost_after - rb.iterations[-1].cost_after) <= 1e-10 * ra.iterations[-1].cost_after
+
+
+def with_env(env, make):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        p = make()
+        p._native_handle()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k)
+            else:
+                os.environ[k] = v
+    return p
+
+
+@pytest.mark.parametrize("fused", ["0", "1"])
+def test_graph_pcg_matches_persistent_kernel(gpu, fused):
+    """The CUDA-graph PCG (conditional WHILE node, one kernel per phase) and
+    the persistent cooperative kernel run the same recurrences; only the
+    vector-phase partial sums are grouped differently (148 vs grid blocks)."""
+    st = wide_scene()
+    loss = b2.RobustLoss("huber", 1.0)
+    cfg = b2.LMConfig(cg_tol=1e-12, cg_max_iters=5000)
+    per = with_env({"SSFM_FUSED": fused, "SSFM_PCG_GRAPH": "0"}, lambda: b2.BAProblem(st, loss))
+    gra = with_env({"SSFM_FUSED": fused, "SSFM_PCG_GRAPH": "1"}, lambda: b2.BAProblem(st, loss))
+    th = per.encode()
+    per.gradient(th)
+    gra.gradient(th)
+    for lam in (1e-4, 1e-1):
+        d0, it0 = solve_normal_native(gpu, per, lam, cfg)
+        d1, it1 = solve_normal_native(gpu, gra, lam, cfg)
+        assert rel(d1, d0) < 1e-9 and abs(it1 - it0) <= max(2, 0.03 * it0)
+        d2, it2 = solve_normal_native(gpu, gra, lam, cfg)
+        assert np.array_equal(d1, d2) and it1 == it2
+    # iteration cap and the CGStall path through the graph
+    with pytest.raises(b2.errors.CGStall):
+        solve_normal_native(gpu, gra, 1e-4, b2.LMConfig(cg_max_iters=3))
