@@ -31,7 +31,7 @@
 #include "common.cuh"
 
 #define SSFM_MAX_RANKS 16
-#define COMM_TIMEOUT_NS 60000000000ull   // 60 s: a lost peer becomes ST_COMM_TIMEOUT, not a hang
+#define COMM_TIMEOUT_NS 60000000000ull   // 60 s (SSFM_COMM_TIMEOUT_S): a lost peer is an error, not a hang
 
 enum { AR_SUM = 0, AR_MAX = 1, AR_OR = 2 };
 
@@ -43,6 +43,7 @@ struct CommDev {
   double* buf[SSFM_MAX_RANKS] = {};                   // every rank's 2 x cap buffers
   unsigned long long* epoch = nullptr;                // own epoch counter (local memory)
   int* status = nullptr;
+  unsigned long long timeout_ns = COMM_TIMEOUT_NS;
 };
 
 __device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
@@ -67,7 +68,7 @@ __device__ __forceinline__ void comm_signal_wait(const CommDev& cm, unsigned lon
   for (int r = 0; r < cm.nranks; ++r) {
     if (r == cm.rank) continue;
     while (ld_acquire_sys_u64(cm.flag[r]) < e) {
-      if (globaltimer_ns() - t0 > COMM_TIMEOUT_NS) { atomicOr(cm.status, ST_COMM_TIMEOUT); return; }
+      if (globaltimer_ns() - t0 > cm.timeout_ns) { atomicOr(cm.status, ST_COMM_TIMEOUT); return; }
     }
   }
 }

@@ -1165,6 +1165,12 @@ extern "C" int ssfm_lm_solve(ssfm_handle* h, double* theta_io, const ssfm_lm_con
       for (int k = 0; k < 5; ++k) h->prof.phase_ms[k] += m.ctl.phase_ns[k] * 1e-6;
     }
     const int code = status_to_code(m.status);
+    if (code == SSFM_COMM_ERROR) {   // a peer did not answer: the exchanged values are not valid
+      CU(cudaMemcpyAsync(theta_io, h->theta, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+      CU(cudaStreamSynchronize(st));
+      if (n_recs) *n_recs = std::min(nrec, (int)cap);
+      return set_err(SSFM_COMM_ERROR, status_msg(m.status, m));
+    }
     const bool pcg_done = !(m.status & (ST_SINGULAR_POINT | ST_PIN_POINT | ST_SINGULAR_PRECOND |
                                         ST_PIN_RETAINED | ST_PIN_SCALE | ST_CG_MAXITER | ST_CG_BREAKDOWN));
     double cost_new = NAN;
@@ -1268,6 +1274,10 @@ extern "C" int ssfm_comm_init(ssfm_handle* h, int32_t rank, int32_t nranks, void
   cm.flag[rank] = static_cast<unsigned long long*>(h->region);
   cm.buf[rank] = reinterpret_cast<double*>(static_cast<char*>(h->region) + 256);
   cm.status = &h->misc->status;
+  if (const char* e = getenv("SSFM_COMM_TIMEOUT_S")) {
+    const double sec = atof(e);
+    if (sec > 0) cm.timeout_ns = (unsigned long long)(sec * 1e9);
+  }
   cm.nranks = 1;   // becomes nranks on connect
   h->comm_nranks = nranks;
   if (ipc_handle_out) {

@@ -1,3 +1,4 @@
 #!/usr/bin/env bash
-timeout 600 python bench.py --no-cpu-baseline --steps 10 > gpurun_out/q.json 2> gpurun_out/q.err
-tail -2 gpurun_out/q.err
+for i in 1 2 3; do
+s=$(date +%s); timeout 300 python -m pytest tests/test_gpu_dist.py -q -x 2>&1 | grep -E "^E  |passed|failed" | head -4; echo "$(( $(date +%s) - s )) s"
+done

@@ -12,6 +12,11 @@ for p in (ROOT, os.path.join(ROOT, "oracle")):
         sys.path.insert(0, p)
 
 
+# several shards of one problem share the single test GPU: a lost exchange must
+# fail fast instead of waiting for the 60 s production timeout
+os.environ.setdefault("SSFM_COMM_TIMEOUT_S", "20")
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the built native library")
 
