@@ -109,32 +109,44 @@ __device__ __forceinline__ void ba_point_pass(const BADev& d, const double* v, d
   }
 }
 
-// P2: per camera tile, sum Jc^T (Jp y_j) -> tile8[t][8]
+// P2: per camera tile, sum Jc^T (Jp y_j) -> tile8[t][8]. One WARP per tile:
+// lanes accumulate the tile's observations round by round in registers, then
+// one butterfly reduction; no CTA barriers (a block reduction per 256-obs
+// tile left 30 % of the warps waiting at __syncthreads). Fixed order:
+// deterministic.
 __device__ __forceinline__ void ba_camera_pass(const BADev& d, const double* y, double* tile8,
                                                double* smred) {
+  (void)smred;
   const unsigned long long pstream = pol_evict_first(), pkeep = pol_evict_last();
   const long long Np = d.Npad;
-  for (int t = blockIdx.x; t < d.topo.nt; t += gridDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  for (int t = gw; t < d.topo.nt; t += warps) {
     const int o0 = __ldg(d.topo.tile_obs + t), o1 = __ldg(d.topo.tile_obs + t + 1);
-    const int i = o0 + threadIdx.x;
     double o[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) o[k] = 0.0;
-    if (i < o1) {
+#pragma unroll 2
+    for (int i = o0 + lane; i < o1; i += 32) {
       double J[BA_JREC];
 #pragma unroll
       for (int k = 0; k < BA_JREC; ++k) J[k] = ldg_stream(d.Jcm + k * Np + i, pstream);
       const int j = ldg_stream_i(d.topo.cm_pt + i, pstream);
       double yj[4];
       ld_v4_hint(y + 4ll * j, yj, pkeep);
-      double tt[2];
+      double tt[2], u[8];
       ba_jp_mul(J, yj, tt);
-      ba_jct_mul(J, tt, o);
-    }
-    block_reduce<8>(o, smred);
-    if (threadIdx.x == 0) {
+      ba_jct_mul(J, tt, u);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) tile8[8ll * t + k] = o[k];
+      for (int k = 0; k < 8; ++k) o[k] += u[k];
+    }
+    warp_allreduce<8>(o);
+    if (lane < 8) {
+      double v = o[0];
+#pragma unroll
+      for (int k = 1; k < 8; ++k) v = lane == k ? o[k] : v;
+      tile8[8ll * t + lane] = v;
     }
   }
 }
