@@ -217,6 +217,24 @@ int ssfm_comm_connect(ssfm_handle* h, const void* ipc_handles, void* const* regi
  * their camera, for theta (device). rmse = sqrt(*sum_sq / *count). BA only. */
 int ssfm_reproj_stats(ssfm_handle* h, const double* theta, double* sum_sq, int64_t* count, void* stream);
 
+/* ---- generic block algebra (the reference's public sparse_block API) -----
+ * Device pointers; the contribution schedules are the reference's JtJPattern
+ * (sparse_block.py:219-323) and JtrPattern (:326-363), built by the caller.
+ * Results are bit-identical to the reference's Cython fills.
+ * ssfm_block_jtj   replaces jtj_fill_cy (_core.pyx:18-58): out_data[key blocks]
+ * ssfm_block_jtr   replaces jtr_fill_cy (_core.pyx:61-97): out[param scalars]
+ * ssfm_block_scale_diag replaces scale_diag_inplace (sparse_block.py:429-439):
+ *                  data[diag_idx[k]] *= factor */
+int ssfm_block_jtj(const double* entry_data, const int64_t* entry_off, const int32_t* entry_h,
+                   const int32_t* entry_w, const int64_t* contrib_a, const int64_t* contrib_b,
+                   const int64_t* seg_start, const int64_t* key_out_off, int64_t nkeys,
+                   double* out_data, void* stream);
+int ssfm_block_jtr(const double* entry_data, const int64_t* entry_off, const int32_t* entry_h,
+                   const int32_t* entry_w, const int32_t* by_entry, const int64_t* seg_start,
+                   const int64_t* seg_out, const int64_t* res_row, int64_t nsegs,
+                   const double* residuals, double* out, void* stream);
+int ssfm_block_scale_diag(double* data, const int64_t* diag_idx, int64_t n, double factor, void* stream);
+
 /* Diagnostic (BA): number of Jacobian entries where the camera-major copy
  * (written by the camera-tile linearize pass) differs bitwise from the
  * point-major copy, after ssfm_linearize. Expected 0. */

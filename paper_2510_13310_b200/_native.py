@@ -22,7 +22,8 @@ EXPORTS = (
     "ssfm_cost", "ssfm_linearize", "ssfm_solve_normal", "ssfm_post_step",
     "ssfm_lm_solve", "ssfm_export_pattern", "ssfm_profile_get", "ssfm_profile_enable",
     "ssfm_operator_info", "ssfm_comm_init", "ssfm_comm_connect", "ssfm_check_jacobian",
-    "ssfm_bench_operator", "ssfm_reproj_stats",
+    "ssfm_bench_operator", "ssfm_reproj_stats", "ssfm_block_jtj", "ssfm_block_jtr",
+    "ssfm_block_scale_diag",
 )
 
 TERMINATIONS = {0: "max_iter", 1: "converged_cost", 2: "converged_grad", 3: "solver_failure"}

@@ -20,6 +20,7 @@
 #include "ba_pcg_graph.cuh"
 #include "gp_kernels.cuh"
 #include "pattern.cuh"
+#include "block_algebra.cuh"
 
 static thread_local std::string g_last_error;
 
@@ -1389,6 +1390,51 @@ extern "C" int ssfm_reproj_stats(ssfm_handle* h, const double* theta, double* su
   CU(cudaGetLastError());
   if (sum_sq) *sum_sq = hv[0];
   if (count) *count = (int64_t)hv[1];
+  return SSFM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// generic block algebra (sparse_block.jtj / jtr / apply_damping)
+// ---------------------------------------------------------------------------
+extern "C" int ssfm_block_jtj(const double* entry_data, const int64_t* entry_off, const int32_t* entry_h,
+                              const int32_t* entry_w, const int64_t* contrib_a, const int64_t* contrib_b,
+                              const int64_t* seg_start, const int64_t* key_out_off, int64_t nkeys,
+                              double* out_data, void* stream) {
+  if (nkeys < 0) return set_err(SSFM_INVALID_ARGUMENT, "negative key count");
+  if (nkeys == 0) return SSFM_OK;
+  if (!entry_data || !entry_off || !entry_h || !entry_w || !contrib_a || !contrib_b || !seg_start ||
+      !key_out_off || !out_data)
+    return set_err(SSFM_INVALID_ARGUMENT, "null argument");
+  k_block_jtj<<<nblk(nkeys, 128), 128, 0, (cudaStream_t)stream>>>(
+      entry_data, (const long long*)entry_off, entry_h, entry_w, (const long long*)contrib_a,
+      (const long long*)contrib_b, (const long long*)seg_start, (const long long*)key_out_off, nkeys, out_data);
+  CU(cudaGetLastError());
+  return SSFM_OK;
+}
+
+extern "C" int ssfm_block_jtr(const double* entry_data, const int64_t* entry_off, const int32_t* entry_h,
+                              const int32_t* entry_w, const int32_t* by_entry, const int64_t* seg_start,
+                              const int64_t* seg_out, const int64_t* res_row, int64_t nsegs,
+                              const double* residuals, double* out, void* stream) {
+  if (nsegs < 0) return set_err(SSFM_INVALID_ARGUMENT, "negative segment count");
+  if (nsegs == 0) return SSFM_OK;
+  if (!entry_data || !entry_off || !entry_h || !entry_w || !by_entry || !seg_start || !seg_out || !res_row ||
+      !residuals || !out)
+    return set_err(SSFM_INVALID_ARGUMENT, "null argument");
+  k_block_jtr<<<nblk(nsegs, 128), 128, 0, (cudaStream_t)stream>>>(
+      entry_data, (const long long*)entry_off, entry_h, entry_w, by_entry, (const long long*)seg_start,
+      (const long long*)seg_out, (const long long*)res_row, nsegs, residuals, out);
+  CU(cudaGetLastError());
+  return SSFM_OK;
+}
+
+extern "C" int ssfm_block_scale_diag(double* data, const int64_t* diag_idx, int64_t n, double factor,
+                                     void* stream) {
+  if (n < 0) return set_err(SSFM_INVALID_ARGUMENT, "negative count");
+  if (n == 0) return SSFM_OK;
+  if (!data || !diag_idx) return set_err(SSFM_INVALID_ARGUMENT, "null argument");
+  k_block_scale_diag<<<nblk(n, 256), 256, 0, (cudaStream_t)stream>>>(data, (const long long*)diag_idx, n, factor);
+  CU(cudaGetLastError());
   return SSFM_OK;
 }
 

@@ -138,9 +138,48 @@ def shared_focal_fixture():
     ba_fixture("ba_shared.npz", start, ref.RobustLoss("huber", 1.0), shared_focal=True)
 
 
+def block_algebra_fixture():
+    """Reference jtj / jtr / apply_damping outputs (Cython backend) on the
+    ba_small and gp_small linearizations: pins the generic block API."""
+    out = {}
+    for tag, z in (("ba", np.load(os.path.join(HERE, "ba_small.npz"))),
+                   ("gp", np.load(os.path.join(HERE, "gp_small.npz")))):
+        if tag == "ba":
+            sc = rsm.generate(rsm.SynthConfig(num_cameras=8, num_points=120, visibility_fraction=0.5,
+                                              pixel_noise_sigma=1.0, seed=3))[1]
+            sc = rsm.perturb(sc, rot_deg=1.0, center_frac=0.01, focal_frac=0.02, point_frac=0.005, seed=1)
+            prob = ref.BAProblem(sc, ref.RobustLoss("huber", 1.0))
+            th = prob.encode()
+        else:
+            sc = rsm.generate(rsm.SynthConfig(num_cameras=10, num_points=200, visibility_fraction=0.4,
+                                              pixel_noise_sigma=0.5, seed=2))[1]
+            prob = ref.fix_gauge(ref.make_rays(sc, False, ref.RobustLoss("huber", 0.1), seed=0))
+            th = prob.initial_theta()
+        r, J = prob.linearize(th)
+        sys_ = jtj(J)
+        g = jtr(J, r)
+        damped = apply_damping(sys_, 0.37)
+        out[f"{tag}_res_ids"] = J.res_ids
+        out[f"{tag}_param_ids"] = J.param_ids
+        out[f"{tag}_data"] = J.data.copy()
+        out[f"{tag}_data_off"] = J.data_off
+        out[f"{tag}_r"] = r.copy()
+        out[f"{tag}_kinds"] = prob.layout.kind_codes
+        out[f"{tag}_heights"] = prob.layout.residual_heights
+        out[f"{tag}_jtj"] = sys_.data.copy()
+        out[f"{tag}_off_keys"] = sys_.off_keys
+        out[f"{tag}_jtr"] = g.copy()
+        out[f"{tag}_damped"] = damped.data.copy()
+    np.savez_compressed(os.path.join(HERE, "block_algebra.npz"), **out)
+    print("block_algebra.npz", {k: v.shape for k, v in out.items() if k.endswith("jtj")})
+
+
 def main():
     if "shared" in sys.argv[1:]:
         shared_focal_fixture()
+        return
+    if "block" in sys.argv[1:]:
+        block_algebra_fixture()
         return
     shared_focal_fixture()
     # --- BA fixtures

@@ -104,3 +104,26 @@ def test_survey_goldens_recorded():
     assert s["c1"]["iterations"] == 22
     assert s["c1"]["final_cost"] == pytest.approx(20994.9852668881, rel=1e-12)
     assert s["c2"]["final_cost"] == pytest.approx(0.990124903324729, rel=1e-12)
+
+
+@pytest.mark.parametrize("tag", ["ba", "gp"])
+def test_block_algebra_golden_vs_dense(tag):
+    """The reference's jtj / jtr fixture (tests/golden/block_algebra.npz) agrees
+    with dense J^T J / J^T r built from the same blocks (CPU, no device)."""
+    from paper_2510_13310_b200.sparse_block import BlockLayout, BlockSparseJacobian, BlockNormalSystem
+    z = golden("block_algebra.npz")
+    lay = BlockLayout(z[f"{tag}_kinds"], z[f"{tag}_heights"])
+    j = BlockSparseJacobian(lay, z[f"{tag}_res_ids"], z[f"{tag}_param_ids"], z[f"{tag}_data"],
+                            z[f"{tag}_data_off"])
+    A = np.zeros((lay.total_residuals, lay.total_params))
+    for e in range(j.num_entries):
+        r0, p0 = lay.residual_offsets[j.res_ids[e]], lay.param_offsets[j.param_ids[e]]
+        blk = j.entry_block(e)
+        A[r0:r0 + blk.shape[0], p0:p0 + blk.shape[1]] = blk
+    full = A.T @ A
+    sys_ = BlockNormalSystem.empty(lay, z[f"{tag}_off_keys"])
+    sys_.data[:] = z[f"{tag}_jtj"]
+    for k in range(lay.num_param_blocks):
+        o, w = lay.param_offsets[k], lay.widths[k]
+        assert np.allclose(sys_.diag_block(k), full[o:o + w, o:o + w], rtol=1e-12, atol=1e-10)
+    assert rel(z[f"{tag}_jtr"], A.T @ z[f"{tag}_r"]) < 1e-12
