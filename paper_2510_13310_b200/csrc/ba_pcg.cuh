@@ -270,13 +270,6 @@ __device__ __forceinline__ void ba_fused_pass(const BADev& d, const FusedTopo& f
         for (int m = 0; m < 8; ++m)
           if (m / SL == g) u[m % SL] = o[m];
       }
-      if (fz.atomic) {   // experiment: unordered shared-memory fp64 atomics (not bit-stable)
-        if (have) {
-#pragma unroll
-          for (int j = 0; j < SL; ++j) atomicAdd(acc + fz_slot<SL>(c, j), u[j]);
-        }
-        continue;
-      }
       const unsigned same = __match_any_sync(SSFM_FULL, have ? c : -1);
       const bool dup = __popc(same) > 1;
       if (__any_sync(SSFM_FULL, dup && have)) {

@@ -30,7 +30,6 @@
 // same steps (their J reads hit L2 for all but the first) and each owns 8/G
 // slots of every camera.
 #pragma once
-#include <cuda/atomic>
 #include "topo.cuh"
 
 #define FZ_WARPS 16
@@ -43,7 +42,6 @@ struct FusedTopo {
   int G = 0;                      // slot groups (0 = fused operator disabled)
   int SL = 0;                     // slots per group = 8 / G (BA) or 4 / G (GP)
   int ngrp = 0;                   // number of CTA groups in the PCG grid (gridDim / G)
-  int atomic = 0;                 // experiment: unordered smem atomics instead of tickets
   unsigned short* tick = nullptr; // [N] point-major: ticket of the observation's unit
   double* gpart = nullptr;        // [ngrp * slots_per_cam * C] per-group camera partials
 };

@@ -309,8 +309,6 @@ static int setup_ba_pcg_op(ssfm_handle* h, cudaStream_t st) {
   if (ok) {
     FusedTopo& fz = h->fz;
     CU(cudaMemsetAsync(h->ba.status, 0, sizeof(int), st));
-    const char* ea = getenv("SSFM_FUSED_ATOMIC");
-    fz.atomic = (ea && ea[0] == '1') ? 1 : 0;
     fz.nsteps = nblk(T.nb, FZ_WARPS);
     DALLOC(fz.tick, T.N);
     DALLOC(fz.gpart, (long long)fz.ngrp * 8 * C);
