@@ -69,12 +69,30 @@ __device__ __forceinline__ void block_reduce(double (&v)[V], double* sm) {
     for (int k = 0; k < V; ++k) sm[warp * V + k] = v[k];
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (V <= 4) {
+    if (threadIdx.x == 0) {
 #pragma unroll
-    for (int k = 0; k < V; ++k) {
-      double s = sm[k];
-      for (int w = 1; w < nw; ++w) s += sm[w * V + k];
-      v[k] = s;
+      for (int k = 0; k < V; ++k) {
+        double s = sm[k];
+        for (int w = 1; w < nw; ++w) s += sm[w * V + k];
+        v[k] = s;
+      }
+    }
+  } else {
+    // wide reductions: lane k of warp 0 sums component k over the warps (same
+    // warp order as the sequential loop, so the same bits), results back
+    // through shared memory for thread 0
+    if (warp == 0) {
+      for (int k = lane; k < V; k += 32) {
+        double s = sm[k];
+        for (int w = 1; w < nw; ++w) s += sm[w * V + k];
+        sm[k] = s;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int k = 0; k < V; ++k) v[k] = sm[k];
     }
   }
   __syncthreads();
