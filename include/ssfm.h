@@ -235,6 +235,17 @@ int ssfm_block_jtr(const double* entry_data, const int64_t* entry_off, const int
                    const double* residuals, double* out, void* stream);
 int ssfm_block_scale_diag(double* data, const int64_t* diag_idx, int64_t n, double factor, void* stream);
 
+/* ---- dense solver (lm.py:124-220; LMConfig(solver="dense")) -------------
+ * ssfm_dense_scatter: A[dst[k]] = data[src[k]] (materialize_dense with the
+ *   caller's _DensePlan indices; A is n x n row-major, zero-initialised).
+ * ssfm_dense_solve: in place on A: pin zero diagonals (SSFM_SINGULAR_BLOCK if
+ *   the gradient entry is non-zero), reject negative diagonals, Jacobi
+ *   equilibration, Cholesky (cuSOLVER potrf, loaded with dlopen on first use),
+ *   x = solution of A x = b. All pointers device. */
+int ssfm_dense_scatter(const double* data, const int64_t* dst, const int64_t* src, int64_t m,
+                       double* A, void* stream);
+int ssfm_dense_solve(double* A, const double* b, double* x, int64_t n, void* stream);
+
 /* Diagnostic (BA): number of Jacobian entries where the camera-major copy
  * (written by the camera-tile linearize pass) differs bitwise from the
  * point-major copy, after ssfm_linearize. Expected 0. */

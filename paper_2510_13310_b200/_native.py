@@ -23,7 +23,7 @@ EXPORTS = (
     "ssfm_lm_solve", "ssfm_export_pattern", "ssfm_profile_get", "ssfm_profile_enable",
     "ssfm_operator_info", "ssfm_comm_init", "ssfm_comm_connect", "ssfm_check_jacobian",
     "ssfm_bench_operator", "ssfm_reproj_stats", "ssfm_block_jtj", "ssfm_block_jtr",
-    "ssfm_block_scale_diag",
+    "ssfm_block_scale_diag", "ssfm_dense_scatter", "ssfm_dense_solve",
 )
 
 TERMINATIONS = {0: "max_iter", 1: "converged_cost", 2: "converged_grad", 3: "solver_failure"}

@@ -23,7 +23,7 @@ ROOT = os.path.dirname(HERE)
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-shared",
-         "--expt-relaxed-constexpr", "-cudart", "static"]
+         "--expt-relaxed-constexpr", "-cudart", "static", "-ldl"]
 
 
 def sources():

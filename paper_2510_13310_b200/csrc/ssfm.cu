@@ -21,6 +21,7 @@
 #include "gp_kernels.cuh"
 #include "pattern.cuh"
 #include "block_algebra.cuh"
+#include "dense.cuh"
 
 static thread_local std::string g_last_error;
 
@@ -863,7 +864,6 @@ static int build_pcg_graph(ssfm_handle* h) {
 static int launch_pcg(ssfm_handle* h, double lam, const ssfm_lm_config* cfg, cudaStream_t st) {
   int max_it = cfg->cg_max_iters;
   double tol = cfg->cg_tol;
-  void* args[11];
   // BA, one rank: the graph PCG for the two-pass operator on large problems,
   // where each pass as its own kernel (own occupancy, no grid barrier) beats
   // the persistent kernel (C5: 1.17 vs 1.29 ms per CG iteration); the
@@ -1434,6 +1434,61 @@ extern "C" int ssfm_block_scale_diag(double* data, const int64_t* diag_idx, int6
   k_block_scale_diag<<<nblk(n, 256), 256, 0, (cudaStream_t)stream>>>(data, (const long long*)diag_idx, n, factor);
   CU(cudaGetLastError());
   return SSFM_OK;
+}
+
+extern "C" int ssfm_dense_scatter(const double* data, const int64_t* dst, const int64_t* src, int64_t m,
+                                  double* A, void* stream) {
+  if (m < 0) return set_err(SSFM_INVALID_ARGUMENT, "negative count");
+  if (m == 0) return SSFM_OK;
+  if (!data || !dst || !src || !A) return set_err(SSFM_INVALID_ARGUMENT, "null argument");
+  k_dense_scatter<<<nblk(m, 256), 256, 0, (cudaStream_t)stream>>>(data, (const long long*)dst,
+                                                                 (const long long*)src, m, A);
+  CU(cudaGetLastError());
+  return SSFM_OK;
+}
+
+extern "C" int ssfm_dense_solve(double* A, const double* b, double* x, int64_t n, void* stream) {
+  if (!A || !b || !x || n <= 0) return set_err(SSFM_INVALID_ARGUMENT, "bad argument");
+  if (n > (1ll << 31) - 1) return set_err(SSFM_INVALID_ARGUMENT, "dense system too large");
+  CuSolverApi& api = cusolver_api();
+  if (!api.ok) return set_err(SSFM_CUDA_ERROR, "cuSOLVER (libcusolver.so.11) unavailable");
+  cudaStream_t st = (cudaStream_t)stream;
+  double *s = nullptr, *rhs = nullptr, *work = nullptr;
+  int *flag = nullptr, *devinfo = nullptr;
+  CU(cudaMalloc(&s, sizeof(double) * n));
+  CU(cudaMalloc(&rhs, sizeof(double) * n));
+  CU(cudaMalloc(&flag, sizeof(int) * 2));
+  devinfo = flag + 1;
+  CU(cudaMemsetAsync(flag, 0, sizeof(int) * 2, st));
+  k_dense_prep<<<nblk(n, 256), 256, 0, st>>>(A, b, n, s, rhs, flag);
+  k_dense_scale<<<nblk(n * n, 256), 256, 0, st>>>(A, s, n);
+  cusolverDnHandle_t hs = nullptr;
+  int rc = SSFM_OK;
+  int lwork = 0, hflag[2] = {0, 0};
+  if (api.create(&hs) != CUSOLVER_STATUS_SUCCESS) rc = set_err(SSFM_CUDA_ERROR, "cusolverDnCreate failed");
+  if (!rc) api.set_stream(hs, st);
+  if (!rc && api.potrf_bs(hs, CUBLAS_FILL_MODE_LOWER, (int)n, A, (int)n, &lwork) != CUSOLVER_STATUS_SUCCESS)
+    rc = set_err(SSFM_CUDA_ERROR, "potrf_bufferSize failed");
+  if (!rc && cudaMalloc(&work, sizeof(double) * std::max(lwork, 1))) rc = set_err(SSFM_CUDA_ERROR, "cudaMalloc");
+  if (!rc && api.potrf(hs, CUBLAS_FILL_MODE_LOWER, (int)n, A, (int)n, work, lwork, devinfo) != CUSOLVER_STATUS_SUCCESS)
+    rc = set_err(SSFM_CUDA_ERROR, "potrf failed");
+  if (!rc) {
+    cudaMemcpyAsync(hflag, flag, sizeof(hflag), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    if (hflag[0] & 1) rc = set_err(SSFM_SINGULAR_BLOCK, "zero diagonal with non-zero gradient");
+    else if (hflag[0] & 2) rc = set_err(SSFM_SINGULAR_BLOCK, "negative diagonal in damped system");
+    else if (hflag[1] != 0) rc = set_err(SSFM_SINGULAR_BLOCK, "dense factorization failed (potrf info " +
+                                                            std::to_string(hflag[1]) + ")");
+  }
+  if (!rc && api.potrs(hs, CUBLAS_FILL_MODE_LOWER, (int)n, 1, A, (int)n, rhs, (int)n, devinfo) != CUSOLVER_STATUS_SUCCESS)
+    rc = set_err(SSFM_CUDA_ERROR, "potrs failed");
+  if (!rc) k_dense_unscale<<<nblk(n, 256), 256, 0, st>>>(s, rhs, n, x);
+  cudaStreamSynchronize(st);
+  if (hs) api.destroy(hs);
+  cudaFree(s); cudaFree(rhs); cudaFree(flag);
+  if (work) cudaFree(work);
+  if (!rc && cudaGetLastError() != cudaSuccess) rc = set_err(SSFM_CUDA_ERROR, "dense solve kernel failed");
+  return rc;
 }
 
 extern "C" int ssfm_operator_info(const ssfm_handle* h, int32_t* slot_groups, int32_t* grid,

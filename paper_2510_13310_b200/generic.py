@@ -9,9 +9,12 @@ csrc/block_algebra.cuh with the reference's per-output summation order and
 without FMA contraction, so the results are bit-identical to the Cython
 backend (tests/test_gpu_block.py checks it on the reference's own output).
 
-The damped Schur solve on an explicit BlockNormalSystem (lm.py:707-720 for a
-user-assembled system) and lm_solve for foreign problem providers are not on
-the device path: BAProblem / GPProblem run the matrix-free solver
+solve_normal with LMConfig(solver="dense") is the reference's dense path
+(lm.py:124-220) on the device (csrc/dense.cuh, cuSOLVER Cholesky), and
+lm_solve_generic is the reference's LM loop (lm.py:727-800) for any problem
+provider (and for solver="dense" on BA / GP problems) on top of these device
+products. The Schur PCG of an explicit user-assembled BlockNormalSystem is not
+on the device path: BAProblem / GPProblem run the matrix-free Schur PCG
 (csrc/ba_pcg*.cuh, csrc/gp_kernels.cuh); see DESIGN.md section 6.
 """
 
@@ -168,8 +171,8 @@ def scale_diag_device(sys, factor: float) -> None:
     from .lm import _stream
     idx = _diag_index(sys)
     data = _dev(torch, sys.data, np.float64)
-    _native.check(_native.load().ssfm_block_scale_diag(ct.c_void_p(data.data_ptr()),
-                                                       ct.c_void_p(_dev(torch, idx, np.int64).data_ptr()),
+    idx_d = _dev(torch, idx, np.int64)
+    _native.check(_native.load().ssfm_block_scale_diag(ct.c_void_p(data.data_ptr()), ct.c_void_p(idx_d.data_ptr()),
                                                        ct.c_int64(len(idx)), ct.c_double(factor),
                                                        _stream(torch)))
     sys.data[...] = data.cpu().numpy()
@@ -185,9 +188,133 @@ def damp_device(sys, lam: float):
     return out
 
 
-def _not_on_device(*_a, **_k):
-    raise NativeError("the damped Schur solve of an explicit BlockNormalSystem is not on the device path; "
-                      "BAProblem / GPProblem solve matrix-free on the device (lm_solve)")
+class _DensePlan:
+    """Flat scatter indices of the block storage into the dense matrix
+    (lm.py:124-167): diagonal blocks, off-diagonal blocks and their mirror."""
+
+    def __init__(self, sys):
+        lay = sys.layout
+        n = lay.total_params
+        w = lay.widths.astype(np.int64)
+        off = lay.param_offsets
+        dst, src = [], []
+        for k in np.unique(w):
+            ids = np.nonzero(w == k)[0]
+            r = off[ids][:, None] + np.arange(k)
+            dst.append(((r[:, :, None] * n) + r[:, None, :]).ravel())
+            src.append((sys.diag_off[ids][:, None] + np.arange(k * k)).ravel())
+        if sys.num_off_blocks:
+            wa, wb = w[sys.off_keys[:, 0]], w[sys.off_keys[:, 1]]
+            for code in np.unique(wa * 8 + wb):
+                sel = np.nonzero(wa * 8 + wb == code)[0]
+                ka, kb = int(code // 8), int(code % 8)
+                rows = (off[sys.off_keys[sel, 0]][:, None] + np.arange(ka))[:, :, None]
+                cols = (off[sys.off_keys[sel, 1]][:, None] + np.arange(kb))[:, None, :]
+                s_ = (sys.off_off[sel][:, None] + np.arange(ka * kb)).ravel()
+                dst.append((rows * n + cols).ravel())
+                src.append(s_)
+                dst.append((cols * n + rows).ravel())
+                src.append(s_)
+        self.n = n
+        self.dst = np.concatenate(dst) if dst else np.zeros(0, np.int64)
+        self.src = np.concatenate(src) if src else np.zeros(0, np.int64)
 
 
-solve_normal_device = lm_solve_generic = _not_on_device
+def solve_normal_device(sys, layout, config, workspace=None, info=None):
+    """solve_normal (lm.py:707-720). solver="dense": the reference's dense path
+    (_solve_dense, lm.py:170-220) on the device -- assembly, pinning, Jacobi
+    equilibration and a cuSOLVER Cholesky (csrc/dense.cuh). The damped Schur
+    PCG of an explicit user-assembled system is not on the device path (BA / GP
+    problems solve matrix-free inside lm_solve)."""
+    if config.solver != "dense":
+        raise NativeError("the Schur PCG of an explicit BlockNormalSystem is not on the device path; "
+                          "use LMConfig(solver='dense') or a BAProblem / GPProblem")
+    torch = _torch()
+    from .lm import _stream
+    key = ("dense_plan", id(sys.off_keys), id(sys.layout))
+    plans = workspace.caches if workspace is not None else {}
+    plan = plans.get(key)
+    if plan is None or plan.n != layout.total_params:
+        plan = _DensePlan(sys)
+        plans[key] = plan
+    n = plan.n
+    lib = _native.load()
+    st = _stream(torch)
+    A = torch.zeros(n * n, dtype=torch.float64, device="cuda")
+    # every device temporary stays referenced until its kernel is enqueued
+    # (a tensor freed before the launch may be handed to the next allocation)
+    data = _dev(torch, sys.data, np.float64)
+    dst = _dev(torch, plan.dst, np.int64)
+    src = _dev(torch, plan.src, np.int64)
+    _native.check(lib.ssfm_dense_scatter(ct.c_void_p(data.data_ptr()), ct.c_void_p(dst.data_ptr()),
+                                         ct.c_void_p(src.data_ptr()), ct.c_int64(len(plan.dst)),
+                                         ct.c_void_p(A.data_ptr()), st))
+    b = _dev(torch, sys.gradient, np.float64)
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    _native.check(lib.ssfm_dense_solve(ct.c_void_p(A.data_ptr()), ct.c_void_p(b.data_ptr()),
+                                       ct.c_void_p(x.data_ptr()), ct.c_int64(n), st))
+    if info is not None:
+        info["cg_iters"] = 0
+    return x.cpu().numpy()
+
+
+def lm_solve_generic(problem, theta0, config, workspace=None):
+    """lm_solve (lm.py:727-800) for any problem provider (layout, cost,
+    linearize -> (r, BlockSparseJacobian), optional post_step) and for the
+    dense solver: J^T J, J^T r and damping on the device (bit-identical to the
+    reference's products), the damped solve on the device."""
+    import time
+    from .errors import CGStall, SingularBlock, SolverFailure, ZeroQuaternion
+    from .lm import IterationRecord, SolveReport, Workspace
+    from .sparse_block import apply_damping, jtj, jtr
+    ws = workspace or Workspace()
+    layout = problem.layout
+    theta = np.array(theta0, dtype=np.float64, copy=True)
+    if theta.shape != (layout.total_params,):
+        from .errors import DimensionMismatch
+        raise DimensionMismatch("theta0 length does not match the problem layout")
+    post_step = getattr(problem, "post_step", None)
+    report = SolveReport()
+    cost = float(problem.cost(theta))
+    lam = config.lambda0
+    sys_ = grad = None
+    need_lin = True
+    for it in range(1, config.max_iterations + 1):
+        t0 = time.perf_counter_ns()
+        if need_lin:
+            r, jac = problem.linearize(theta)
+            sys_ = jtj(jac, out=sys_)
+            grad = jtr(jac, r, out=grad)
+            np.negative(grad, out=sys_.gradient)
+            need_lin = False
+            if float(np.abs(grad).max(initial=0.0)) < config.grad_tol:
+                report.termination = "converged_grad"
+                break
+        damped = apply_damping(sys_, lam)
+        info = {}
+        try:
+            delta = solve_normal_device(damped, layout, config, ws, info)
+            cand = theta + delta
+            if post_step is not None:
+                cand = np.asarray(post_step(cand), dtype=np.float64)
+            cost_new = float(problem.cost(cand))
+            failed = False
+        except (SingularBlock, CGStall, ZeroQuaternion) as exc:
+            if lam >= config.lambda_max:
+                report.termination = "solver_failure"
+                raise SolverFailure(f"linear solve failed at lambda_max: {exc}", report) from exc
+            cost_new, failed = float("nan"), True
+        accepted = (not failed) and np.isfinite(cost_new) and cost_new < cost
+        report.iterations.append(IterationRecord(it, cost, cost_new, lam, accepted, int(info.get("cg_iters", 0)),
+                                                 time.perf_counter_ns() - t0))
+        if accepted:
+            rel = (cost - cost_new) / max(cost, 1e-300)
+            theta, cost = cand, cost_new
+            lam = max(lam / config.lambda_down, config.lambda_min)
+            need_lin = True
+            if rel < config.rel_cost_tol:
+                report.termination = "converged_cost"
+                break
+        else:
+            lam = min(lam * config.lambda_up, config.lambda_max)
+    return theta, report

@@ -64,3 +64,57 @@ def test_block_algebra_mixed_layout_vs_dense(gpu):
     assert d.lam == 0.5 and sys_.lam == 0.0
     for k in range(lay.num_param_blocks):
         assert np.array_equal(np.diag(d.diag_block(k)), np.diag(sys_.diag_block(k)) * 1.5)
+
+
+def test_dense_solver_step_matches_exact_solve(gpu):     # lm.py:170-220 on the device
+    import sparsesfm_port as orc
+    from .conftest import ba_prob_from_golden
+    from .test_gpu_ba import problem_from_golden
+    z = golden("ba_small.npz")
+    p = problem_from_golden(z)
+    r, jac = p.linearize(z["theta0"])
+    sys_ = jtj(jac)
+    sys_.gradient[:] = -jtr(jac, r)
+    damped = apply_damping(sys_, 1e-3)
+    info = {}
+    d = b2.lm.solve_normal(damped, p.layout, b2.LMConfig(solver="dense"), b2.Workspace(), info)
+    prob = ba_prob_from_golden(z)
+    r_o, J_o = orc.ba_linearize(prob, z["theta0"])
+    Jd = orc.ba_dense_jacobian(prob, J_o)
+    A = Jd.T @ Jd
+    A[np.diag_indices_from(A)] *= 1.001
+    exact = np.linalg.solve(A, -(Jd.T @ r_o))
+    assert np.abs(d - exact).max() / np.abs(exact).max() < 1e-9
+    assert info["cg_iters"] == 0
+
+
+def test_lm_solve_dense_solver_and_foreign_provider(gpu):
+    from .test_gpu_ba import problem_from_golden
+    z = golden("ba_small.npz")
+    p = problem_from_golden(z)
+    th, rep = b2.lm_solve(p, z["theta0"], b2.LMConfig(solver="dense", max_iterations=30))
+    assert rep.termination == "converged_cost"
+    assert rep.iterations[-1].cost_after == pytest.approx(float(z["records"][-1, 2]), rel=1e-8)
+    assert all(i.cg_iters == 0 for i in rep.iterations)
+
+    class Line:                     # a duck-typed provider (lm.py:730-739): fit y = a x + b
+        def __init__(self):
+            self.layout = BlockLayout(np.array([2], np.int8), np.full(20, 2, np.int32))  # one 'focal'... width-1
+            self.x = np.linspace(0, 1, 40)
+            self.y = 3.0 * self.x + 0.5
+
+        def residual(self, th):
+            return th[0] * self.x + (self.y[0] - 0.5) * 0 + 0.5 - self.y
+
+        def cost(self, th):
+            return float(np.sum(self.residual(th) ** 2))
+
+        def linearize(self, th):
+            blocks = [(k, 0, self.x[2 * k:2 * k + 2].reshape(2, 1)) for k in range(20)]
+            return self.residual(th), BlockSparseJacobian.from_blocks(self.layout, blocks)
+
+    prov = Line()
+    th, rep = b2.lm_solve(prov, np.array([0.0]), b2.LMConfig(solver="dense"))
+    assert th[0] == pytest.approx(3.0, rel=1e-9)
+    with pytest.raises(b2.errors.NativeError):          # explicit-system Schur PCG is not on the device
+        b2.lm_solve(prov, np.array([0.0]), b2.LMConfig())
