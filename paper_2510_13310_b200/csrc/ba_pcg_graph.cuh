@@ -11,9 +11,12 @@
 // results are identical to the persistent kernel's (tests compare them
 // bitwise). lambda, the tolerance and the iteration cap live in device memory:
 // the instantiated graph is reused for every damped solve of the handle.
-// Sharded handles keep the persistent kernel (in-kernel exchange, comm.cuh).
+// Sharded handles add two kernels between the passes and q: k_gx_post (this
+// rank's camera sums into its exchange buffer) and k_gx_barrier (signal and
+// wait, comm.cuh); k_g_q then sums the ranks in rank order.
 #pragma once
 #include "ba_pcg.cuh"
+#include "comm.cuh"
 
 #define CGV_BLOCKS 148   // vector-phase grid (partials per reduction)
 
@@ -103,8 +106,9 @@ __global__ void __launch_bounds__(FZ_THREADS, 1) k_g_fused(BADev d, FusedTopo fz
 }
 
 // q = S p per slot (P3 of ba_k_pcg), p.q partials -> partA, shared-focal shares
-__global__ void __launch_bounds__(256) k_g_q(BADev d, FusedTopo fz, CGGraphDev g) {
+__global__ void __launch_bounds__(256) k_g_q(BADev d, FusedTopo fz, CGGraphDev g, CommDev cm) {
   if (*(volatile int*)(g.ic + 3)) return;
+  const long long xoff = cm.nranks > 1 ? (long long)(*cm.epoch & 1) * cm.cap : 0;
   __shared__ double smred[64];
   const int S = 8 * d.bp.C;
   const int stride = gridDim.x * blockDim.x;
@@ -128,7 +132,10 @@ __global__ void __launch_bounds__(256) k_g_q(BADev d, FusedTopo fz, CGGraphDev g
     }
     if (ok) {
       double acc = 0.0;
-      if (!g.fused) {
+      if (cm.nranks > 1) {            // camera sums exchanged by k_gx_post / k_gx_barrier
+        acc = comm_peer_load(cm.buf[0] + xoff + s);
+        for (int rk = 1; rk < cm.nranks; ++rk) acc += comm_peer_load(cm.buf[rk] + xoff + s);
+      } else if (!g.fused) {
         const int t0 = d.topo.cam_tile[c], t1 = d.topo.cam_tile[c + 1];
         for (int t = t0; t < t1; ++t) acc += d.tilebuf[8ll * t + k];
       } else {
@@ -147,6 +154,34 @@ __global__ void __launch_bounds__(256) k_g_q(BADev d, FusedTopo fz, CGGraphDev g
   }
   block_reduce<1>(v, smred);
   if (threadIdx.x == 0) g.partA[2ll * blockIdx.x] = v[0];
+}
+
+// sharded: this rank's camera sums -> own exchange buffer of the next epoch
+__global__ void __launch_bounds__(256) k_gx_post(BADev d, FusedTopo fz, CGGraphDev g, CommDev cm) {
+  if (*(volatile int*)(g.ic + 3)) return;
+  const int S = 8 * d.bp.C;
+  double* mine = cm.buf[cm.rank] + (long long)((*cm.epoch + 1) & 1) * cm.cap;
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x) {
+    const int c = s >> 3, k = s & 7;
+    double a = 0.0;
+    if (!g.fused) {
+      for (int t = d.topo.cam_tile[c]; t < d.topo.cam_tile[c + 1]; ++t) a += d.tilebuf[8ll * t + k];
+    } else {
+      for (int gq = 0; gq < g.ngrp; ++gq) a += fz.gpart[(long long)gq * S + s];
+    }
+    mine[s] = a;
+  }
+}
+
+// sharded: signal this epoch and wait for the peers (skipped identically on
+// every rank once the solve is done)
+__global__ void k_gx_barrier(CGGraphDev g, CommDev cm) {
+  if (*(volatile int*)(g.ic + 3)) return;
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    const unsigned long long e = *cm.epoch + 1;
+    comm_signal_wait(cm, e);
+    *cm.epoch = e;
+  }
 }
 
 // alpha = rho / p.q (every block, same order); x += a p, r -= a q, z = M r;

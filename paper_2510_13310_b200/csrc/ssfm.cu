@@ -86,6 +86,7 @@ struct ssfm_handle {
   int comm_nranks = 1;
   // graph PCG (ba_pcg_graph.cuh): built on first use, reused for every solve
   int graph_state = 0;          // 0 not built, 1 ready, -1 unavailable (persistent kernel)
+  bool graph_sharded = false;   // the built graph carries the exchange kernels
   cudaGraph_t pcg_graph = nullptr;
   cudaGraphExec_t pcg_exec = nullptr;
   CGGraphDev gdev{};
@@ -850,7 +851,11 @@ static int build_pcg_graph(ssfm_handle* h) {
     k_g_point<<<std::max(1, occ_p) * h->num_sms, PCG_THREADS, 0, cs>>>(d, g);
     if (d.topo.nt) k_g_camera<<<std::max(1, occ_c) * h->num_sms, PCG_THREADS, 0, cs>>>(d, g);
   }
-  k_g_q<<<CGV_BLOCKS, 256, 0, cs>>>(d, h->fz, g);
+  if (sharded(h)) {   // exchange of the camera half of S*p between the passes and q
+    k_gx_post<<<CGV_BLOCKS, 256, 0, cs>>>(d, h->fz, g, h->cm);
+    k_gx_barrier<<<1, 32, 0, cs>>>(g, h->cm);
+  }
+  k_g_q<<<CGV_BLOCKS, 256, 0, cs>>>(d, h->fz, g, h->cm);
   k_g_update<<<CGV_BLOCKS, 256, 0, cs>>>(d, g, CGV_BLOCKS);
   k_g_pupdate<<<CGV_BLOCKS, 256, 0, cs>>>(d, g, CGV_BLOCKS);
   k_g_scalars<<<1, 32, 0, cs>>>(d, g, CGV_BLOCKS, hc);
@@ -871,11 +876,20 @@ static int launch_pcg(ssfm_handle* h, double lam, const ssfm_lm_config* cfg, cud
   // (C4-BA fused 0.204 vs 0.229 ms, C1 0.025 vs 0.035 ms). SSFM_PCG_GRAPH=1/0
   // forces either.
   // (decided at handle creation, setup_ba_pcg; built here on first use)
-  if (h->kind == 0 && !sharded(h) && h->graph_state == 0) {
+  if (h->kind == 0 && h->graph_state == 1 && h->graph_sharded != sharded(h)) {
+    // connected after the graph was built: rebuild it with the exchange kernels
+    cudaGraphExecDestroy(h->pcg_exec);
+    cudaGraphDestroy(h->pcg_graph);
+    h->pcg_exec = nullptr;
+    h->pcg_graph = nullptr;
+    h->graph_state = 0;
+  }
+  if (h->kind == 0 && h->graph_state == 0) {
     int rc = build_pcg_graph(h);
     if (rc) return rc;
+    h->graph_sharded = sharded(h);
   }
-  if (h->kind == 0 && !sharded(h) && h->graph_state == 1) {
+  if (h->kind == 0 && h->graph_state == 1) {
     CGGraphDev& g = h->gdev;
     k_g_setparams<<<1, 1, 0, st>>>(g, lam, tol, max_it);
     k_g_init<<<CGV_BLOCKS, 256, 0, st>>>(h->ba, g);

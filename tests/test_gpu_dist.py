@@ -37,9 +37,10 @@ def scene(cams=40, pts=3000, k=5, seed=0):
     return synth.perturb_arrays(obs, rot_deg=1.0, center_frac=0.01, focal_frac=0.02, point_frac=0.005, seed=1)
 
 
-def solve_local_shards(gpu, st, world, cfg, fused="1"):
+def solve_local_shards(gpu, st, world, cfg, fused="1", graph="0"):
     os.environ["SSFM_PCG_SMS"] = str(140 // world)
     os.environ["SSFM_FUSED"] = fused
+    os.environ["SSFM_PCG_GRAPH"] = graph
     try:
         probs = [bd.ShardedBAProblem(st, b2.RobustLoss("huber", 1.0), rank=r, world=world, comm="local")
                  for r in range(world)]
@@ -47,6 +48,7 @@ def solve_local_shards(gpu, st, world, cfg, fused="1"):
     finally:
         os.environ.pop("SSFM_PCG_SMS")
         os.environ.pop("SSFM_FUSED")
+        os.environ.pop("SSFM_PCG_GRAPH")
     out = [None] * world
     errs = []
 
@@ -67,8 +69,9 @@ def solve_local_shards(gpu, st, world, cfg, fused="1"):
     return probs, out
 
 
-@pytest.mark.parametrize("world,fused", [(2, "1"), (3, "1"), (2, "0")])
-def test_local_shards_match_single_gpu(gpu, world, fused):
+@pytest.mark.parametrize("world,fused,graph", [(2, "1", "0"), (3, "1", "0"), (2, "0", "0"), (2, "0", "1"),
+                                              (3, "1", "1")])
+def test_local_shards_match_single_gpu(gpu, world, fused, graph):
     st = scene()
     cfg = b2.LMConfig(max_iterations=15)
     os.environ["SSFM_FUSED"] = fused          # the same operator as the shards
@@ -78,7 +81,7 @@ def test_local_shards_match_single_gpu(gpu, world, fused):
     finally:
         os.environ.pop("SSFM_FUSED")
     th1, rep1 = b2.lm_solve(single, single.encode(), cfg)
-    probs, out = solve_local_shards(gpu, st, world, cfg, fused)
+    probs, out = solve_local_shards(gpu, st, world, cfg, fused, graph)
     reps = [o[1] for o in out]
     # identical on every shard (bitwise)
     for rep in reps[1:]:
