@@ -58,6 +58,7 @@ __device__ __forceinline__ double cta_partials_sum(const double* part, int n, in
 }
 
 // P1 for a camera vector v -> y (per point): y_j = Cinv_j sum_o Jp^T (Jc v_c)
+template <bool RO = false>
 __device__ __forceinline__ void ba_point_pass(const BADev& d, const double* v, double* y,
                                               double (*sm)[SSFM_BATCH][3]) {
   const unsigned long long pstream = pol_evict_first(), pkeep = pol_evict_last();
@@ -81,8 +82,13 @@ __device__ __forceinline__ void ba_point_pass(const BADev& d, const double* v, d
         for (int k = 0; k < BA_JREC; ++k) J[k] = ldg_stream(d.Jpm + k * Np + i, pstream);
         const int c = ldg_stream_i(d.topo.pm_cam + i, pstream);
         double pc[8];
-        ld_v4(v + 8ll * c, pc);
-        ld_v4(v + 8ll * c + 4, pc + 4);
+        if constexpr (RO) {
+          ld_v4_ro(v + 8ll * c, pc, pkeep);
+          ld_v4_ro(v + 8ll * c + 4, pc + 4, pkeep);
+        } else {
+          ld_v4(v + 8ll * c, pc);
+          ld_v4(v + 8ll * c + 4, pc + 4);
+        }
         if (d.bp.focal_mode == 2) pc[7] = v[7];   // shared focal (camera 0, slot 7)
         double t[2];
         ba_jc_mul(J, pc, t);
@@ -114,6 +120,7 @@ __device__ __forceinline__ void ba_point_pass(const BADev& d, const double* v, d
 // one butterfly reduction; no CTA barriers (a block reduction per 256-obs
 // tile left 30 % of the warps waiting at __syncthreads). Fixed order:
 // deterministic.
+template <bool RO = false>
 __device__ __forceinline__ void ba_camera_pass(const BADev& d, const double* y, double* tile8,
                                                double* smred) {
   (void)smred;
@@ -134,7 +141,8 @@ __device__ __forceinline__ void ba_camera_pass(const BADev& d, const double* y, 
       for (int k = 0; k < BA_JREC; ++k) J[k] = ldg_stream(d.Jcm + k * Np + i, pstream);
       const int j = ldg_stream_i(d.topo.cm_pt + i, pstream);
       double yj[4];
-      ld_v4_hint(y + 4ll * j, yj, pkeep);
+      if constexpr (RO) ld_v4_ro(y + 4ll * j, yj, pkeep);
+      else ld_v4_hint(y + 4ll * j, yj, pkeep);
       double tt[2], u[8];
       ba_jp_mul(J, yj, tt);
       ba_jct_mul(J, tt, u);

@@ -86,13 +86,13 @@ __global__ void k_g_init2(BADev d, CGGraphDev g, int nblk) {
 __global__ void __launch_bounds__(PCG_THREADS, 4) k_g_point(BADev d, CGGraphDev g) {
   if (*(volatile int*)(g.ic + 3)) return;
   __shared__ double smp[PCG_THREADS / 32][SSFM_BATCH][3];
-  ba_point_pass(d, g.p, d.yv, smp);
+  ba_point_pass<true>(d, g.p, d.yv, smp);   // p is constant during this kernel
 }
 
 __global__ void __launch_bounds__(PCG_THREADS, 4) k_g_camera(BADev d, CGGraphDev g) {
   if (*(volatile int*)(g.ic + 3)) return;
   __shared__ double smred[(PCG_THREADS / 32) * 8];
-  ba_camera_pass(d, d.yv, d.tilebuf, smred);
+  ba_camera_pass<true>(d, d.yv, d.tilebuf, smred);   // y is constant during this kernel
 }
 
 template <int SL>

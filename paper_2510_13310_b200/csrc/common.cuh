@@ -136,6 +136,14 @@ __device__ __forceinline__ void ld_v4_hint(const double* a, double* x, unsigned 
   asm volatile("ld.global.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
                : "=d"(x[0]), "=d"(x[1]), "=d"(x[2]), "=d"(x[3]) : "l"(a), "l"(pol));
 }
+// read-only variant for kernels in which the gathered vector is constant (the
+// graph-PCG passes): non-coherent path, no L1 allocation (random 32-byte
+// gathers have little L1 reuse and the fills compete with the streams)
+__device__ __forceinline__ void ld_v4_ro(const double* a, double* x, unsigned long long pol) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+               : "=d"(x[0]), "=d"(x[1]), "=d"(x[2]), "=d"(x[3]) : "l"(a), "l"(pol));
+}
+
 __device__ __forceinline__ void st_hint(double* a, double v, unsigned long long pol) {
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
 }
