@@ -52,7 +52,7 @@ struct GPDev {
   double* gcam;           // [3C] J^T r camera part
   double* Minv_pt;        // [6P] C'_j^-1
   double* y0;             // [3P]
-  double* yv;             // [3P]
+  double* yv;             // [4P] (padded for 32-byte gathers)
   double* Bp;             // [6C] B'_c (upper)
   double* Minv;           // [16C] preconditioner (4x4 slots, 3x3 used)
   double* bred;           // [4C]
@@ -524,9 +524,8 @@ __device__ __forceinline__ void gp_point_pass(const GPDev& g, const double* v, d
         const int c = __ldg(g.topo.pm_cam + i);
         const double at = gp_at(g, c, rec[0]);
         const double inv = gp_inv(lam, rec);
-        double pc[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) pc[k] = v[4ll * c + k];
+        double pc[4];
+        ld_v4(v + 4ll * c, pc);   // 4 slots per camera: one 32-byte gather
         gp_u_mul(at, rec[0], inv, rec + 1, pc, val);
       }
 #pragma unroll
@@ -545,37 +544,40 @@ __device__ __forceinline__ void gp_point_pass(const GPDev& g, const double* v, d
       for (int k = 0; k < 6; ++k) M[k] = __ldg(g.Minv_pt + 6ll * my_pt + k);
       sym3_matvec(M, acc, w);
 #pragma unroll
-      for (int k = 0; k < 3; ++k) y[3ll * my_pt + k] = w[k];
+      for (int k = 0; k < 3; ++k) y[4ll * my_pt + k] = w[k];   // padded: one 32-byte gather
     }
   }
 }
 
 __device__ __forceinline__ void gp_camera_pass(const GPDev& g, const double* y, double* tile4,
                                                double* smred) {
+  // one warp per camera tile, register accumulation, one butterfly (no CTA
+  // barriers; same structure as ba_camera_pass)
+  (void)smred;
   const long long Np = g.Npad;
   const double lam = g.lam;
-  for (int t = blockIdx.x; t < g.topo.nt; t += gridDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  for (int t = gw; t < g.topo.nt; t += warps) {
     const int o0 = __ldg(g.topo.tile_obs + t), o1 = __ldg(g.topo.tile_obs + t + 1);
     const int c = __ldg(g.topo.tile_cam + t);
-    const int i = o0 + threadIdx.x;
     double o[3] = {0.0, 0.0, 0.0};
-    if (i < o1) {
+    for (int i = o0 + lane; i < o1; i += 32) {
       double rec[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) rec[k] = __ldg(g.Jcm + k * Np + i);
       const int j = __ldg(g.topo.cm_pt + i);
       const double at = gp_at(g, c, rec[0]);
       const double inv = gp_inv(lam, rec);
-      double yj[3];
+      double yj[4], u[3];
+      ld_v4(y + 4ll * j, yj);
+      gp_u_mul(at, rec[0], inv, rec + 1, yj, u);
 #pragma unroll
-      for (int k = 0; k < 3; ++k) yj[k] = y[3ll * j + k];
-      gp_u_mul(at, rec[0], inv, rec + 1, yj, o);
+      for (int k = 0; k < 3; ++k) o[k] += u[k];
     }
-    block_reduce<3>(o, smred);
-    if (threadIdx.x == 0) {
-#pragma unroll
-      for (int k = 0; k < 3; ++k) tile4[4ll * t + k] = o[k];
-    }
+    warp_allreduce<3>(o);
+    if (lane < 3) tile4[4ll * t + lane] = lane == 0 ? o[0] : (lane == 1 ? o[1] : o[2]);
   }
 }
 

@@ -518,7 +518,7 @@ extern "C" int ssfm_create_gp(const ssfm_gp_desc* desc, void* stream, ssfm_handl
   if ((rc = dalloc(h, &g.gcam, 3ll * C))) return fail(rc);
   if ((rc = dalloc(h, &g.Minv_pt, 6ll * P))) return fail(rc);
   if ((rc = dalloc(h, &g.y0, 3ll * P))) return fail(rc);
-  if ((rc = dalloc(h, &g.yv, 3ll * P))) return fail(rc);
+  if ((rc = dalloc(h, &g.yv, 4ll * P))) return fail(rc);   // padded: 32-byte gathers
   if ((rc = dalloc(h, &g.Bp, 6ll * C))) return fail(rc);
   if ((rc = dalloc(h, &g.Minv, 16ll * C))) return fail(rc);
   if ((rc = dalloc(h, &g.bred, 4ll * C))) return fail(rc);
