@@ -453,28 +453,42 @@ def run_reference(args, ws, rank):
     if rank != 0:
         return None
     ref, why = _import_reference()
-    cams, pts, k, sigma, delta, label = CONFIGS[args.config]
     if ref is None:
         return {"impl": "reference", "unavailable": why}
+    if args.config in PIPELINE:
+        return {"impl": "reference", "unavailable": "the reference has no GP->BA pipeline function "
+                "(SURVEY.md 8(d) C4); its stages are timed by --config c4gp / c4ba"}
+    cams, pts, k, sigma, delta, label = CONFIGS[args.config]
     from sparsesfm import synth_metrics as rsm
-    scams, spts, sk = REF_SAMPLE if args.config == "c5" else (cams, pts, k)
+    is_gp = args.config in GP_CONFIGS
+    # bounded samples keep the CPU run to a few minutes: C5 (does not fit /
+    # ~2 min per iteration) and the 4M-observation GP stage
+    scams, spts, sk = REF_SAMPLE if args.config == "c5" else \
+        ((1000, 50000, 8) if args.config == "c4gp" else (cams, pts, k))
     truth, obs = rsm.generate(rsm.SynthConfig(num_cameras=scams, num_points=spts,
                                               visibility_fraction=sk / scams, pixel_noise_sigma=sigma,
                                               seed=0))
-    start = rsm.perturb(obs, rot_deg=1.0, center_frac=0.01, focal_frac=0.02, point_frac=0.005, seed=1)
-    prob = ref.BAProblem(start, ref.RobustLoss("huber", delta))
-    n = start.num_observations
+    if is_gp:
+        prob = ref.fix_gauge(ref.make_rays(obs, False, ref.RobustLoss("huber", delta), seed=0))
+        th0 = prob.initial_theta()
+        n = obs.num_observations
+    else:
+        start = rsm.perturb(obs, rot_deg=1.0, center_frac=0.01, focal_frac=0.02, point_frac=0.005, seed=1)
+        prob = ref.BAProblem(start, ref.RobustLoss("huber", delta))
+        th0 = prob.encode()
+        n = start.num_observations
     cfg = ref.LMConfig(max_iterations=args.warmup + args.steps)
     t0 = time.perf_counter()
-    _, rep = ref.lm_solve(prob, prob.encode(), cfg)
+    _, rep = ref.lm_solve(prob, th0, cfg)
     wall = time.perf_counter() - t0
     its = rep.iterations
     timed = its[args.warmup:] or its
     t_timed = sum(i.wall_time_ns for i in timed) / 1e9
     value = n * len(timed) / t_timed
     cores = int(os.environ.get("SPARSESFM_WORKERS", "1"))
-    sample = (f"reference sparsesfm BA {scams} cams / {spts} pts / {n} obs (k={sk}"
-              f"{', bounded C5-shaped sample' if args.config == 'c5' else ''}); "
+    bounded = args.config in ("c5", "c4gp")
+    sample = (f"reference sparsesfm {'GP' if is_gp else 'BA'} {scams} cams / {spts} pts / {n} obs (k={sk}"
+              f"{', bounded sample of the config shape' if bounded else ''}); "
               f"{len(its)} LM iterations, last {len(timed)} timed; total {wall:.1f} s")
     return {"metric": METRIC, "value": value, "unit": "obs/s", "n_gpus": ws, "steps": len(timed),
             "warmup": args.warmup, "ms_per_step": 1e3 * t_timed / len(timed), "higher_is_better": True,
