@@ -380,6 +380,8 @@ def run_b200(args, ws, rank, local):
         h2d = (Nl * (np.asarray(arr_host.cam_idx).itemsize + np.asarray(arr_host.pt_idx).itemsize
                      + (24 if is_gp else 16)) + C * (16 + 16 + 8) + theta_host.nbytes)
         e2e = {"value": N * its / wall, "unit": "obs/s",
+               "first_iteration_ms": round(rep_e.iterations[0].device_ms, 3) if rep_e.iterations else None,
+               "time_to_solution_s": round(wall, 3),
                "h2d_bytes_per_step": int(h2d / its), "d2h_bytes_per_step": int(theta_host.nbytes / its),
                "iterations": its, "wall_s": round(wall, 3), "device_ms": round(e_ms, 1),
                "termination": rep_e.termination}
@@ -396,6 +398,10 @@ def run_b200(args, ws, rank, local):
                    "l2": "inputs larger than L2 (J 2x2.56 GB)" if N >= 10**6 else "small (latency bound)"},
         "cg_iters_per_step": [i.cg_iters for i in rep_t.iterations],
         "lm_ms_per_iteration": [round(i.device_ms, 3) for i in rep_t.iterations],
+        # LM-iteration time = median over iterations 2..n; the
+        # first iteration of a solve (setup, first linearization) separately
+        "lm_ms_median": round(statistics.median([i.device_ms for i in rep_t.iterations[1:]]
+                                                or [i.device_ms for i in rep_t.iterations]), 3),
         "roofline": roof, "e2e": e2e, "clocks": clocks, "gpu_launches": int(launches.value),
     }
     if rank == 0 and not args.no_cpu_baseline and not is_gp:
