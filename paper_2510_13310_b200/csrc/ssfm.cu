@@ -87,6 +87,8 @@ struct ssfm_handle {
   // graph PCG (ba_pcg_graph.cuh): built on first use, reused for every solve
   int graph_state = 0;          // 0 not built, 1 ready, -1 unavailable (persistent kernel)
   bool graph_sharded = false;   // the built graph carries the exchange kernels
+  bool graph_pending = false;   // a graph solve whose body kernels are not yet counted
+  int graph_body_kernels = 0;   // kernels per WHILE-body iteration
   cudaGraph_t pcg_graph = nullptr;
   cudaGraphExec_t pcg_exec = nullptr;
   CGGraphDev gdev{};
@@ -859,6 +861,7 @@ static int build_pcg_graph(ssfm_handle* h) {
   k_g_update<<<CGV_BLOCKS, 256, 0, cs>>>(d, g, CGV_BLOCKS);
   k_g_pupdate<<<CGV_BLOCKS, 256, 0, cs>>>(d, g, CGV_BLOCKS);
   k_g_scalars<<<1, 32, 0, cs>>>(d, g, CGV_BLOCKS, hc);
+  h->graph_body_kernels = (g.fused ? 1 : 2) + (sharded(h) ? 2 : 0) + 4;
   if ((e = cudaStreamEndCapture(cs, &body))) return unavailable(e);
   if ((e = cudaGraphInstantiate(&h->pcg_exec, h->pcg_graph, 0))) return unavailable(e);
   cudaStreamDestroy(cs);
@@ -896,6 +899,7 @@ static int launch_pcg(ssfm_handle* h, double lam, const ssfm_lm_config* cfg, cud
     k_g_init2<<<1, 32, 0, st>>>(h->ba, g, CGV_BLOCKS);
     CU(cudaGraphLaunch(h->pcg_exec, st));
     count_launch(h, 3);
+    h->graph_pending = true;   // the body kernels are counted once the CG count is known
     return SSFM_OK;
   }
   if (h->kind == 0) {
@@ -1176,6 +1180,10 @@ extern "C" int ssfm_lm_solve(ssfm_handle* h, double* theta_io, const ssfm_lm_con
       h->prof.pcg_launches += 1;
       h->prof.cg_iters += m.ctl.iters;
       for (int k = 0; k < 5; ++k) h->prof.phase_ms[k] += m.ctl.phase_ns[k] * 1e-6;
+    }
+    if (h->graph_pending) {   // graph PCG: the WHILE body ran once per CG iteration (at least once)
+      count_launch(h, h->graph_body_kernels * std::max(1, m.ctl.iters));
+      h->graph_pending = false;
     }
     const int code = status_to_code(m.status);
     if (code == SSFM_COMM_ERROR) {   // a peer did not answer: the exchanged values are not valid
