@@ -18,6 +18,7 @@
 #pragma once
 #include "ba_kernels.cuh"
 #include "comm.cuh"
+#include "fused.cuh"
 #include <cooperative_groups.h>
 
 #define GP_JREC 4
@@ -581,14 +582,140 @@ __device__ __forceinline__ void gp_camera_pass(const GPDev& g, const double* y, 
   }
 }
 
-__global__ void __launch_bounds__(PCG_THREADS) gp_k_pcg(GPDev g, CommDev cm, double lam, int max_iters,
-                                                        double cg_tol, double* x, double* r,
-                                                        double* z, double* p, double* q,
-                                                        double* part, CGCtl* ctl) {
+// Fused single pass for GP (the BA version is ba_fused_pass, fused.cuh): y_j
+// for every point of the warp's batch, then each observation's camera term
+// U'_o y_j added into the CTA's shared copy of the camera vector (4 slots per
+// camera) in ticket order. The GP camera vector always fits one CTA.
+// Dynamic shared memory: acc [4C] | stage [FZ_WARPS][4][32] | cnt [C] ints.
+__device__ __forceinline__ void gp_fused_pass(const GPDev& g, const FusedTopo& fz, const double* __restrict__ v,
+                                              double* dyn, double (*smv)[SSFM_BATCH][3],
+                                              double (*smy)[SSFM_BATCH][3], int (*smown)[SSFM_BATCH]) {
+  constexpr int SL = 4;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = blockIdx.x, ngrp = gridDim.x;
+  const int C = g.gp.C;
+  const long long Np = g.Npad;
+  const double lam = g.lam;
+  double* acc = dyn;
+  double* stage = dyn + (long long)SL * C + (long long)warp * 32 * SL;
+  int* cnt = reinterpret_cast<int*>(dyn + (long long)SL * C + FZ_WARPS * 32 * SL);
+  for (int k = threadIdx.x; k < SL * C; k += blockDim.x) acc[k] = 0.0;
+  for (int k = threadIdx.x; k < C; k += blockDim.x) cnt[k] = 0;
+  __syncthreads();
+  const int sstride = ngrp * FZ_WARPS;
+  for (int b = grp * FZ_WARPS + warp; b < g.topo.nb; b += sstride) {
+    const int ob0 = __ldg(g.topo.bat_obs + b), ob1 = __ldg(g.topo.bat_obs + b + 1);
+    const int pb0 = __ldg(g.topo.bat_pt + b), pb1 = __ldg(g.topo.bat_pt + b + 1);
+    const int rounds = (ob1 - ob0 + 31) >> 5;
+    const int my_pt = pb0 + lane;
+    const bool own = my_pt < pb1;
+    int ps = 0, pe = 0;
+    if (own) { ps = __ldg(g.topo.pt_seg + my_pt); pe = __ldg(g.topo.pt_seg + my_pt + 1); }
+    double rec[4] = {0.0, 0.0, 0.0, 0.0};
+    int c = 0, tk = 0;
+    double a3[3] = {0.0, 0.0, 0.0};
+    for (int r = 0; r < rounds; ++r) {
+      const int base = ob0 + 32 * r;
+      const int i = base + lane;
+      double val[3] = {0.0, 0.0, 0.0};
+      if (i < ob1) {
+        c = __ldg(g.topo.pm_cam + i);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) rec[k] = __ldg(g.Jpm + k * Np + i);
+        tk = __ldg(fz.tick + i);
+        double pc[4];
+        ld_v4(v + 4ll * c, pc);
+        gp_u_mul(gp_at(g, c, rec[0]), rec[0], gp_inv(lam, rec), rec + 1, pc, val);
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) smv[warp][lane][k] = val[k];
+      __syncwarp();
+      const int lo = max(ps, base), hi = min(pe, base + SSFM_BATCH);
+      for (int o = lo; o < hi; ++o) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) a3[k] += smv[warp][o - base][k];
+        smown[warp][o - base] = lane;
+      }
+      __syncwarp();
+    }
+    if (own) {
+      double M[6], w[3];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) M[k] = __ldg(g.Minv_pt + 6ll * my_pt + k);
+      sym3_matvec(M, a3, w);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) smy[warp][lane][k] = w[k];
+    }
+    __syncwarp();
+    for (int r = 0; r < rounds; ++r) {
+      const int i = ob0 + 32 * r + lane;
+      const bool have = i < ob1;
+      double u[SL] = {0.0, 0.0, 0.0, 0.0};
+      if (have) {
+        if (rounds > 1) {
+          c = __ldg(g.topo.pm_cam + i);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) rec[k] = __ldg(g.Jpm + k * Np + i);
+          tk = __ldg(fz.tick + i);
+        }
+        const int owner = rounds > 1 ? 0 : smown[warp][lane];
+        double y[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) y[k] = smy[warp][owner][k];
+        gp_u_mul(gp_at(g, c, rec[0]), rec[0], gp_inv(lam, rec), rec + 1, y, u);
+      }
+      const unsigned same = __match_any_sync(SSFM_FULL, have ? c : -1);
+      const bool dup = __popc(same) > 1;
+      if (__any_sync(SSFM_FULL, dup && have)) {
+#pragma unroll
+        for (int j = 0; j < SL; ++j) stage[j * 32 + lane] = u[j];
+        __syncwarp();
+        if (have && dup && lane == __ffs(same) - 1) {
+#pragma unroll
+          for (int j = 0; j < SL; ++j) u[j] = 0.0;
+          for (unsigned m = same; m; m &= m - 1) {
+            const int l = __ffs(m) - 1;
+#pragma unroll
+            for (int j = 0; j < SL; ++j) u[j] += stage[j * 32 + l];
+          }
+        }
+        __syncwarp();
+      }
+      if (have && lane == __ffs(same) - 1) {
+        int spins = 0;
+        while (ld_acquire_smem(cnt + c) != tk) {
+          if (++spins > FZ_SPIN_LIMIT) { atomicOr(g.status, ST_SCHEDULE); break; }
+        }
+        fz_add<SL>(acc, c, u);
+        st_release_smem(cnt + c, tk + 1);
+      }
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  double* dst = fz.gpart + (long long)grp * SL * C;
+  for (int k = threadIdx.x; k < SL * C; k += blockDim.x) {
+    const int cc = k / SL, j = k - cc * SL;
+    dst[k] = acc[fz_slot<SL>(cc, j)];
+  }
+}
+
+// FUSED: one-pass operator (gp_fused_pass, 512 threads, dynamic shared
+// camera vector, 2 CTAs per SM: 62 registers, no spills; 1 CTA per SM at 101
+// registers was 0.207 vs 0.158 ms per C4 GP CG iteration); otherwise the
+// two-pass operator (256 threads).
+template <bool FUSED>
+__global__ void __launch_bounds__(FUSED ? FZ_THREADS : PCG_THREADS, FUSED ? 2 : 4)
+gp_k_pcg(GPDev g, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg_tol, double* x, double* r,
+         double* z, double* p, double* q, double* part, CGCtl* ctl) {
+  constexpr int NT = FUSED ? FZ_THREADS : PCG_THREADS;
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
-  __shared__ double smp[PCG_THREADS / 32][SSFM_BATCH][3];
-  __shared__ double smred[(PCG_THREADS / 32) * 8];
+  __shared__ double smp[NT / 32][SSFM_BATCH][3];
+  __shared__ double smy[FUSED ? NT / 32 : 1][SSFM_BATCH][3];
+  __shared__ int smown[FUSED ? NT / 32 : 1][SSFM_BATCH];
+  __shared__ double smred[(NT / 32) * 8];
   __shared__ double smb[4];
+  extern __shared__ double gdyn[];
   g.lam = lam;
   const int S = 4 * g.gp.C;
   const int stride = gridDim.x * blockDim.x;
@@ -596,9 +723,13 @@ __global__ void __launch_bounds__(PCG_THREADS) gp_k_pcg(GPDev g, CommDev cm, dou
   double* tile4 = g.tilebuf;
   const int NP = gridDim.x;
   auto local_cam = [&](int s) -> double {   // local camera half of S*p, slot s = 4c + k
-    const int c = s >> 2, k = s & 3;
     double a = 0.0;
-    for (int t = g.topo.cam_tile[c]; t < g.topo.cam_tile[c + 1]; ++t) a += tile4[4ll * t + k];
+    if constexpr (FUSED) {
+      for (int gq = 0; gq < NP; ++gq) a += fz.gpart[(long long)gq * S + s];
+    } else {
+      const int c = s >> 2, k = s & 3;
+      for (int t = g.topo.cam_tile[c]; t < g.topo.cam_tile[c + 1]; ++t) a += tile4[4ll * t + k];
+    }
     return a;
   };
   unsigned long long ep = cm.nranks > 1 ? *cm.epoch : 0ull;
@@ -634,9 +765,13 @@ __global__ void __launch_bounds__(PCG_THREADS) gp_k_pcg(GPDev g, CommDev cm, dou
   if (rn > tol) {
     while (true) {
       if (iters >= max_iters) { flag = ST_CG_MAXITER; break; }
-      gp_point_pass(g, p, g.yv, smp);
-      grid.sync();
-      gp_camera_pass(g, g.yv, tile4, smred);
+      if constexpr (FUSED) {
+        gp_fused_pass(g, fz, p, gdyn, smp, smy, smown);
+      } else {
+        gp_point_pass(g, p, g.yv, smp);
+        grid.sync();
+        gp_camera_pass(g, g.yv, tile4, smred);
+      }
       grid.sync();
       if (cm.nranks > 1) {   // exchange the camera half of S*p with the peers (comm.cuh)
         ++ep;

@@ -279,7 +279,97 @@ static int try_fused_ba(ssfm_handle* h, int* ok) {
   return SSFM_OK;
 }
 
+// Ticket schedule of the fused operator (fused.cuh): stable sort of the
+// observations by (CTA group, camera), runs walked in order. gpart gets
+// `slots` doubles per camera per CTA group. *ok = 0 (fz cleared) when a camera
+// has more than FZ_MAX_TICKET units in one group: use the two-pass operator.
+static int build_fused_schedule(ssfm_handle* h, int slots, int* status, cudaStream_t st, int* ok) {
+  const Topo& T = h->topo;
+  FusedTopo& fz = h->fz;
+  const int C = T.C;
+  CU(cudaMemsetAsync(status, 0, sizeof(int), st));
+  fz.nsteps = nblk(T.nb, FZ_WARPS);
+  DALLOC(fz.tick, T.N);
+  DALLOC(fz.gpart, (long long)fz.ngrp * slots * C);
+  unsigned long long *key, *skey;
+  int *unit, *idx, *sidx;
+  std::vector<void*> tmp;
+  auto talloc = [&](void** p, size_t b) { cudaError_t e = cudaMalloc(p, b); if (!e) tmp.push_back(*p); return e; };
+  auto tfree = [&]() { cudaStreamSynchronize(st); for (void* q : tmp) cudaFree(q); };
+  const long long N = T.N;
+  if (talloc((void**)&key, 8 * N) || talloc((void**)&skey, 8 * N) || talloc((void**)&unit, 4 * N) ||
+      talloc((void**)&idx, 4 * N) || talloc((void**)&sidx, 4 * N)) {
+    tfree();
+    return set_err(SSFM_CUDA_ERROR, "fused schedule: out of device memory");
+  }
+  k_fz_keys<<<nblk((long long)T.nb * 32, 256), 256, 0, st>>>(T, fz.ngrp, key, unit, idx);
+  int kbits = 1;
+  while ((1ull << kbits) < (unsigned long long)fz.ngrp * C) ++kbits;
+  size_t sb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, sb, key, skey, idx, sidx, (int)N, 0, kbits, st);
+  void* stmp = nullptr;
+  if (talloc(&stmp, sb)) { tfree(); return set_err(SSFM_CUDA_ERROR, "fused schedule: out of device memory"); }
+  cub::DeviceRadixSort::SortPairs(stmp, sb, key, skey, idx, sidx, (int)N, 0, kbits, st);
+  k_fz_tickets<<<nblk(N, 256), 256, 0, st>>>(skey, sidx, unit, N, fz.tick, status);
+  int hst = 0;
+  cudaMemcpyAsync(&hst, status, sizeof(int), cudaMemcpyDeviceToHost, st);
+  tfree();
+  *ok = 1;
+  if (hst & ST_SCHEDULE) {
+    h->fz = FusedTopo{};
+    cudaMemsetAsync(status, 0, sizeof(int), st);
+    *ok = 0;
+  }
+  CU(cudaGetLastError());
+  return SSFM_OK;
+}
+
 static int setup_ba_pcg_op(ssfm_handle* h, cudaStream_t st);
+// GP PCG operator: fused single pass (gp_fused_pass) for N >= 1M observations
+// when the 4-slot camera vector fits one CTA's shared memory, else two-pass.
+// Measured (1xB200, ms per CG iteration): C4 GP 4M obs 0.158 fused vs 0.175
+// two-pass; C2 GP 300k obs 0.042 vs 0.034 (too little work per CTA for the
+// ticket-ordered accumulation to pay). SSFM_FUSED=0/1 forces either.
+static int setup_gp_pcg_op(ssfm_handle* h, cudaStream_t st) {
+  h->pcg_sms = pcg_sms_of(h);
+  const int C = h->gp.gp.C;
+  const char* env = getenv("SSFM_FUSED");
+  const bool want = env ? env[0] != '0' : h->topo.N >= 1000000;
+  if (want && C < FZ_MAX_CAMERAS) {
+    cudaFuncAttributes fa;
+    CU(cudaFuncGetAttributes(&fa, gp_k_pcg<true>));
+    int optin = 0;
+    CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+    const size_t dyn = sizeof(double) * (4ull * C + FZ_WARPS * 32 * 4) + sizeof(int) * (size_t)C;
+    int occ = 0;
+    if (fa.sharedSizeBytes + dyn <= (size_t)optin) {
+      CU(cudaFuncSetAttribute(gp_k_pcg<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gp_k_pcg<true>, FZ_THREADS, dyn));
+    }
+    if (occ >= 1) {
+      h->pcg_grid = occ * h->pcg_sms;
+      h->pcg_threads = FZ_THREADS;
+      h->pcg_smem = dyn;
+      h->pcg_fn = (void*)gp_k_pcg<true>;
+      h->fz.G = 1;
+      h->fz.SL = 4;
+      h->fz.ngrp = h->pcg_grid;
+      int ok = 0, rc;
+      if ((rc = build_fused_schedule(h, 4, h->gp.status, st, &ok))) return rc;
+      if (ok) return SSFM_OK;
+    }
+  }
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gp_k_pcg<false>, PCG_THREADS, 0) || occ < 1)
+    return set_err(SSFM_CUDA_ERROR, "occupancy query for the PCG kernel failed");
+  h->pcg_grid = occ * h->pcg_sms;
+  h->pcg_threads = PCG_THREADS;
+  h->pcg_smem = 0;
+  h->pcg_fn = (void*)gp_k_pcg<false>;
+  h->fz = FusedTopo{};
+  return SSFM_OK;
+}
+
 
 static int setup_ba_pcg(ssfm_handle* h, cudaStream_t st) {
   int rc = setup_ba_pcg_op(h, st);
@@ -291,7 +381,6 @@ static int setup_ba_pcg(ssfm_handle* h, cudaStream_t st) {
 }
 
 static int setup_ba_pcg_op(ssfm_handle* h, cudaStream_t st) {
-  const Topo& T = h->topo;
   // SSFM_PCG_SMS caps the SMs of the persistent PCG grid (several sharded
   // handles on one device must be co-resident: their kernels wait on each other)
   h->pcg_sms = pcg_sms_of(h);
@@ -311,41 +400,7 @@ static int setup_ba_pcg_op(ssfm_handle* h, cudaStream_t st) {
   if (want && multi && !ok && force_g <= 4 && (rc = try_fused_ba<2>(h, &ok))) return rc;
   if (want && multi && !ok && (rc = try_fused_ba<1>(h, &ok))) return rc;
   if (ok) {
-    FusedTopo& fz = h->fz;
-    CU(cudaMemsetAsync(h->ba.status, 0, sizeof(int), st));
-    fz.nsteps = nblk(T.nb, FZ_WARPS);
-    DALLOC(fz.tick, T.N);
-    DALLOC(fz.gpart, (long long)fz.ngrp * 8 * C);
-    // tickets: stable sort of observations by (CTA group, camera), runs walked in order
-    unsigned long long *key, *skey;
-    int *unit, *idx, *sidx;
-    std::vector<void*> tmp;
-    auto talloc = [&](void** p, size_t b) { cudaError_t e = cudaMalloc(p, b); if (!e) tmp.push_back(*p); return e; };
-    auto tfree = [&]() { cudaStreamSynchronize(st); for (void* q : tmp) cudaFree(q); };
-    const long long N = T.N;
-    if (talloc((void**)&key, 8 * N) || talloc((void**)&skey, 8 * N) || talloc((void**)&unit, 4 * N) ||
-        talloc((void**)&idx, 4 * N) || talloc((void**)&sidx, 4 * N)) {
-      tfree();
-      return set_err(SSFM_CUDA_ERROR, "fused schedule: out of device memory");
-    }
-    k_fz_keys<<<nblk((long long)T.nb * 32, 256), 256, 0, st>>>(T, fz.ngrp, key, unit, idx);
-    int kbits = 1;
-    while ((1ull << kbits) < (unsigned long long)fz.ngrp * C) ++kbits;
-    size_t sb = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, sb, key, skey, idx, sidx, (int)N, 0, kbits, st);
-    void* stmp = nullptr;
-    if (talloc(&stmp, sb)) { tfree(); return set_err(SSFM_CUDA_ERROR, "fused schedule: out of device memory"); }
-    cub::DeviceRadixSort::SortPairs(stmp, sb, key, skey, idx, sidx, (int)N, 0, kbits, st);
-    k_fz_tickets<<<nblk(N, 256), 256, 0, st>>>(skey, sidx, unit, N, fz.tick, h->ba.status);
-    int hst = 0;
-    cudaMemcpyAsync(&hst, h->ba.status, sizeof(int), cudaMemcpyDeviceToHost, st);
-    tfree();
-    if (hst & ST_SCHEDULE) {   // a camera with > 65535 units in one CTA group: two-pass operator
-      h->fz = FusedTopo{};
-      cudaMemsetAsync(h->ba.status, 0, sizeof(int), st);
-      ok = 0;
-    }
-    CU(cudaGetLastError());
+    if ((rc = build_fused_schedule(h, 8, h->ba.status, st, &ok))) return rc;
     if (ok) return SSFM_OK;
   }
   int occ = 0;
@@ -529,11 +584,7 @@ extern "C" int ssfm_create_gp(const ssfm_gp_desc* desc, void* stream, ssfm_handl
   if ((rc = common_alloc(h, 4 * C, C))) return fail(rc);
   g.scal = h->misc->scal;
   g.status = &h->misc->status;
-  int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gp_k_pcg, PCG_THREADS, 0) || occ < 1)
-    return fail(set_err(SSFM_CUDA_ERROR, "occupancy query for the PCG kernel failed"));
-  h->pcg_sms = pcg_sms_of(h);
-  h->pcg_grid = occ * h->pcg_sms;
+  if ((rc = setup_gp_pcg_op(h, st))) return fail(rc);
   h->lin_blocks = std::max(1, std::min(nblk(T.nb, 8), h->num_sms * 16));
   h->cost_blocks = nblk(N, 256);
   h->cam_blocks = nblk(C, 256);
@@ -912,12 +963,12 @@ static int launch_pcg(ssfm_handle* h, double lam, const ssfm_lm_config* cfg, cud
     CU(cudaLaunchCooperativeKernel(h->pcg_fn, dim3(h->pcg_grid), dim3(h->pcg_threads), a, h->pcg_smem, st));
   } else {
     GPDev& g = h->gp;
-    void* a[12];
+    void* a[13];
     CGCtl* ctl = &h->misc->ctl;
-    a[0] = &g; a[1] = &h->cm; a[2] = &lam; a[3] = &max_it; a[4] = &tol;
-    a[5] = &h->x; a[6] = &h->r; a[7] = &h->z; a[8] = &h->p; a[9] = &h->q;
-    a[10] = &h->part; a[11] = &ctl;
-    CU(cudaLaunchCooperativeKernel((void*)gp_k_pcg, dim3(h->pcg_grid), dim3(PCG_THREADS), a, 0, st));
+    a[0] = &g; a[1] = &h->fz; a[2] = &h->cm; a[3] = &lam; a[4] = &max_it; a[5] = &tol;
+    a[6] = &h->x; a[7] = &h->r; a[8] = &h->z; a[9] = &h->p; a[10] = &h->q;
+    a[11] = &h->part; a[12] = &ctl;
+    CU(cudaLaunchCooperativeKernel(h->pcg_fn, dim3(h->pcg_grid), dim3(h->pcg_threads), a, h->pcg_smem, st));
   }
   count_launch(h);
   return SSFM_OK;
@@ -1518,7 +1569,7 @@ extern "C" int ssfm_operator_info(const ssfm_handle* h, int32_t* slot_groups, in
   if (!h) return set_err(SSFM_INVALID_ARGUMENT, "null argument");
   if (slot_groups) *slot_groups = h->fz.G;
   if (grid) *grid = h->pcg_grid;
-  if (threads) *threads = h->kind == 0 ? h->pcg_threads : PCG_THREADS;
+  if (threads) *threads = h->pcg_threads;
   if (smem_bytes) *smem_bytes = (int64_t)h->pcg_smem;
   return SSFM_OK;
 }

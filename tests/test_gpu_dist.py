@@ -150,7 +150,8 @@ def test_two_processes_ipc(gpu, tmp_path):
     assert r0["costs"] == pytest.approx(np.array([i.cost_after for i in rep.iterations]), rel=1e-7)
 
 
-def test_local_gp_shards_match_single_gpu(gpu):
+@pytest.mark.parametrize("fused", ["0", "1"])
+def test_local_gp_shards_match_single_gpu(gpu, fused):
     """GP (gp.py) sharded by point: scales follow their observations, centres
     are replicated, the mean-scale gauge is taken over every rank."""
     _, obs = synth.generate_arrays(synth.SynthConfig(num_cameras=30, num_points=2000, visibility_fraction=5 / 30,
@@ -160,11 +161,13 @@ def test_local_gp_shards_match_single_gpu(gpu):
     th1, rep1 = b2.lm_solve(base, base.initial_theta(), cfg)
     # both shards' persistent PCG grids must be co-resident on the one device
     os.environ["SSFM_PCG_SMS"] = "40"
+    os.environ["SSFM_FUSED"] = fused
     try:
         probs = [bd.ShardedGPProblem(base, rank=r, world=2, comm="local") for r in range(2)]
         bd.connect_local(probs)
     finally:
         os.environ.pop("SSFM_PCG_SMS")
+        os.environ.pop("SSFM_FUSED")
     out = [None, None]
 
     def work(r):

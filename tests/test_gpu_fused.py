@@ -147,3 +147,52 @@ def test_graph_pcg_matches_persistent_kernel(gpu, fused):
     # iteration cap and the CGStall path through the graph
     with pytest.raises(b2.errors.CGStall):
         solve_normal_native(gpu, gra, 1e-4, b2.LMConfig(cg_max_iters=3))
+
+
+def gp_wide():
+    """GP rays of the wide scene: multi-round batches (points seen by 40-60
+    cameras) next to 2-view points, gauge fixed (camera 0 pinned)"""
+    st = wide_scene()
+    return lambda: b2.fix_gauge(b2.make_rays(st, depth_mode=False, loss=b2.RobustLoss("huber", 0.1), seed=0))
+
+
+def test_gp_fused_matches_two_pass_damped_solve(gpu):
+    make = gp_wide()
+    ref = with_operator("0", make)
+    fz = with_operator("1", make)
+    assert op_info(ref)[0] == 0 and op_info(fz)[0] == 1
+    cfg = b2.LMConfig(cg_tol=1e-12, cg_max_iters=5000)
+    th = ref.initial_theta()
+    ref.gradient(th)
+    fz.gradient(th)
+    for lam in (1e-4, 1e-1):
+        d0, it0 = solve_normal_native(gpu, ref, lam, cfg)
+        d1, it1 = solve_normal_native(gpu, fz, lam, cfg)
+        assert rel(d1, d0) < 1e-9, (lam, rel(d1, d0))
+        assert abs(it1 - it0) <= max(2, 0.03 * it0)
+        d2, it2 = solve_normal_native(gpu, fz, lam, cfg)
+        assert np.array_equal(d1, d2) and it1 == it2
+
+
+def test_gp_fused_default_on_reference_golden(gpu):
+    from .test_gpu_gp import gp_from_golden
+    z = golden("gp_small.npz")
+    assert op_info(gp_from_golden(z))[0] == 0      # small problem: two-pass by default
+    p = with_operator("1", lambda: gp_from_golden(z))
+    assert op_info(p)[0] == 1
+    p.gradient(z["theta0"])
+    d, it = solve_normal_native(gpu, p, 1e-2, b2.LMConfig())
+    assert rel(d, z["delta_lam1e2"]) < 1e-7
+    assert abs(it - int(z["cg_lam1e2"])) <= 2
+
+
+def test_gp_fused_lm_trajectory_matches_two_pass(gpu):
+    make = gp_wide()
+    ref = with_operator("0", make)
+    fz = with_operator("1", make)
+    th0 = ref.initial_theta()
+    a, ra = b2.lm_solve(ref, th0, b2.LMConfig(max_iterations=15))
+    b, rb = b2.lm_solve(fz, th0, b2.LMConfig(max_iterations=15))
+    assert [i.step_accepted for i in ra.iterations] == [i.step_accepted for i in rb.iterations]
+    assert abs(ra.iterations[-1].cost_after - rb.iterations[-1].cost_after) <= 1e-10 * ra.iterations[-1].cost_after
+    assert np.abs(a - b).max() < 1e-8
