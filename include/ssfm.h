@@ -266,6 +266,23 @@ int ssfm_bench_operator(ssfm_handle* h, int32_t which, int32_t reps, double* ms_
 int ssfm_operator_info(const ssfm_handle* h, int32_t* slot_groups, int32_t* grid,
                        int32_t* threads, int64_t* smem_bytes);
 
+/* ---- accuracy metrics on device-resident scenes ----------------------------
+ * ssfm_rotation_auc   replaces synth_metrics.rotation_auc (synth_metrics.py:
+ *   281-309): q_est/q_true [C][4] device (w,x,y,z, unnormalised), taus/auc host
+ *   [ntau] (1..16), auc on the reference's 0-100 scale.
+ * ssfm_center_moments  the Umeyama moments of synth_metrics.align (:225-238):
+ *   x (estimate), y (truth) [n][3] device; out host [17] = mx(3), my(3),
+ *   cov = yc^T xc / n (9, row-major), var_x, sum |x - y|^2 (center_rmse, :260).
+ *   The 3x3 SVD and sign fix are host logic, as in the reference.
+ * ssfm_apply_sim3  the scene transform of align (:244-256): rot [9] row-major,
+ *   trans [3], rq_conj [4] host; quats [C][4], centers [C][3], points [P][3]
+ *   device, transformed in place. */
+int ssfm_rotation_auc(const double* q_est, const double* q_true, int32_t C, const double* taus, int32_t ntau,
+                      double* auc, void* stream);
+int ssfm_center_moments(const double* x, const double* y, int32_t n, double* out, void* stream);
+int ssfm_apply_sim3(const double* rot, const double* trans, double scale, const double* rq_conj, double* quats,
+                    double* centers, int32_t C, double* points, int64_t P, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

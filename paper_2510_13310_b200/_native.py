@@ -24,6 +24,7 @@ EXPORTS = (
     "ssfm_operator_info", "ssfm_comm_init", "ssfm_comm_connect", "ssfm_check_jacobian",
     "ssfm_bench_operator", "ssfm_reproj_stats", "ssfm_block_jtj", "ssfm_block_jtr",
     "ssfm_block_scale_diag", "ssfm_dense_scatter", "ssfm_dense_solve",
+    "ssfm_rotation_auc", "ssfm_center_moments", "ssfm_apply_sim3",
 )
 
 TERMINATIONS = {0: "max_iter", 1: "converged_cost", 2: "converged_grad", 3: "solver_failure"}
@@ -100,6 +101,9 @@ def load(required: bool = True):
     lib.ssfm_export_pattern.argtypes = [P, P, P, P, I64, ct.POINTER(I64), P, I64, ct.POINTER(I64), P]
     lib.ssfm_profile_get.argtypes = [P, I32, ct.POINTER(D), ct.POINTER(I64), ct.POINTER(D)]
     lib.ssfm_profile_enable.argtypes = [P, I32]
+    lib.ssfm_rotation_auc.argtypes = [P, P, I32, P, I32, P, P]
+    lib.ssfm_center_moments.argtypes = [P, P, I32, P, P]
+    lib.ssfm_apply_sim3.argtypes = [P, P, D, P, P, P, I32, P, I64, P]
     for fn in EXPORTS:
         if fn not in ("ssfm_last_error", "ssfm_version", "ssfm_num_params", "ssfm_num_residuals",
                       "ssfm_device_bytes"):

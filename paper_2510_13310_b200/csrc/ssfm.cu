@@ -22,6 +22,7 @@
 #include "pattern.cuh"
 #include "block_algebra.cuh"
 #include "dense.cuh"
+#include "metrics.cuh"
 
 static thread_local std::string g_last_error;
 
@@ -1585,5 +1586,69 @@ extern "C" int ssfm_export_pattern(ssfm_handle* h, int32_t* obs_pt_order, int32_
   int rc = export_keys(h, off_keys, off_cap, n_off, slots, slot_cap, n_slots, st);
   if (rc) return rc;
   CU(cudaStreamSynchronize(st));
+  return SSFM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// accuracy metrics (synth_metrics.py:210-309), device-resident scenes
+// ---------------------------------------------------------------------------
+extern "C" int ssfm_rotation_auc(const double* q_est, const double* q_true, int32_t C, const double* taus,
+                                 int32_t ntau, double* auc, void* stream) {
+  if (!q_est || !q_true || !taus || !auc) return set_err(SSFM_INVALID_ARGUMENT, "null argument");
+  if (C < 2) return set_err(SSFM_INVALID_ARGUMENT, "need >= 2 cameras");
+  if (ntau < 1 || ntau > MET_MAX_TAU) return set_err(SSFM_INVALID_ARGUMENT, "1..16 thresholds");
+  AucArgs a{};
+  a.ntau = ntau;
+  for (int k = 0; k < ntau; ++k) {
+    if (!(taus[k] > 0.0)) return set_err(SSFM_INVALID_ARGUMENT, "thresholds must be positive");
+    a.inv_tau[k] = 1.0 / taus[k];
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  double* buf = nullptr;
+  const long long rows = C - 1;
+  CU(cudaMalloc(&buf, sizeof(double) * (8ll * C + MET_MAX_TAU * rows + MET_MAX_TAU)));
+  double *ne = buf, *nt = buf + 4ll * C, *part = buf + 8ll * C, *res = part + MET_MAX_TAU * rows;
+  k_met_qnorm<<<nblk(2ll * C, 256), 256, 0, st>>>(q_est, q_true, C, ne, nt);
+  k_met_auc_rows<<<(int)rows, MET_THREADS, 0, st>>>(ne, nt, C, a, part);
+  k_met_auc_final<<<1, 32, 0, st>>>(part, (int)rows, ntau, res);
+  double hv[MET_MAX_TAU];
+  cudaMemcpyAsync(hv, res, sizeof(double) * ntau, cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  cudaFree(buf);
+  CU(cudaGetLastError());
+  const double npairs = 0.5 * (double)C * (double)(C - 1);
+  for (int k = 0; k < ntau; ++k) auc[k] = hv[k] / npairs * 100.0;
+  return SSFM_OK;
+}
+
+extern "C" int ssfm_center_moments(const double* x, const double* y, int32_t n, double* out, void* stream) {
+  if (!x || !y || !out) return set_err(SSFM_INVALID_ARGUMENT, "null argument");
+  if (n < 1) return set_err(SSFM_INVALID_ARGUMENT, "need >= 1 camera");
+  cudaStream_t st = (cudaStream_t)stream;
+  double* d = nullptr;
+  CU(cudaMalloc(&d, sizeof(double) * 17));
+  k_met_moments<<<1, 1024, 0, st>>>(x, y, n, d);
+  cudaMemcpyAsync(out, d, sizeof(double) * 17, cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  cudaFree(d);
+  CU(cudaGetLastError());
+  return SSFM_OK;
+}
+
+extern "C" int ssfm_apply_sim3(const double* rot, const double* trans, double scale, const double* rq_conj,
+                               double* quats, double* centers, int32_t C, double* points, int64_t P,
+                               void* stream) {
+  if (!rot || !trans || !rq_conj) return set_err(SSFM_INVALID_ARGUMENT, "null argument");
+  if ((C > 0 && (!quats || !centers)) || (P > 0 && !points) || C < 0 || P < 0)
+    return set_err(SSFM_INVALID_ARGUMENT, "bad scene arrays");
+  Sim3Args a{};
+  for (int k = 0; k < 9; ++k) a.R[k] = rot[k];
+  for (int k = 0; k < 3; ++k) a.t[k] = trans[k];
+  for (int k = 0; k < 4; ++k) a.rqc[k] = rq_conj[k];
+  a.s = scale;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (C > 0) k_met_apply_cameras<<<nblk(C, 256), 256, 0, st>>>(a, quats, centers, C);
+  if (P > 0) k_met_apply_points<<<nblk(P, 256), 256, 0, st>>>(a, points, P);
+  CU(cudaGetLastError());
   return SSFM_OK;
 }

@@ -29,6 +29,10 @@ class PipelineReport:
     ba: SolveReport
     rmse_after_gp: float
     rmse_after_ba: float
+    # with `truth`: Sim(3)-aligned camera-centre RMSE and pairwise rotation AUC
+    # (synth_metrics.align / center_rmse / rotation_auc, on the device)
+    center_rmse: float | None = None
+    rotation_auc: dict | None = None
 
 
 def reproj_stats(problem: BAProblem, theta) -> tuple[float, int]:
@@ -51,9 +55,10 @@ def reproj_rmse_device(problem: BAProblem, theta) -> float:
 
 def run_global_sfm(scene, gp_loss: RobustLoss | None = None, ba_loss: RobustLoss | None = None,
                    gp_config: LMConfig | None = None, ba_config: LMConfig | None = None, seed: int = 0,
-                   optimize_focal: bool = True):
+                   optimize_focal: bool = True, truth=None, auc_thresholds=(1.0, 3.0, 5.0, 10.0)):
     """GP (Huber 0.1 by default, seeded init, gauge fixed) then BA (Huber 1.0)
-    on the GP output. Returns (scene, PipelineReport)."""
+    on the GP output. Returns (scene, PipelineReport); with `truth` the report
+    carries the aligned centre RMSE and the rotation AUC (metrics.py)."""
     arr = as_arrays(scene)
     gp_loss = gp_loss or RobustLoss("huber", 0.1)
     ba_loss = ba_loss or RobustLoss("huber", 1.0)
@@ -71,4 +76,10 @@ def run_global_sfm(scene, gp_loss: RobustLoss | None = None, ba_loss: RobustLoss
     rm1 = reproj_rmse_device(ba, th_ba)
     out = ba.decode(th_ba)
     ba.release()
-    return (out if isinstance(scene, SceneArrays) else out), PipelineReport(rep_gp, rep_ba, rm0, rm1)
+    rep = PipelineReport(rep_gp, rep_ba, rm0, rm1)
+    if truth is not None:
+        from . import metrics
+        _, aligned = metrics.align(out, truth, "sim3")
+        rep.center_rmse = metrics.center_rmse(aligned, truth)
+        rep.rotation_auc = metrics.rotation_auc(aligned, truth, auc_thresholds)
+    return out, rep

@@ -174,7 +174,49 @@ def block_algebra_fixture():
     print("block_algebra.npz", {k: v.shape for k, v in out.items() if k.endswith("jtj")})
 
 
+def metrics_fixture():
+    """Reference synth_metrics.align (sim3, se3), center_rmse and rotation_auc
+    on a perturbed scene moved by a known similarity: pins the device metrics
+    (paper_2510_13310_b200/metrics.py)."""
+    from sparsesfm.scene import Camera, Point3D, Scene, quat_to_matrix
+    truth, obs = rsm.generate(rsm.SynthConfig(num_cameras=60, num_points=400, visibility_fraction=0.2,
+                                              pixel_noise_sigma=1.0, seed=11))
+    est = rsm.perturb(obs, rot_deg=2.0, center_frac=0.02, focal_frac=0.0, point_frac=0.01, seed=4)
+    qs = quat_from_axis_angle(np.array([0.3, -0.5, 0.8]), 0.7)
+    Rs, s, t = quat_to_matrix(qs), 1.7, np.array([0.5, -2.0, 3.0])
+    qs_c = np.array([qs[0], -qs[1], -qs[2], -qs[3]])
+    moved = Scene([Camera(quat_multiply(c.rotation, qs_c), s * Rs @ c.center + t, c.focal,
+                          c.principal_point.copy(), c.model_tag, c.bal_distortion.copy()) for c in est.cameras],
+                  [Point3D(s * Rs @ p.position + t) for p in est.points], list(est.observations))
+    taus = np.array([1.0, 2.0, 5.0, 10.0, 30.0])
+    out = {"taus": taus}
+    a = scene_to_arrays(moved)
+    tr = scene_to_arrays(truth)
+    out.update(est_quats=a.quats, est_centers=a.centers, est_points=a.points, true_quats=tr.quats,
+               true_centers=tr.centers)
+    for kind in ("sim3", "se3"):
+        al, aligned = rsm.align(moved, truth, kind)
+        b = scene_to_arrays(aligned)
+        out[f"{kind}_rotation"] = al.rotation
+        out[f"{kind}_translation"] = al.translation
+        out[f"{kind}_scale"] = al.scale
+        out[f"{kind}_quats"] = b.quats
+        out[f"{kind}_centers"] = b.centers
+        out[f"{kind}_points"] = b.points
+        out[f"{kind}_center_rmse"] = rsm.center_rmse(aligned, truth)
+        auc = rsm.rotation_auc(aligned, truth, taus)
+        out[f"{kind}_auc"] = np.array([auc[float(x)] for x in taus])
+    auc = rsm.rotation_auc(moved, truth, taus)
+    out["moved_auc"] = np.array([auc[float(x)] for x in taus])
+    out["moved_center_rmse"] = rsm.center_rmse(moved, truth)
+    np.savez_compressed(os.path.join(HERE, "metrics.npz"), **out)
+    print("metrics.npz", out["sim3_scale"], out["sim3_auc"], out["moved_auc"])
+
+
 def main():
+    if "metrics" in sys.argv[1:]:
+        metrics_fixture()
+        return
     if "shared" in sys.argv[1:]:
         shared_focal_fixture()
         return
@@ -182,6 +224,7 @@ def main():
         block_algebra_fixture()
         return
     shared_focal_fixture()
+    metrics_fixture()
     # --- BA fixtures
     truth, obs = rsm.generate(rsm.SynthConfig(num_cameras=8, num_points=120, visibility_fraction=0.5,
                                               pixel_noise_sigma=1.0, seed=3))

@@ -390,9 +390,9 @@ def test_reproj_rmse_device_matches_host(gpu):        # synth_metrics.py:312-325
 
 
 def test_global_sfm_pipeline(gpu):                     # SURVEY.md 8(d) C4 recipe, small
-    _, obs = synth.generate_arrays(synth.SynthConfig(num_cameras=30, num_points=3000, visibility_fraction=8 / 30,
-                                                     pixel_noise_sigma=1.0, seed=0))
-    out, rep = b2.run_global_sfm(obs)
+    truth, obs = synth.generate_arrays(synth.SynthConfig(num_cameras=30, num_points=3000,
+                                                         visibility_fraction=8 / 30, pixel_noise_sigma=1.0, seed=0))
+    out, rep = b2.run_global_sfm(obs, truth=truth)
     # the same two stages run by hand
     mid, rg = b2.run_gp(obs, loss=b2.RobustLoss("huber", 0.1), config=b2.LMConfig(max_iterations=20))
     ref, rb = b2.run_ba(mid, b2.RobustLoss("huber", 1.0), b2.LMConfig(max_iterations=10))
@@ -403,3 +403,9 @@ def test_global_sfm_pipeline(gpu):                     # SURVEY.md 8(d) C4 recip
     # BA minimises the Huber cost, not the RMSE: the RMSE stays at the noise level
     assert rep.ba.iterations[-1].cost_after < rep.ba.iterations[0].cost_before
     assert rep.rmse_after_ba < 1.5
+    # accuracy against the truth, device metrics vs the host restatement
+    _, al = synth.align(out, truth, "sim3")
+    assert rep.center_rmse == pytest.approx(synth.center_rmse(al, truth), rel=1e-9)
+    h = synth.rotation_auc(al, truth, [1.0, 3.0, 5.0, 10.0])
+    assert max(abs(rep.rotation_auc[t] - h[t]) for t in h) < 1e-6
+    assert rep.rotation_auc[5.0] > 50.0

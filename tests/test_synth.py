@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from paper_2510_13310_b200 import synth
-from .conftest import summary
+from .conftest import golden, summary
 
 
 def digest(a):
@@ -73,3 +73,15 @@ def test_metrics_on_exact_scene():
     assert synth.reproj_rmse(truth) < 1e-9
     auc = synth.rotation_auc(truth, truth, [1.0, 5.0])
     assert auc[1.0] == pytest.approx(100.0)
+
+
+def test_host_metrics_match_reference_golden():
+    """the host restatement of synth_metrics (test harness) vs the reference's outputs"""
+    from .test_gpu_metrics import moved_arrays, truth_arrays
+    z = golden("metrics.npz")
+    for kind in ("sim3", "se3"):
+        al, out = synth.align(moved_arrays(z), truth_arrays(z), kind)
+        assert np.abs(al.rotation - z[f"{kind}_rotation"]).max() < 1e-12
+        assert np.abs(out.points - z[f"{kind}_points"]).max() < 1e-10
+        auc = synth.rotation_auc(out, truth_arrays(z), z["taus"])
+        assert np.abs(np.array(list(auc.values())) - z[f"{kind}_auc"]).max() < 1e-9
