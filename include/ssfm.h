@@ -54,7 +54,10 @@ typedef enum {
   SSFM_DIMENSION_MISMATCH = 8,  /* errors.DimensionMismatch  (errors.py:16)  */
   SSFM_INVALID_ARGUMENT = 9,    /* ValueError / IndexError                    */
   SSFM_CUDA_ERROR = 10,
-  SSFM_COMM_ERROR = 11         /* peer exchange of a sharded handle failed / timed out */
+  SSFM_COMM_ERROR = 11,        /* peer exchange of a sharded handle failed / timed out */
+  SSFM_PARSE_ERROR = 12,       /* errors.ParseError "line N: reason" (errors.py:51) */
+  SSFM_COUNT_MISMATCH = 13,    /* errors.CountMismatch      (errors.py:59)  */
+  SSFM_DUPLICATE_OBSERVATION = 14 /* errors.DuplicateObservation (errors.py:63) */
 } ssfm_status;
 
 /* Termination reasons of SolveReport.termination (lm.py:61-83). */
@@ -282,6 +285,19 @@ int ssfm_rotation_auc(const double* q_est, const double* q_true, int32_t C, cons
 int ssfm_center_moments(const double* x, const double* y, int32_t n, double* out, void* stream);
 int ssfm_apply_sim3(const double* rot, const double* trans, double scale, const double* rq_conj, double* quats,
                     double* centers, int32_t C, double* points, int64_t P, void* stream);
+
+/* ---- BAL problem files (io.read_bal, io.py:83-131) ------------------------
+ * Array-native host reader: ssfm_bal_read parses `path` (the reference's token,
+ * error-message and line-number rules) and returns counts[3] = C, P, N;
+ * ssfm_bal_take copies out cam_idx / pt_idx [N] int64, pixels [N][2],
+ * cam_params [C][9] (angle-axis, translation, focal, k1, k2), points [P][3]
+ * (host arrays); ssfm_bal_free releases the reader. Errors: SSFM_PARSE_ERROR,
+ * SSFM_COUNT_MISMATCH (trailing tokens), SSFM_DUPLICATE_OBSERVATION. */
+typedef struct ssfm_bal ssfm_bal;
+int ssfm_bal_read(const char* path, ssfm_bal** out, int64_t* counts);
+int ssfm_bal_take(ssfm_bal* reader, int64_t* cam_idx, int64_t* pt_idx, double* pixels, double* cam_params,
+                  double* points);
+void ssfm_bal_free(ssfm_bal* reader);
 
 #ifdef __cplusplus
 }

@@ -25,6 +25,7 @@ EXPORTS = (
     "ssfm_bench_operator", "ssfm_reproj_stats", "ssfm_block_jtj", "ssfm_block_jtr",
     "ssfm_block_scale_diag", "ssfm_dense_scatter", "ssfm_dense_solve",
     "ssfm_rotation_auc", "ssfm_center_moments", "ssfm_apply_sim3",
+    "ssfm_bal_read", "ssfm_bal_take", "ssfm_bal_free",
 )
 
 TERMINATIONS = {0: "max_iter", 1: "converged_cost", 2: "converged_grad", 3: "solver_failure"}
@@ -104,9 +105,13 @@ def load(required: bool = True):
     lib.ssfm_rotation_auc.argtypes = [P, P, I32, P, I32, P, P]
     lib.ssfm_center_moments.argtypes = [P, P, I32, P, P]
     lib.ssfm_apply_sim3.argtypes = [P, P, D, P, P, P, I32, P, I64, P]
+    lib.ssfm_bal_read.argtypes = [ct.c_char_p, ct.POINTER(P), P]
+    lib.ssfm_bal_take.argtypes = [P, P, P, P, P, P]
+    lib.ssfm_bal_free.argtypes = [P]
+    lib.ssfm_bal_free.restype = None
     for fn in EXPORTS:
         if fn not in ("ssfm_last_error", "ssfm_version", "ssfm_num_params", "ssfm_num_residuals",
-                      "ssfm_device_bytes"):
+                      "ssfm_device_bytes", "ssfm_bal_free"):
             getattr(lib, fn).restype = ct.c_int
     _lib = lib
     return lib

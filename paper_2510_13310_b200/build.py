@@ -3,7 +3,7 @@
     python -m paper_2510_13310_b200.build
 
 nvcc compiles csrc/ssfm.cu (kernels + C-ABI + host drivers, one translation
-unit) and csrc/synth_host.cpp into _lib/libssfm_b200.so with the CUDA runtime
+unit), csrc/synth_host.cpp and csrc/bal_host.cpp into _lib/libssfm_b200.so with the CUDA runtime
 linked statically, so the library carries its own cudart and interoperates
 with PyTorch through the driver's primary context and raw stream handles.
 """
@@ -27,7 +27,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-shared",
 
 
 def sources():
-    return [os.path.join(CSRC, "ssfm.cu"), os.path.join(CSRC, "synth_host.cpp")]
+    return [os.path.join(CSRC, "ssfm.cu"), os.path.join(CSRC, "synth_host.cpp"), os.path.join(CSRC, "bal_host.cpp")]
 
 
 def deps():

@@ -31,6 +31,9 @@ static int set_err(int code, const std::string& msg) {
   return code;
 }
 
+// error hand-off for the host-only translation units (bal_host.cpp)
+extern "C" int ssfm_internal_set_error(int code, const char* msg) { return set_err(code, msg ? msg : ""); }
+
 #define CU(call)                                                                   \
   do {                                                                             \
     cudaError_t _e = (call);                                                       \

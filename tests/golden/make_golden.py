@@ -213,7 +213,83 @@ def metrics_fixture():
     print("metrics.npz", out["sim3_scale"], out["sim3_auc"], out["moved_auc"])
 
 
+def bal_cases():
+    """BAL texts for the reader (valid files and every error path of io.read_bal)"""
+    truth, _ = rsm.generate(rsm.SynthConfig(num_cameras=20, num_points=300, visibility_fraction=0.3,
+                                            pixel_noise_sigma=1.0, seed=9))
+    rng = np.random.default_rng(3)
+    a = scene_to_arrays(truth)
+    lines = [f"{len(a.quats)} {len(a.points)} {len(a.cam_idx)}"]
+    lines += [f"{c} {p} {float(u)!r} {float(v)!r}" for c, p, (u, v) in zip(a.cam_idx, a.pt_idx, a.pixels)]
+    for i in range(len(a.quats)):
+        lines += [repr(float(x)) for x in np.concatenate([rng.normal(size=3) * 0.3, rng.normal(size=3),
+                                                          [500 + 50 * rng.random()], rng.normal(size=2) * 1e-3])]
+    lines += [" ".join(repr(float(x)) for x in pt) for pt in a.points]
+    synth_text = "\n".join(lines) + "\n"
+    mini = ("# a BAL file with comments\r\n3 4 7  # header\r\n"
+            "0 0 1.5 -0.5\r\n0 1\t-2.0 +0.25\r\n1 0 0.75 0.125\n001 3 -0.25 2.0\r2 2 1_000.5 3\f"
+            "2 3 -1e3 .5\v0 2 5. -0E0\n"
+            "0.01 -0.02 0.03 0.1 -0.2 1.5 420.0 -1e-7 2e-13\n"
+            "0 0 0 0.3 -0.4 2 415.5 0 0\n"
+            "1e-13 0 -0 0 0 -1 300 0.5 -0.5 # tiny angle\n"
+            "-0.1 0.2 -3.0\n0.5 -0.25 -2.5\n1 2 -4\ninf -inf 6\n")
+    head = "2 2 3\n0 0 1 2\n1 1 3 4\n0 1 5 6\n"
+    cams = " ".join(["0.1"] * 18) + "\n"
+    pts = "1 2 3\n4 5 6\n"
+    ok = head + cams + pts
+    return {
+        "synth": synth_text,
+        "mini": mini,
+        "header_only": "0 0 0\n",
+        "empty": "",
+        "comment_only": "# nothing here\n\n",
+        "truncated_obs": head[:-6] + "\n",
+        "truncated_cams": head + " ".join(["0.1"] * 11) + "\n",
+        "truncated_pts": head + cams + "1 2 3\n4\n",
+        "bad_camera": ok.replace("1 1 3 4", "2 1 3 4"),
+        "bad_point": ok.replace("0 1 5 6", "0 -1 5 6"),
+        "negative_count": "2 -2 3\n",
+        "float_index": ok.replace("1 1 3 4", "1.0 1 3 4"),
+        "bad_number": ok.replace("1 2 3\n4 5 6", "1 2 3\n4 5.5.5 6"),
+        "hex_number": ok.replace("0 0 1 2", "0 0 0x1p3 2"),
+        "bad_underscore": ok.replace("1 2 3\n4", "1 2_ 3\n4"),
+        "nan_payload": ok.replace("1 2 3\n4", "1 nan(1) 3\n4"),
+        "trailing": ok + "42.0\n7\n",
+        "duplicate": "2 2 3\n0 0 1 2\n1 1 3 4\n1 1 5 6\n" + cams + pts,
+        "bad_header": "two 2 3\n",
+    }
+
+
+def bal_fixture():
+    """Reference io.read_bal on every case of bal_cases(): arrays or the error"""
+    import tempfile
+    from sparsesfm.io import read_bal
+    cases = bal_cases()
+    arrays, expect = {}, {}
+    with tempfile.TemporaryDirectory() as d:
+        for name, text in cases.items():
+            path = os.path.join(d, name + ".bal")
+            with open(path, "w", newline="") as fh:
+                fh.write(text)
+            try:
+                sc = read_bal(path)
+            except Exception as e:   # noqa: BLE001 - the error is the golden output
+                expect[name] = {"error": type(e).__name__, "message": str(e), "line": getattr(e, "line", None)}
+                continue
+            a = scene_to_arrays(sc)
+            expect[name] = {"error": None, "counts": [len(a.quats), len(a.points), len(a.cam_idx)]}
+            for k in ("quats", "centers", "focals", "dists", "points", "cam_idx", "pt_idx", "pixels"):
+                arrays[f"{name}__{k}"] = getattr(a, k)
+    with open(os.path.join(HERE, "bal_cases.json"), "w") as fh:
+        json.dump({"texts": cases, "expect": expect}, fh, indent=1)
+    np.savez_compressed(os.path.join(HERE, "bal.npz"), **arrays)
+    print("bal cases", {k: v["error"] for k, v in expect.items()})
+
+
 def main():
+    if "bal" in sys.argv[1:]:
+        bal_fixture()
+        return
     if "metrics" in sys.argv[1:]:
         metrics_fixture()
         return
@@ -225,6 +301,7 @@ def main():
         return
     shared_focal_fixture()
     metrics_fixture()
+    bal_fixture()
     # --- BA fixtures
     truth, obs = rsm.generate(rsm.SynthConfig(num_cameras=8, num_points=120, visibility_fraction=0.5,
                                               pixel_noise_sigma=1.0, seed=3))
