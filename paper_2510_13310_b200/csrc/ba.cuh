@@ -27,7 +27,7 @@ struct __align__(16) BACam {
   double f;         // focal (theta or fixed)
   double pp[2];     // principal point
   double k[2];      // bal radial k1, k2
-  double pad;
+  double pad;       // 1/|q|
 };
 
 struct BAParams {
@@ -63,7 +63,7 @@ __device__ __forceinline__ void ba_make_cam(const double* q, const double* t, do
   c.f = f;
   c.pp[0] = pp[0]; c.pp[1] = pp[1];
   c.k[0] = k[0]; c.k[1] = k[1];
-  c.pad = 0.0;
+  c.pad = 1.0 / n;   // 1/|q| for the factored operator (ba_pi_mul)
 }
 
 // Projection of one observation (ba.py:111-131). Returns camera point p,
@@ -237,4 +237,75 @@ __device__ __forceinline__ void ba_jpt_mul(const double* J, const double* t, dou
   o[0] = J[8] * t[0] + J[11] * t[1];
   o[1] = J[9] * t[0] + J[12] * t[1];
   o[2] = J[10] * t[0] + J[13] * t[1];
+}
+
+// Factored operator record of one observation (6 doubles), for the two-pass
+// Schur operator: with E = [[1, 0, -e0], [0, 1, -e1]] (e = p_xy / z_s) and a
+// symmetric 2x2 S,   sw du_dp = S E,   sw du_df = phi e.   Then
+//   Jp = S E R,   Jc = [S E D(v) Pi | -S E R | phi e]
+// with Pi = (I - qh qh^T) / |q| and D(v) the 3x4 of scene.py:153-184; R, qh,
+// |q| are per camera and v = X - t per observation, so an observation costs
+// 6 doubles (+ v in the camera-major copy) instead of the 16 of BA_JREC.
+// Rows: 0 s00, 1 e0, 2 e1, 3 phi, 4 s01, 5 s11 (pinhole: s01 = 0, s11 = s00,
+// rows 4-5 unused).
+#define BA_FREC 6
+__device__ __forceinline__ void ba_factor(const BAParams& bp, const BACam& c, const BAProj& pr, double sw,
+                                          double* F) {
+  const double inv_z = 1.0 / pr.zs;
+  const double e0 = pr.p[0] * inv_z, e1 = pr.p[1] * inv_z;
+  F[1] = e0;
+  F[2] = e1;
+  if (bp.model == 1) {
+    const double k1 = c.k[0], k2 = c.k[1];
+    const double n0 = -e0, n1 = -e1;
+    const double r2 = n0 * n0 + n1 * n1;
+    const double sc = 1.0 + k1 * r2 + k2 * r2 * r2;
+    const double a = c.f * sc, b = 2.0 * c.f * (k1 + 2.0 * k2 * r2);
+    const double g = -sw * inv_z;
+    F[0] = g * (a + b * n0 * n0);
+    F[4] = g * (b * n0 * n1);
+    F[5] = g * (a + b * n1 * n1);
+    F[3] = bp.focal_mode != 0 ? -sw * sc : 0.0;
+  } else {
+    const double a = sw * (c.f * inv_z);
+    F[0] = a;
+    F[4] = 0.0;
+    F[5] = a;
+    F[3] = bp.focal_mode != 0 ? sw : 0.0;
+  }
+}
+
+// (D(v) w)_i for a quaternion-space 4-vector w (D of scene.py:153-184):
+//   2 [ (u x v)_i w0 - qw (v x w')_i + (u.v) w'_i + u_i (v.w') - 2 v_i (u.w') ]
+__device__ __forceinline__ void ba_dq_mul(const double* qh, const double* v, const double* w, double* o) {
+  const double u0 = qh[1], u1 = qh[2], u2 = qh[3], qw = qh[0];
+  const double ud = u0 * v[0] + u1 * v[1] + u2 * v[2];
+  const double vw = v[0] * w[1] + v[1] * w[2] + v[2] * w[3];
+  const double uw = u0 * w[1] + u1 * w[2] + u2 * w[3];
+  const double c0 = u1 * v[2] - u2 * v[1], c1 = u2 * v[0] - u0 * v[2], c2 = u0 * v[1] - u1 * v[0];
+  const double x0 = v[1] * w[3] - v[2] * w[2], x1 = v[2] * w[1] - v[0] * w[3], x2 = v[0] * w[2] - v[1] * w[1];
+  o[0] = 2.0 * (c0 * w[0] - qw * x0 + ud * w[1] + u0 * vw - 2.0 * v[0] * uw);
+  o[1] = 2.0 * (c1 * w[0] - qw * x1 + ud * w[2] + u1 * vw - 2.0 * v[1] * uw);
+  o[2] = 2.0 * (c2 * w[0] - qw * x2 + ud * w[3] + u2 * vw - 2.0 * v[2] * uw);
+}
+
+// D(v)^T g (4-vector):  [2 (u x v).g,  2 (qw (v x g)_j + (u.v) g_j + (u.g) v_j - 2 (v.g) u_j)]
+__device__ __forceinline__ void ba_dqt_mul(const double* qh, const double* v, const double* g, double* o) {
+  const double u0 = qh[1], u1 = qh[2], u2 = qh[3], qw = qh[0];
+  const double ud = u0 * v[0] + u1 * v[1] + u2 * v[2];
+  const double ug = u0 * g[0] + u1 * g[1] + u2 * g[2];
+  const double vg = v[0] * g[0] + v[1] * g[1] + v[2] * g[2];
+  const double c0 = u1 * v[2] - u2 * v[1], c1 = u2 * v[0] - u0 * v[2], c2 = u0 * v[1] - u1 * v[0];
+  const double x0 = v[1] * g[2] - v[2] * g[1], x1 = v[2] * g[0] - v[0] * g[2], x2 = v[0] * g[1] - v[1] * g[0];
+  o[0] = 2.0 * (c0 * g[0] + c1 * g[1] + c2 * g[2]);
+  o[1] = 2.0 * (qw * x0 + ud * g[0] + ug * v[0] - 2.0 * vg * u0);
+  o[2] = 2.0 * (qw * x1 + ud * g[1] + ug * v[1] - 2.0 * vg * u1);
+  o[3] = 2.0 * (qw * x2 + ud * g[2] + ug * v[2] - 2.0 * vg * u2);
+}
+
+// Pi w = (w - qh (qh.w)) / |q|  (Pi symmetric); inv_qn = 1 / |q|
+__device__ __forceinline__ void ba_pi_mul(const double* qh, double inv_qn, const double* w, double* o) {
+  const double d = qh[0] * w[0] + qh[1] * w[1] + qh[2] * w[2] + qh[3] * w[3];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) o[k] = (w[k] - d * qh[k]) * inv_qn;
 }

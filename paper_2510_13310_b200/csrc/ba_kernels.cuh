@@ -26,6 +26,8 @@ struct BADev {
   double* Jpm;            // [16 * Npad]
   double* Jcm;            // [16 * Npad]
   double* rcm;            // [2 * Npad]
+  double* Fcm;            // [9 * Npad] factored records (ba_factor) + v = X - t, camera-major (two-pass only)
+  BACam* camlin;          // [C] camera cache at the linearization (cams is overwritten by trial costs)
   long long Npad;
   double* Cpt;            // [6P]
   double* gpt;            // [3P]
@@ -130,12 +132,17 @@ __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
 // rounding and contraction), so they are bit-identical; ssfm_check_jacobian
 // verifies it on the device (tests/test_gpu_ba.py).
 __device__ __forceinline__ void ba_obs_eval(const BAParams& bp, const BACam* __restrict__ cam, const double* X,
-                                         const double* pix, double* r, double* J, double* cost_term) {
+                                         const double* pix, double* r, double* J, double* cost_term,
+                                         double* F = nullptr) {
   const BACam cc = *cam;
   BAProj pr;
   double sw;
   ba_residual(bp, cc, X, pix, pr, r, sw, *cost_term);
   ba_jacobian(bp, cc, pr, sw, J);
+  if (F) {   // factored record (+ v) for the two-pass operator
+    ba_factor(bp, cc, pr, sw, F);
+    F[6] = pr.v[0]; F[7] = pr.v[1]; F[8] = pr.v[2];
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -270,10 +277,15 @@ __global__ void __launch_bounds__(SSFM_TILE) ba_k_linearize_cm(BADev d, const do
   if (i < o1) {
     const long long Np = d.Npad;
     const int j = d.topo.cm_pt[i];
-    double r[2], J[BA_JREC], ct;
-    ba_obs_eval(d.bp, d.cams + c, theta + d.bp.off_pts + 3ll * j, d.pix_cm + 2ll * i, r, J, &ct);
+    double r[2], J[BA_JREC], ct, F[BA_FREC + 3];
+    ba_obs_eval(d.bp, d.cams + c, theta + d.bp.off_pts + 3ll * j, d.pix_cm + 2ll * i, r, J, &ct,
+                d.Fcm ? F : nullptr);
 #pragma unroll
     for (int k = 0; k < BA_JREC; ++k) d.Jcm[k * Np + i] = J[k];
+    if (d.Fcm) {
+#pragma unroll
+      for (int k = 0; k < BA_FREC + 3; ++k) d.Fcm[k * Np + i] = F[k];
+    }
     d.rcm[i] = r[0];
     d.rcm[Np + i] = r[1];
     double a[8], b[8];

@@ -57,6 +57,95 @@ __device__ __forceinline__ double cta_partials_sum(const double* part, int n, in
   return v;
 }
 
+// Factored camera pass (ba_factor records, ba.cuh). Per observation it
+// streams 7 (pinhole) / 9 (bal) doubles (S, e, phi, v = X - t) + 1 index
+// instead of the 16-double Jacobian record, and applies the tile's camera
+// (R, Pi from camlin, the linearization's camera cache) once per tile: C5
+// camera pass 0.535 -> 0.329 ms. The operator is the stored Jacobian's to
+// rounding. (A factored point pass lost, 0.555 -> 0.832 ms: every observation
+// gathers its camera's R, qh, t through L1, which saturates at 89 %; the
+// point pass keeps the Jacobian record.)
+__device__ __forceinline__ void ba_load_frec(const double* __restrict__ F, long long Np, long long i, int model,
+                                             unsigned long long pol, double* f) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) f[k] = ldg_stream(F + k * Np + i, pol);
+  if (model == 1) {
+    f[4] = ldg_stream(F + 4 * Np + i, pol);
+    f[5] = ldg_stream(F + 5 * Np + i, pol);
+  } else {
+    f[4] = 0.0;
+    f[5] = f[0];
+  }
+}
+
+template <bool RO>
+__device__ __forceinline__ void ba_camera_pass_f(const BADev& d, const double* y, double* tile8) {
+  const unsigned long long pstream = pol_evict_first(), pkeep = pol_evict_last();
+  const long long Np = d.Npad;
+  const int model = d.bp.model;
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  for (int t = gw; t < d.topo.nt; t += warps) {
+    const int o0 = __ldg(d.topo.tile_obs + t), o1 = __ldg(d.topo.tile_obs + t + 1);
+    const int c = __ldg(d.topo.tile_cam + t);
+    const double* cb = reinterpret_cast<const double*>(d.camlin + c);
+    double o[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = 0.0;
+#pragma unroll 1
+    for (int i = o0 + lane; i < o1; i += 32) {
+      // the tile's camera: warp-uniform addresses, L1 broadcasts (not kept
+      // in registers across the loop: 64-register budget)
+      double R[9], qh[4];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) R[k] = __ldg(cb + k);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) qh[k] = __ldg(cb + 9 + k);
+      double f[6], vv[3];
+      ba_load_frec(d.Fcm, Np, i, model, pstream, f);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) vv[k] = ldg_stream(d.Fcm + (6 + k) * Np + i, pstream);
+      const int j = ldg_stream_i(d.topo.cm_pt + i, pstream);
+      double yj[4];
+      if constexpr (RO) ld_v4_ro(y + 4ll * j, yj, pkeep);
+      else ld_v4_hint(y + 4ll * j, yj, pkeep);
+      double ry[3];
+#pragma unroll
+      for (int r = 0; r < 3; ++r) ry[r] = R[3 * r] * yj[0] + R[3 * r + 1] * yj[1] + R[3 * r + 2] * yj[2];
+      const double h0 = ry[0] - f[1] * ry[2], h1 = ry[1] - f[2] * ry[2];
+      const double s0 = f[0] * h0 + f[4] * h1, s1 = f[4] * h0 + f[5] * h1;
+      const double k0 = f[0] * s0 + f[4] * s1, k1 = f[4] * s0 + f[5] * s1;
+      const double g[3] = {k0, k1, -(f[1] * k0 + f[2] * k1)};
+      double dt[4];
+      ba_dqt_mul(qh, vv, g, dt);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o[k] += dt[k];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) o[4 + k] += g[k];
+      o[7] += f[3] * (f[1] * s0 + f[2] * s1);
+    }
+    warp_allreduce<8>(o);
+    // camera frame -> theta slots: quaternion Pi (.), centre -R^T (.)
+    double R[9], qh[4];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) R[k] = __ldg(cb + k);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) qh[k] = __ldg(cb + 9 + k);
+    double out[8];
+    ba_pi_mul(qh, __ldg(cb + 22), o, out);
+#pragma unroll
+    for (int m = 0; m < 3; ++m) out[4 + m] = -(R[m] * o[4] + R[3 + m] * o[5] + R[6 + m] * o[6]);
+    out[7] = o[7];
+    if (lane < 8) {
+      double x = out[0];
+#pragma unroll
+      for (int k = 1; k < 8; ++k) x = lane == k ? out[k] : x;
+      tile8[8ll * t + lane] = x;
+    }
+  }
+}
+
 // P1 for a camera vector v -> y (per point): y_j = Cinv_j sum_o Jp^T (Jc v_c)
 template <bool RO = false>
 __device__ __forceinline__ void ba_point_pass(const BADev& d, const double* v, double* y,
@@ -317,7 +406,7 @@ __device__ __forceinline__ void ba_fused_pass(const BADev& d, const FusedTopo& f
 // The whole PCG as one persistent cooperative kernel. SL = 0: two-pass
 // operator (P1 point pass, P2 camera tiles). SL > 0: fused single pass with
 // 8/SL slot groups (fused.cuh); needs SL*C doubles of dynamic shared memory.
-template <int SL>
+template <int SL, bool FAC = false>
 __global__ void __launch_bounds__(SL ? FZ_THREADS : PCG_THREADS, SL ? 1 : 4)
 ba_k_pcg(BADev d, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg_tol, double* x,
          double* r, double* z, double* p, double* q, double* part, CGCtl* ctl) {
@@ -397,7 +486,8 @@ ba_k_pcg(BADev d, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg
         grid.sync();
         if (tim) { const unsigned long long t1 = gtimer(); ph[0] += t1 - pt0; pt0 = t1; }
         // P2: camera tiles
-        ba_camera_pass(d, d.yv, tile8, smred);
+        if constexpr (FAC) ba_camera_pass_f<false>(d, d.yv, tile8);
+        else ba_camera_pass(d, d.yv, tile8, smred);
       } else {
         ba_fused_pass<SL>(d, fz, p, dyn_acc, smp, smy, smown);
       }
@@ -523,9 +613,11 @@ ba_k_pcg(BADev d, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg
 // kernels (per-pass timing and roofline, ssfm_bench_operator).
 __global__ void __launch_bounds__(PCG_THREADS, 4) k_op_point(BADev d, const double* v, double* y) {
   __shared__ double smp[PCG_THREADS / 32][SSFM_BATCH][3];
-  ba_point_pass(d, v, y, smp);
+  ba_point_pass<true>(d, v, y, smp);
 }
-__global__ void __launch_bounds__(PCG_THREADS, 4) k_op_camera(BADev d, const double* y, double* tile8) {
+template <bool FAC>
+__global__ void __launch_bounds__(PCG_THREADS, FAC ? 3 : 4) k_op_camera(BADev d, const double* y, double* tile8) {
   __shared__ double smred[(PCG_THREADS / 32) * 8];
-  ba_camera_pass(d, y, tile8, smred);
+  if constexpr (FAC) ba_camera_pass_f<true>(d, y, tile8);
+  else ba_camera_pass<true>(d, y, tile8, smred);
 }

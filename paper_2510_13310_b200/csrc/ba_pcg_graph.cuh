@@ -89,10 +89,13 @@ __global__ void __launch_bounds__(PCG_THREADS, 4) k_g_point(BADev d, CGGraphDev 
   ba_point_pass<true>(d, g.p, d.yv, smp);   // p is constant during this kernel
 }
 
-__global__ void __launch_bounds__(PCG_THREADS, 4) k_g_camera(BADev d, CGGraphDev g) {
+// FAC: the factored camera pass (ba_camera_pass_f)
+template <bool FAC>
+__global__ void __launch_bounds__(PCG_THREADS, FAC ? 3 : 4) k_g_camera(BADev d, CGGraphDev g) {
   if (*(volatile int*)(g.ic + 3)) return;
   __shared__ double smred[(PCG_THREADS / 32) * 8];
-  ba_camera_pass<true>(d, d.yv, d.tilebuf, smred);   // y is constant during this kernel
+  if constexpr (FAC) ba_camera_pass_f<true>(d, d.yv, d.tilebuf);   // y is constant during this kernel
+  else ba_camera_pass<true>(d, d.yv, d.tilebuf, smred);
 }
 
 template <int SL>

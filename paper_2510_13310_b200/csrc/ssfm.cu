@@ -378,6 +378,15 @@ static int setup_gp_pcg_op(ssfm_handle* h, cudaStream_t st) {
 static int setup_ba_pcg(ssfm_handle* h, cudaStream_t st) {
   int rc = setup_ba_pcg_op(h, st);
   if (rc) return rc;
+  // two-pass operator: the camera pass reads factored records (ba_factor,
+  // 7 / 9 doubles per observation instead of 16; SSFM_FACTORED=0: off)
+  const char* fe = getenv("SSFM_FACTORED");
+  if (h->fz.G == 0 && !(fe && fe[0] == '0')) {
+    BADev& d = h->ba;
+    DALLOC(d.Fcm, (long long)(BA_FREC + 3) * d.Npad);
+    DALLOC(d.camlin, d.bp.C);
+    h->pcg_fn = (void*)ba_k_pcg<0, true>;
+  }
   const char* ge = getenv("SSFM_PCG_GRAPH");
   const bool want = ge ? ge[0] == '1' : (h->fz.G == 0 && h->topo.N >= 1000000);
   h->graph_state = want ? 0 : -1;
@@ -772,6 +781,7 @@ static int launch_linearize(ssfm_handle* h, const double* theta, double* r_out, 
   if (h->kind == 0) {
     BADev& d = h->ba;
     ba_k_prep<<<h->cam_blocks, 256, 0, st>>>(d, theta);
+    if (d.camlin) CU(cudaMemcpyAsync(d.camlin, d.cams, sizeof(BACam) * d.bp.C, cudaMemcpyDeviceToDevice, st));
     ba_k_linearize<<<h->lin_blocks, 256, 0, st>>>(d, theta, r_out, J_out, h->red);
     if (d.topo.nt) ba_k_linearize_cm<<<d.topo.nt, SSFM_TILE, 0, st>>>(d, theta);
     if (!sharded(h)) {
@@ -895,8 +905,11 @@ static int build_pcg_graph(ssfm_handle* h) {
     return unavailable(e);
   BADev& d = h->ba;
   int occ_p = 0, occ_c = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, k_g_point, PCG_THREADS, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, k_g_camera, PCG_THREADS, 0);
+  const bool fac = d.Fcm != nullptr;
+  void* kp = (void*)k_g_point;
+  void* kc = fac ? (void*)k_g_camera<true> : (void*)k_g_camera<false>;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, kp, PCG_THREADS, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, kc, PCG_THREADS, 0);
   if (g.fused) {
     switch (h->fz.SL) {
       case 8: capture_fused<8>(h, cs); break;
@@ -906,7 +919,10 @@ static int build_pcg_graph(ssfm_handle* h) {
     }
   } else {
     k_g_point<<<std::max(1, occ_p) * h->num_sms, PCG_THREADS, 0, cs>>>(d, g);
-    if (d.topo.nt) k_g_camera<<<std::max(1, occ_c) * h->num_sms, PCG_THREADS, 0, cs>>>(d, g);
+    if (d.topo.nt) {
+      if (fac) k_g_camera<true><<<std::max(1, occ_c) * h->num_sms, PCG_THREADS, 0, cs>>>(d, g);
+      else k_g_camera<false><<<std::max(1, occ_c) * h->num_sms, PCG_THREADS, 0, cs>>>(d, g);
+    }
   }
   if (sharded(h)) {   // exchange of the camera half of S*p between the passes and q
     k_gx_post<<<CGV_BLOCKS, 256, 0, cs>>>(d, h->fz, g, h->cm);
@@ -1414,20 +1430,24 @@ extern "C" int ssfm_bench_operator(ssfm_handle* h, int32_t which, int32_t reps, 
   if (!h || !ms_out || reps < 1) return set_err(SSFM_INVALID_ARGUMENT, "bad argument");
   if (h->kind != 0) return set_err(SSFM_INVALID_ARGUMENT, "BA handles only");
   cudaStream_t st = (cudaStream_t)stream;
-  int occ = 0;
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, which == 0 ? (const void*)k_op_point : (const void*)k_op_camera,
-                                                   PCG_THREADS, 0));
-  const int grid = std::max(1, occ) * h->num_sms;
   BADev& d = h->ba;
-  for (int w = 0; w < 2; ++w) {   // warm-up
-    if (which == 0) k_op_point<<<grid, PCG_THREADS, 0, st>>>(d, h->p, d.yv);
-    else k_op_camera<<<grid, PCG_THREADS, 0, st>>>(d, d.yv, d.tilebuf);
-  }
+  const bool fac = d.Fcm != nullptr;
+  const void* fn = which == 0 ? (const void*)k_op_point
+                              : (fac ? (const void*)k_op_camera<true> : (const void*)k_op_camera<false>);
+  int occ = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, PCG_THREADS, 0));
+  const int grid = std::max(1, occ) * h->num_sms;
+  auto run = [&]() {
+    if (which == 0) {
+      k_op_point<<<grid, PCG_THREADS, 0, st>>>(d, h->p, d.yv);
+    } else {
+      if (fac) k_op_camera<true><<<grid, PCG_THREADS, 0, st>>>(d, d.yv, d.tilebuf);
+      else k_op_camera<false><<<grid, PCG_THREADS, 0, st>>>(d, d.yv, d.tilebuf);
+    }
+  };
+  for (int w = 0; w < 2; ++w) run();   // warm-up
   CU(cudaEventRecord(h->ev0, st));
-  for (int k = 0; k < reps; ++k) {
-    if (which == 0) k_op_point<<<grid, PCG_THREADS, 0, st>>>(d, h->p, d.yv);
-    else k_op_camera<<<grid, PCG_THREADS, 0, st>>>(d, d.yv, d.tilebuf);
-  }
+  for (int k = 0; k < reps; ++k) run();
   CU(cudaEventRecord(h->ev1, st));
   CU(cudaEventSynchronize(h->ev1));
   float ms = 0.f;
