@@ -13,7 +13,8 @@ import os
 
 from .errors import NativeError, raise_for_status
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libssfm_b200.so")
+LIB_PATH = os.environ.get("SSFM_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
+                                                         "libssfm_b200.so")   # override: kernel-variant experiments
 
 # Functions the header declares (checked by tests/test_native_abi.py).
 EXPORTS = (

@@ -78,6 +78,16 @@ __device__ __forceinline__ void ba_load_frec(const double* __restrict__ F, long 
   }
 }
 
+#ifndef CAMF_MINB
+#define CAMF_MINB 2      // CTAs per SM of the factored camera pass
+#endif
+#ifndef CAMF_UNROLL
+#define CAMF_UNROLL 2
+#endif
+constexpr int kCamfUnroll = CAMF_UNROLL;
+#ifndef CAMF_HOIST
+#define CAMF_HOIST 1     // keep the tile camera's R, qh in registers across the loop
+#endif
 template <bool RO>
 __device__ __forceinline__ void ba_camera_pass_f(const BADev& d, const double* y, double* tile8) {
   const unsigned long long pstream = pol_evict_first(), pkeep = pol_evict_last();
@@ -93,15 +103,24 @@ __device__ __forceinline__ void ba_camera_pass_f(const BADev& d, const double* y
     double o[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) o[k] = 0.0;
-#pragma unroll 1
+#if CAMF_HOIST
+    double R[9], qh[4];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) R[k] = __ldg(cb + k);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) qh[k] = __ldg(cb + 9 + k);
+#endif
+#pragma unroll kCamfUnroll
     for (int i = o0 + lane; i < o1; i += 32) {
+#if !CAMF_HOIST
       // the tile's camera: warp-uniform addresses, L1 broadcasts (not kept
-      // in registers across the loop: 64-register budget)
+      // in registers across the loop: register budget)
       double R[9], qh[4];
 #pragma unroll
       for (int k = 0; k < 9; ++k) R[k] = __ldg(cb + k);
 #pragma unroll
       for (int k = 0; k < 4; ++k) qh[k] = __ldg(cb + 9 + k);
+#endif
       double f[6], vv[3];
       ba_load_frec(d.Fcm, Np, i, model, pstream, f);
 #pragma unroll
@@ -127,11 +146,13 @@ __device__ __forceinline__ void ba_camera_pass_f(const BADev& d, const double* y
     }
     warp_allreduce<8>(o);
     // camera frame -> theta slots: quaternion Pi (.), centre -R^T (.)
+#if !CAMF_HOIST
     double R[9], qh[4];
 #pragma unroll
     for (int k = 0; k < 9; ++k) R[k] = __ldg(cb + k);
 #pragma unroll
     for (int k = 0; k < 4; ++k) qh[k] = __ldg(cb + 9 + k);
+#endif
     double out[8];
     ba_pi_mul(qh, __ldg(cb + 22), o, out);
 #pragma unroll
@@ -616,7 +637,7 @@ __global__ void __launch_bounds__(PCG_THREADS, 4) k_op_point(BADev d, const doub
   ba_point_pass<true>(d, v, y, smp);
 }
 template <bool FAC>
-__global__ void __launch_bounds__(PCG_THREADS, FAC ? 3 : 4) k_op_camera(BADev d, const double* y, double* tile8) {
+__global__ void __launch_bounds__(PCG_THREADS, FAC ? CAMF_MINB : 4) k_op_camera(BADev d, const double* y, double* tile8) {
   __shared__ double smred[(PCG_THREADS / 32) * 8];
   if constexpr (FAC) ba_camera_pass_f<true>(d, y, tile8);
   else ba_camera_pass<true>(d, y, tile8, smred);

@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(PCG_THREADS, 4) k_g_point(BADev d, CGGraphDev 
 
 // FAC: the factored camera pass (ba_camera_pass_f)
 template <bool FAC>
-__global__ void __launch_bounds__(PCG_THREADS, FAC ? 3 : 4) k_g_camera(BADev d, CGGraphDev g) {
+__global__ void __launch_bounds__(PCG_THREADS, FAC ? CAMF_MINB : 4) k_g_camera(BADev d, CGGraphDev g) {
   if (*(volatile int*)(g.ic + 3)) return;
   __shared__ double smred[(PCG_THREADS / 32) * 8];
   if constexpr (FAC) ba_camera_pass_f<true>(d, d.yv, d.tilebuf);   // y is constant during this kernel
