@@ -13,8 +13,15 @@ for p in (ROOT, os.path.join(ROOT, "oracle")):
 
 
 # several shards of one problem share the single test GPU: a lost exchange must
-# fail fast instead of waiting for the 60 s production timeout
-os.environ.setdefault("SSFM_COMM_TIMEOUT_S", "20")
+# fail in bounded time. Same-device shards occasionally stall ~20 s while one
+# shard's kernel waits to be scheduled next to its peer's spinning PCG kernel
+# (not seen with one process per GPU), hence 45 s rather than 20 s.
+os.environ.setdefault("SSFM_COMM_TIMEOUT_S", "45")
+# ... and their streams must not share a hardware work queue: with the default
+# 8 connections two shards' streams can map onto one queue, so a shard's kernel
+# waits behind its peer's spinning PCG kernel (false serialisation, observed as
+# 40 s stalls). Read at CUDA context creation, so set before torch touches CUDA.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 
 def pytest_configure(config):

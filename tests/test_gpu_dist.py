@@ -160,7 +160,7 @@ def test_local_gp_shards_match_single_gpu(gpu, fused):
     cfg = b2.LMConfig(max_iterations=15)
     th1, rep1 = b2.lm_solve(base, base.initial_theta(), cfg)
     # both shards' persistent PCG grids must be co-resident on the one device
-    os.environ["SSFM_PCG_SMS"] = "40"
+    os.environ["SSFM_PCG_SMS"] = "20"
     os.environ["SSFM_FUSED"] = fused
     try:
         probs = [bd.ShardedGPProblem(base, rank=r, world=2, comm="local") for r in range(2)]
