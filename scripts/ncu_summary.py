@@ -28,8 +28,9 @@ for row in det[1:]:
         seen[n] = f"{d.get('Metric Value', '')} {d.get('Metric Unit', '')}".strip()
 kernel = dict(zip(h, det[1])).get("Kernel Name", "") if len(det) > 1 else ""
 raw = page("--page", "raw")
-rh, rv = raw[0], raw[2]
+rh, ru, rv = raw[0], raw[1], raw[2]
 rawd = dict(zip(rh, rv))
+rawu = dict(zip(rh, ru))
 print(f"# {title}\n")
 print(f"Kernel: `{kernel[:120]}`\n")
 print("| metric | value |\n|---|---|")
@@ -38,7 +39,7 @@ for k in want:
         print(f"| {k} | {seen[k]} |")
 for k in ("dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum", "gpu__time_duration.sum"):
     if k in rawd:
-        print(f"| {k} | {rawd[k]} |")
+        print(f"| {k} | {rawd[k]} {rawu.get(k, '')} |")
 src = page("--page", "source", "--print-source", "sass")
 sh = src[1]
 data = [dict(zip(sh, r)) for r in src[2:] if len(r) == len(sh)]
