@@ -345,6 +345,10 @@ def run_b200(args, ws, rank, local):
     e2e = None
     if not args.no_e2e:
         theta_host = theta_start(problem)
+        if ws == 1 and hasattr(problem, "release"):
+            # the device-timed handle is done: its device blocks go back to the
+            # library's block cache, as in an application solving problems in turn
+            problem.release()
         # the per-observation inputs live in pinned host memory (staged before
         # the timed region, as an application feeding the solver would)
         def pinned(x):

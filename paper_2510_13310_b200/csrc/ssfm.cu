@@ -12,6 +12,8 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -102,17 +104,51 @@ struct ssfm_handle {
   bool linearized = false;
   Profile prof;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
+  std::vector<size_t> alloc_bytes;   // sizes of allocs (block cache)
 };
+
+// Device blocks of destroyed handles are kept for reuse by exact size (per
+// device, up to SSFM_BLOCK_CACHE_GB, default 48): re-creating a handle of the
+// same shape -- repeated solves, the GP -> BA pipeline, the e2e bench -- skips
+// cudaMalloc / cudaFree, whose page mapping and implicit device syncs cost
+// 40-190 ms at C5. Guarded by a mutex (handles may be created from several
+// host threads).
+struct BlockCache {
+  std::mutex mu;
+  std::multimap<std::pair<int, size_t>, void*> free_blocks;   // (device, bytes) -> block
+  size_t bytes = 0;
+};
+static BlockCache& block_cache() {
+  static BlockCache c;
+  return c;
+}
+static size_t block_cache_cap() {
+  const char* e = getenv("SSFM_BLOCK_CACHE_GB");
+  return (size_t)((e ? atof(e) : 48.0) * (double)(1ull << 30));
+}
 
 template <typename T>
 static int dalloc(ssfm_handle* h, T** ptr, size_t count) {
   size_t b = sizeof(T) * (count > 0 ? count : 1);
   b = (b + 255) & ~size_t(255);
   void* p = nullptr;
-  cudaError_t e = cudaMalloc(&p, b);
-  if (e != cudaSuccess)
-    return set_err(SSFM_CUDA_ERROR, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  {
+    BlockCache& bc = block_cache();
+    std::lock_guard<std::mutex> lk(bc.mu);
+    auto it = bc.free_blocks.find({h->device, b});
+    if (it != bc.free_blocks.end()) {
+      p = it->second;
+      bc.free_blocks.erase(it);
+      bc.bytes -= b;
+    }
+  }
+  if (!p) {
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e != cudaSuccess)
+      return set_err(SSFM_CUDA_ERROR, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  }
   h->allocs.push_back(p);
+  h->alloc_bytes.push_back(b);
   h->bytes += b;
   *ptr = static_cast<T*>(p);
   return SSFM_OK;
@@ -131,7 +167,22 @@ static void free_handle(ssfm_handle* h) {
   for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
   if (h->pcg_exec) cudaGraphExecDestroy(h->pcg_exec);
   if (h->pcg_graph) cudaGraphDestroy(h->pcg_graph);
-  for (void* p : h->allocs) cudaFree(p);
+  if (!h->allocs.empty()) {
+    // no kernel may still use the blocks (cudaFree synchronized implicitly)
+    cudaDeviceSynchronize();
+    BlockCache& bc = block_cache();
+    const size_t cap = block_cache_cap();
+    std::lock_guard<std::mutex> lk(bc.mu);
+    for (size_t k = 0; k < h->allocs.size(); ++k) {
+      const size_t b = h->alloc_bytes[k];
+      if (bc.bytes + b <= cap) {
+        bc.free_blocks.emplace(std::make_pair(h->device, b), h->allocs[k]);
+        bc.bytes += b;
+      } else {
+        cudaFree(h->allocs[k]);
+      }
+    }
+  }
   if (h->region) cudaFree(h->region);
   if (h->hmisc) cudaFreeHost(h->hmisc);
   if (h->ev0) cudaEventDestroy(h->ev0);
@@ -454,11 +505,22 @@ extern "C" int ssfm_create_ba(const ssfm_ba_desc* desc, void* stream, ssfm_handl
   h->total_params = 7ll * C + 3ll * P + (d.bp.focal_mode == 1 ? C : d.bp.focal_mode == 2 ? 1 : 0);
   h->total_res = 2 * N;
   auto fail = [&](int rc) { free_handle(h); return rc; };
+  // SSFM_TIMING=1: phase times of the creation on stderr (diagnostic)
+  const bool timing = getenv("SSFM_TIMING") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!timing) return;
+    cudaStreamSynchronize(st);
+    auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[ssfm create] %s %.1f ms\n", what, std::chrono::duration<double, std::milli>(t - t_last).count());
+    t_last = t;
+  };
   int rc;
   int* dstatus;
   if ((rc = dalloc(h, &dstatus, 1))) return fail(rc);
   d.status = dstatus;
   if ((rc = build_topo(h, desc->cam_idx, desc->pt_idx, C, P, N, st, dstatus))) return fail(rc);
+  mark("topology");
   d.topo = h->topo;
   const Topo& T = h->topo;
   d.Npad = (N + 31) & ~31ll;
@@ -507,9 +569,11 @@ extern "C" int ssfm_create_ba(const ssfm_ba_desc* desc, void* stream, ssfm_handl
   if ((rc = common_alloc(h, 8 * C, C))) return fail(rc);
   d.scal = h->misc->scal;
   d.status = &h->misc->status;
+  mark("arrays");
   // launch geometry of the PCG kernel (fused single-pass operator when the
   // camera vector fits the shared memory of <= 8 CTAs, else two-pass)
   if ((rc = setup_ba_pcg(h, st))) return fail(rc);
+  mark("pcg setup");
   h->lin_blocks = std::max(1, std::min(nblk(T.nb, 8), h->num_sms * 16));
   h->cost_blocks = nblk(N, 256);
   h->cam_blocks = nblk(C, 256);
@@ -959,7 +1023,11 @@ static int launch_pcg(ssfm_handle* h, double lam, const ssfm_lm_config* cfg, cud
     h->graph_state = 0;
   }
   if (h->kind == 0 && h->graph_state == 0) {
+    const auto tg = std::chrono::steady_clock::now();
     int rc = build_pcg_graph(h);
+    if (getenv("SSFM_TIMING"))
+      fprintf(stderr, "[ssfm] graph build %.1f ms\n",
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tg).count());
     if (rc) return rc;
     h->graph_sharded = sharded(h);
   }
