@@ -452,7 +452,11 @@ static int setup_ba_pcg_op(ssfm_handle* h, cudaStream_t st) {
   h->pcg_sms = pcg_sms_of(h);
   const int C = h->ba.bp.C;
   const char* env = getenv("SSFM_FUSED");
-  const bool want = !(env && env[0] == '0') && C < FZ_MAX_CAMERAS;
+  // Default: fused below 250k observations; from there the two-pass operator
+  // with the factored camera pass in the CUDA graph is faster (C4-BA 4M obs:
+  // 0.169 vs 0.21 ms per CG iteration; C3 680k: 0.056 vs 0.066).
+  // SSFM_FUSED=1 (or 2/4/8) forces the fused operator, SSFM_FUSED=0 two-pass.
+  const bool want = (env ? env[0] != '0' : h->topo.N < 250000) && C < FZ_MAX_CAMERAS;
   // SSFM_FUSED=0 forces the two-pass operator; SSFM_FUSED=2/4/8 forces that many
   // slot groups (tests exercise the multi-group path on small problems)
   const int force_g = (env && (env[0] == '2' || env[0] == '4' || env[0] == '8')) ? env[0] - '0' : 1;
