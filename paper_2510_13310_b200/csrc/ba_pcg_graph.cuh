@@ -65,7 +65,8 @@ __global__ void __launch_bounds__(256) k_g_init(BADev d, CGGraphDev g) {
 }
 
 // init scalars: rho, tol, done (rn <= tol), iteration cap
-__global__ void k_g_init2(BADev d, CGGraphDev g, int nblk) {
+template <typename Dev>   // BADev or GPDev: scal
+__global__ void k_g_init2(Dev d, CGGraphDev g, int nblk) {
   __shared__ double smb[4];
   const double rr = g_partials_sum(g.partA, nblk, 0, &smb[0]);
   const double rho = g_partials_sum(g.partA, nblk, 1, &smb[1]);
@@ -249,7 +250,8 @@ __global__ void __launch_bounds__(256) k_g_pupdate(BADev d, CGGraphDev g, int nb
 }
 
 // scalars of the iteration and the loop condition (one block)
-__global__ void k_g_scalars(BADev d, CGGraphDev g, int nblk, cudaGraphConditionalHandle hc) {
+template <typename Dev>   // BADev or GPDev: status
+__global__ void k_g_scalars(Dev d, CGGraphDev g, int nblk, cudaGraphConditionalHandle hc) {
   __shared__ double smb[4];
   int done = *(volatile int*)(g.ic + 3);
   if (!done) {

@@ -20,6 +20,7 @@
 #include "../../include/ssfm.h"
 #include "ba_pcg.cuh"
 #include "ba_pcg_graph.cuh"
+#include "gp_pcg_graph.cuh"
 #include "gp_kernels.cuh"
 #include "pattern.cuh"
 #include "block_algebra.cuh"
@@ -380,16 +381,18 @@ static int build_fused_schedule(ssfm_handle* h, int slots, int* status, cudaStre
 }
 
 static int setup_ba_pcg_op(ssfm_handle* h, cudaStream_t st);
-// GP PCG operator: fused single pass (gp_fused_pass) for N >= 1M observations
-// when the 4-slot camera vector fits one CTA's shared memory, else two-pass.
-// Measured (1xB200, ms per CG iteration): C4 GP 4M obs 0.158 fused vs 0.175
-// two-pass; C2 GP 300k obs 0.042 vs 0.034 (too little work per CTA for the
-// ticket-ordered accumulation to pay). SSFM_FUSED=0/1 forces either.
+// GP PCG operator. Default: the two-pass operator, as a CUDA graph from 250k
+// observations (single-rank), else the persistent kernel. Measured (1xB200,
+// ms per CG iteration): C4 GP 4M obs -- graph two-pass 0.137, fused persistent
+// 0.158, two-pass persistent 0.175; C2 GP 300k obs -- 0.035 either two-pass,
+// fused 0.042. SSFM_FUSED=1 selects the fused single pass (gp_fused_pass) when
+// the 4-slot camera vector fits one CTA's shared memory; SSFM_FUSED=0 two-pass.
 static int setup_gp_pcg_op(ssfm_handle* h, cudaStream_t st) {
   h->pcg_sms = pcg_sms_of(h);
+  h->graph_state = -1;
   const int C = h->gp.gp.C;
   const char* env = getenv("SSFM_FUSED");
-  const bool want = env ? env[0] != '0' : h->topo.N >= 1000000;
+  const bool want = env ? env[0] != '0' : false;
   if (want && C < FZ_MAX_CAMERAS) {
     cudaFuncAttributes fa;
     CU(cudaFuncGetAttributes(&fa, gp_k_pcg<true>));
@@ -422,6 +425,10 @@ static int setup_gp_pcg_op(ssfm_handle* h, cudaStream_t st) {
   h->pcg_smem = 0;
   h->pcg_fn = (void*)gp_k_pcg<false>;
   h->fz = FusedTopo{};
+  // the two-pass GP operator runs as a CUDA graph (gp_pcg_graph.cuh) from
+  // 250k observations on single-rank handles; SSFM_GP_GRAPH=1 / 0 forces either
+  const char* ge = getenv("SSFM_GP_GRAPH");
+  h->graph_state = (ge ? ge[0] == '1' : h->topo.N >= 250000) ? 0 : -1;
   return SSFM_OK;
 }
 
@@ -1010,6 +1017,59 @@ static int build_pcg_graph(ssfm_handle* h) {
   return SSFM_OK;
 }
 
+// GP: the PCG as a CUDA graph (gp_pcg_graph.cuh); single-rank two-pass handles
+static int build_gp_pcg_graph(ssfm_handle* h) {
+  CGGraphDev& g = h->gdev;
+  g.x = h->x; g.r = h->r; g.z = h->z; g.p = h->p; g.q = h->q;
+  DALLOC(g.partA, 2 * CGV_BLOCKS + 2);
+  DALLOC(g.partB, 2 * CGV_BLOCKS + 2);
+  DALLOC(g.sc, 8);
+  DALLOC(g.ic, 4);
+  g.ctl = &h->misc->ctl;
+  g.fused = 0;
+  g.ngrp = 0;
+  cudaGraphConditionalHandle hc;
+  cudaGraphNodeParams cp = {};
+  cudaGraphNode_t cn;
+  cudaStream_t cs = nullptr;
+  auto unavailable = [&](cudaError_t e) {
+    cudaGetLastError();
+    if (cs) cudaStreamDestroy(cs);
+    h->pcg_graph = nullptr;
+    h->graph_state = -1;
+    (void)e;
+    return SSFM_OK;
+  };
+  cudaError_t e;
+  if ((e = cudaGraphCreate(&h->pcg_graph, 0))) return unavailable(e);
+  if ((e = cudaGraphConditionalHandleCreate(&hc, h->pcg_graph, 1, cudaGraphCondAssignDefault))) return unavailable(e);
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = hc;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  if ((e = cudaGraphAddNode(&cn, h->pcg_graph, nullptr, 0, &cp))) return unavailable(e);
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  if ((e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking))) return unavailable(e);
+  if ((e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed)))
+    return unavailable(e);
+  GPDev& d = h->gp;
+  int occ_p = 0, occ_c = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, (const void*)k_gg_point, PCG_THREADS, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, (const void*)k_gg_camera, PCG_THREADS, 0);
+  k_gg_point<<<std::max(1, occ_p) * h->num_sms, PCG_THREADS, 0, cs>>>(d, g);
+  if (d.topo.nt) k_gg_camera<<<std::max(1, occ_c) * h->num_sms, PCG_THREADS, 0, cs>>>(d, g);
+  k_gg_q<<<CGV_BLOCKS, 256, 0, cs>>>(d, g);
+  k_gg_update<<<CGV_BLOCKS, 256, 0, cs>>>(d, g, CGV_BLOCKS);
+  k_gg_pupdate<<<CGV_BLOCKS, 256, 0, cs>>>(d, g, CGV_BLOCKS);
+  k_g_scalars<<<1, 32, 0, cs>>>(d, g, CGV_BLOCKS, hc);
+  h->graph_body_kernels = 6;
+  if ((e = cudaStreamEndCapture(cs, &body))) return unavailable(e);
+  if ((e = cudaGraphInstantiate(&h->pcg_exec, h->pcg_graph, 0))) return unavailable(e);
+  cudaStreamDestroy(cs);
+  h->graph_state = 1;
+  return SSFM_OK;
+}
+
 static int launch_pcg(ssfm_handle* h, double lam, const ssfm_lm_config* cfg, cudaStream_t st) {
   int max_it = cfg->cg_max_iters;
   double tol = cfg->cg_tol;
@@ -1027,6 +1087,21 @@ static int launch_pcg(ssfm_handle* h, double lam, const ssfm_lm_config* cfg, cud
     h->pcg_exec = nullptr;
     h->pcg_graph = nullptr;
     h->graph_state = 0;
+  }
+  if (h->kind == 1 && sharded(h)) h->graph_state = -1;   // sharded GP: persistent kernel (in-kernel exchange)
+  if (h->kind == 1 && h->graph_state == 0) {
+    int rc = build_gp_pcg_graph(h);
+    if (rc) return rc;
+  }
+  if (h->kind == 1 && h->graph_state == 1) {
+    CGGraphDev& g = h->gdev;
+    k_g_setparams<<<1, 1, 0, st>>>(g, lam, tol, max_it);
+    k_gg_init<<<CGV_BLOCKS, 256, 0, st>>>(h->gp, g);
+    k_g_init2<<<1, 32, 0, st>>>(h->gp, g, CGV_BLOCKS);
+    CU(cudaGraphLaunch(h->pcg_exec, st));
+    count_launch(h, 3);
+    h->graph_pending = true;
+    return SSFM_OK;
   }
   if (h->kind == 0 && h->graph_state == 0) {
     const auto tg = std::chrono::steady_clock::now();

@@ -241,3 +241,27 @@ def test_factored_wide_scene_and_trajectory(gpu, graph):
     b, rb = b2.lm_solve(fac, th0, b2.LMConfig(max_iterations=10))
     assert [i.step_accepted for i in ra.iterations] == [i.step_accepted for i in rb.iterations]
     assert abs(ra.iterations[-1].cost_after - rb.iterations[-1].cost_after) <= 1e-10 * ra.iterations[-1].cost_after
+
+
+def test_gp_graph_pcg_matches_persistent_kernel(gpu):
+    """GP PCG as a CUDA graph (gp_pcg_graph.cuh) vs the persistent two-pass
+    kernel: same damped step, deterministic, CGStall at the cap."""
+    make = gp_wide()
+    per = with_env({"SSFM_FUSED": "0", "SSFM_GP_GRAPH": "0"}, make)
+    gra = with_env({"SSFM_FUSED": "0", "SSFM_GP_GRAPH": "1"}, make)
+    cfg = b2.LMConfig(cg_tol=1e-12, cg_max_iters=5000)
+    th = per.initial_theta()
+    per.gradient(th)
+    gra.gradient(th)
+    for lam in (1e-4, 1e-1):
+        d0, it0 = solve_normal_native(gpu, per, lam, cfg)
+        d1, it1 = solve_normal_native(gpu, gra, lam, cfg)
+        assert rel(d1, d0) < 1e-9 and abs(it1 - it0) <= max(2, 0.03 * it0)
+        d2, it2 = solve_normal_native(gpu, gra, lam, cfg)
+        assert np.array_equal(d1, d2) and it1 == it2
+    with pytest.raises(b2.errors.CGStall):
+        solve_normal_native(gpu, gra, 1e-4, b2.LMConfig(cg_max_iters=2))
+    a, ra = b2.lm_solve(per, th, b2.LMConfig(max_iterations=10))
+    b, rb = b2.lm_solve(gra, th, b2.LMConfig(max_iterations=10))
+    assert [i.step_accepted for i in ra.iterations] == [i.step_accepted for i in rb.iterations]
+    assert np.abs(a - b).max() < 1e-8
