@@ -325,7 +325,7 @@ def run_b200(args, ws, rank, local):
     ms_per_step = ms_max / max(steps, 1)
     value = N * steps / (ms_max / 1e3)
     log(f"[rank {rank}] timed {steps} its in {ms_total:.1f} ms; cg {[i.cg_iters for i in rep_t.iterations]}; "
-        f"term {rep_t.termination}")
+        f"term {rep_t.termination}; device ms {[round(i.device_ms, 2) for i in rep_t.iterations]}")
 
     # roofline of the dominant kernel: the PCG solve (ba_k_pcg), S*p dominated
     peak, peak_kind = peaks()
