@@ -15,6 +15,7 @@ within 1e-7 relative: only the summation order differs, so
 each damped step agrees with the single-GPU one to the CG tolerance 1e-8 and
 the cost after it to about that, relative).
 """
+import gc
 import os
 import subprocess
 import sys
@@ -60,13 +61,27 @@ def solve_local_shards(gpu, st, world, cfg, fused="1", graph="0"):
         except Exception as e:   # noqa: BLE001
             errs.append(e)
 
-    ts = [threading.Thread(target=work, args=(r,)) for r in range(world)]
-    for t in ts:
-        t.start()
-    for t in ts:
-        t.join(timeout=300)
+    run_shards(work, world, 300)
     assert not errs, errs
     return probs, out
+
+
+def run_shards(work, n, timeout):
+    """One host thread per same-device shard. Unreachable handles of earlier
+    tests are destroyed first and the garbage collector is paused meanwhile: a
+    handle destroyed inside a shard's thread synchronises the device while the
+    peer's PCG kernel waits on that shard (a same-device-only hazard; with one
+    process per GPU it cannot happen)."""
+    gc.collect()
+    gc.disable()
+    try:
+        ts = [threading.Thread(target=work, args=(r,)) for r in range(n)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join(timeout=timeout)
+    finally:
+        gc.enable()
 
 
 @pytest.mark.parametrize("world,fused,graph", [(2, "1", "0"), (3, "1", "0"), (2, "0", "0"), (2, "0", "1"),
@@ -118,9 +133,7 @@ def test_sharded_cost_and_gradient_are_global(gpu):
             p = probs[r]
             res[r] = (p.cost(p.encode()), p.gradient(p.encode()))
 
-    ts = [threading.Thread(target=work, args=(r,)) for r in range(2)]
-    [t.start() for t in ts]
-    [t.join(timeout=120) for t in ts]
+    run_shards(work, 2, 120)
     assert res[0][0] == res[1][0] == pytest.approx(c1, rel=1e-13)
     C = st.num_cameras
     # camera part of the gradient is the global one on every rank; point parts are local
@@ -174,9 +187,7 @@ def test_local_gp_shards_match_single_gpu(gpu, fused):
         with gpu.cuda.stream(gpu.cuda.Stream()):
             out[r] = b2.lm_solve(probs[r], probs[r].initial_theta(), cfg)
 
-    ts = [threading.Thread(target=work, args=(r,)) for r in range(2)]
-    [t.start() for t in ts]
-    [t.join(timeout=300) for t in ts]
+    run_shards(work, 2, 300)
     ra, rb = out[0][1], out[1][1]
     assert [(i.cost_after, i.cg_iters) for i in ra.iterations] == [(i.cost_after, i.cg_iters) for i in rb.iterations]
     assert [i.step_accepted for i in ra.iterations] == [i.step_accepted for i in rep1.iterations]
