@@ -15,6 +15,6 @@ timeout 600 python bench.py --config c4ba --no-cpu-baseline --steps 10 > gpurun_
 timeout 600 ncu --graph-profiling graph --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 1200 --csv --log-file gpurun_out/launches_c5.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_op_point -s 2 -c 1 -o gpurun_out/op_point_c5 -f python scripts/dev_passes.py > gpurun_out/ncu_p.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_op_camera -s 2 -c 1 -o gpurun_out/op_camera_c5 -f python scripts/dev_passes.py > gpurun_out/ncu_c.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:ba_k_pcg -c 1 -o gpurun_out/pcg_c4ba_full -f python bench.py --config c4ba --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_c4.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:gp_k_pcg -c 1 -o gpurun_out/pcg_c4gp_full -f python bench.py --config c4gp --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_gp.log 2>&1
+SSFM_FUSED=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:ba_k_pcg -c 1 -o gpurun_out/pcg_c4ba_full -f python bench.py --config c4ba --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_c4.log 2>&1
+SSFM_FUSED=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gp_k_pcg -c 1 -o gpurun_out/pcg_c4gp_full -f python bench.py --config c4gp --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_gp.log 2>&1
 cat gpurun_out/pytest_gpu.log
