@@ -280,8 +280,10 @@ __global__ void __launch_bounds__(SSFM_TILE) ba_k_linearize_cm(BADev d, const do
     double r[2], J[BA_JREC], ct, F[BA_FREC + 3];
     ba_obs_eval(d.bp, d.cams + c, theta + d.bp.off_pts + 3ll * j, d.pix_cm + 2ll * i, r, J, &ct,
                 d.Fcm ? F : nullptr);
+    if (d.Jcm) {
 #pragma unroll
-    for (int k = 0; k < BA_JREC; ++k) d.Jcm[k * Np + i] = J[k];
+      for (int k = 0; k < BA_JREC; ++k) d.Jcm[k * Np + i] = J[k];
+    }
     if (d.Fcm) {
 #pragma unroll
       for (int k = 0; k < BA_FREC + 3; ++k) d.Fcm[k * Np + i] = F[k];
@@ -445,6 +447,103 @@ __global__ void ba_k_ptinv(BADev d, double lam) {
 //   sum_o E_o y0_j                                 -> 8
 // (the diagonal slots of schur_fill_cy and b_red, lm.py:608-626)
 // ---------------------------------------------------------------------------
+// Factored form (two-pass handles, no Jcm): the rows of Jc in the camera
+// frame, a~_r = [D(v)^T (SE)_r ; -(SE)_r ; phi e_r], are reduced over the
+// tile and mapped once per tile by T = diag(Pi, R^T, 1): W = T W~ T^T.
+__device__ __forceinline__ void ba_precond_f(const BADev& d, int t, double* v) {
+  const int o0 = d.topo.tile_obs[t], o1 = d.topo.tile_obs[t + 1];
+  const int i = o0 + threadIdx.x;
+  if (i >= o1) return;
+  const long long Np = d.Npad;
+  const double* cb = reinterpret_cast<const double*>(d.camlin + d.topo.tile_cam[t]);
+  double f[6], vv[3];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) f[k] = d.Fcm[k * Np + i];
+  if (d.bp.model == 1) { f[4] = d.Fcm[4 * Np + i]; f[5] = d.Fcm[5 * Np + i]; }
+  else { f[4] = 0.0; f[5] = f[0]; }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) vv[k] = d.Fcm[(6 + k) * Np + i];
+  const int j = d.topo.cm_pt[i];
+  double ci[6], y[3], qh[4];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) ci[k] = d.Cinv[6ll * j + k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) y[k] = d.y0[3ll * j + k];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) qh[k] = cb[9 + k];
+  const double se[2][3] = {{f[0], f[4], -(f[0] * f[1] + f[4] * f[2])},
+                           {f[4], f[5], -(f[4] * f[1] + f[5] * f[2])}};
+  double jp[2][3];
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) jp[r][k] = se[r][0] * cb[k] + se[r][1] * cb[3 + k] + se[r][2] * cb[6 + k];
+  double w0[3], w1[3];
+  sym3_matvec(ci, jp[0], w0);
+  sym3_matvec(ci, jp[1], w1);
+  const double k00 = jp[0][0] * w0[0] + jp[0][1] * w0[1] + jp[0][2] * w0[2];
+  const double k01 = jp[1][0] * w0[0] + jp[1][1] * w0[1] + jp[1][2] * w0[2];
+  const double k11 = jp[1][0] * w1[0] + jp[1][1] * w1[1] + jp[1][2] * w1[2];
+  double a[8], b[8];
+  ba_dqt_mul(qh, vv, se[0], a);
+  ba_dqt_mul(qh, vv, se[1], b);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) { a[4 + k] = -se[0][k]; b[4 + k] = -se[1][k]; }
+  a[7] = f[3] * f[1];
+  b[7] = f[3] * f[2];
+  double ka[8], kb[8];
+#pragma unroll
+  for (int p = 0; p < 8; ++p) { ka[p] = k00 * a[p] + k01 * b[p]; kb[p] = k01 * a[p] + k11 * b[p]; }
+  int idx = 0;
+#pragma unroll
+  for (int p = 0; p < 8; ++p)
+#pragma unroll
+    for (int q = p; q < 8; ++q) v[idx++] = a[p] * ka[q] + b[p] * kb[q];
+  const double ty0 = jp[0][0] * y[0] + jp[0][1] * y[1] + jp[0][2] * y[2];
+  const double ty1 = jp[1][0] * y[0] + jp[1][1] * y[1] + jp[1][2] * y[2];
+#pragma unroll
+  for (int p = 0; p < 8; ++p) v[36 + p] = a[p] * ty0 + b[p] * ty1;
+}
+
+// W = T W~ T^T, u = T u~ for the tile's camera, T = diag(Pi, R^T, 1): one
+// output entry per lane of warp 0 (packed upper 36 + 8), from W~ in shared
+__device__ __forceinline__ double ba_precond_t(const double* cb, int p, int a) {
+  if (p < 4) return a < 4 ? ((p == a ? 1.0 : 0.0) - cb[9 + p] * cb[9 + a]) * cb[22] : 0.0;
+  if (p < 7) return (a >= 4 && a < 7) ? cb[3 * (a - 4) + (p - 4)] : 0.0;   // R^T
+  return a == 7 ? 1.0 : 0.0;
+}
+__device__ __forceinline__ int ba_pk(int a, int b) {   // packed upper index, a <= b
+  return a * 8 - a * (a - 1) / 2 + (b - a);
+}
+__device__ __forceinline__ void ba_blk(int p, int* lo, int* hi) {
+  if (p < 4) { *lo = 0; *hi = 4; } else if (p < 7) { *lo = 4; *hi = 7; } else { *lo = 7; *hi = 8; }
+}
+__device__ __forceinline__ double ba_precond_f_entry(const double* cb, const double* w, int o) {
+  if (o >= 36) {
+    const int p = o - 36;
+    int lo, hi;
+    ba_blk(p, &lo, &hi);
+    double sacc = 0.0;
+    for (int a = lo; a < hi; ++a) sacc += ba_precond_t(cb, p, a) * w[36 + a];
+    return sacc;
+  }
+  int p = 0, rem = o;
+  while (rem >= 8 - p) { rem -= 8 - p; ++p; }
+  const int q = p + rem;
+  int pl, ph, ql, qh_;
+  ba_blk(p, &pl, &ph);
+  ba_blk(q, &ql, &qh_);
+  double sacc = 0.0;
+  for (int a = pl; a < ph; ++a) {
+    const double tpa = ba_precond_t(cb, p, a);
+    for (int b = ql; b < qh_; ++b) {
+      const double wab = a <= b ? w[ba_pk(a, b)] : w[ba_pk(b, a)];
+      sacc += tpa * wab * ba_precond_t(cb, q, b);
+    }
+  }
+  return sacc;
+}
+
 __global__ void __launch_bounds__(SSFM_TILE) ba_k_precond(BADev d) {
   __shared__ double sm[(SSFM_TILE / 32) * CAM_V];
   const int t = blockIdx.x;
@@ -453,6 +552,22 @@ __global__ void __launch_bounds__(SSFM_TILE) ba_k_precond(BADev d) {
   double v[CAM_V];
 #pragma unroll
   for (int k = 0; k < CAM_V; ++k) v[k] = 0.0;
+  if (!d.Jcm) {
+    __shared__ double smw[CAM_V];
+    ba_precond_f(d, t, v);
+    block_reduce<CAM_V>(v, sm);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int k = 0; k < CAM_V; ++k) smw[k] = v[k];
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const double* cb = reinterpret_cast<const double*>(d.camlin + d.topo.tile_cam[t]);
+      double* dst = d.tilebuf + (long long)CAM_V * t;
+      for (int o = threadIdx.x; o < CAM_V; o += 32) dst[o] = ba_precond_f_entry(cb, smw, o);
+    }
+    return;
+  }
   if (i < o1) {
     const long long Np = d.Npad;
     double J[BA_JREC];

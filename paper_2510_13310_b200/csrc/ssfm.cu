@@ -559,7 +559,6 @@ extern "C" int ssfm_create_ba(const ssfm_ba_desc* desc, void* stream, ssfm_handl
   d.pix_pm = pix_pm; d.pps = pps; d.dists = dists; d.focals = focals;
   if ((rc = dalloc(h, &d.cams, C))) return fail(rc);
   if ((rc = dalloc(h, &d.Jpm, BA_JREC * d.Npad))) return fail(rc);
-  if ((rc = dalloc(h, &d.Jcm, BA_JREC * d.Npad))) return fail(rc);
   if ((rc = dalloc(h, &d.rcm, 2 * d.Npad))) return fail(rc);
   if ((rc = dalloc(h, &d.Cpt, 6ll * P))) return fail(rc);
   if ((rc = dalloc(h, &d.gpt, 3ll * P))) return fail(rc);
@@ -586,6 +585,9 @@ extern "C" int ssfm_create_ba(const ssfm_ba_desc* desc, void* stream, ssfm_handl
   // launch geometry of the PCG kernel (fused single-pass operator when the
   // camera vector fits the shared memory of <= 8 CTAs, else two-pass)
   if ((rc = setup_ba_pcg(h, st))) return fail(rc);
+  // the camera-major Jacobian copy: only without the factored record (the
+  // fused operator, SSFM_FACTORED=0); two-pass handles read Fcm instead
+  if (!d.Fcm && (rc = dalloc(h, &d.Jcm, BA_JREC * d.Npad))) return fail(rc);
   mark("pcg setup");
   h->lin_blocks = std::max(1, std::min(nblk(T.nb, 8), h->num_sms * 16));
   h->cost_blocks = nblk(N, 256);
@@ -1561,6 +1563,9 @@ extern "C" int ssfm_check_jacobian(ssfm_handle* h, int64_t* mismatches, void* st
   if (!h || !mismatches) return set_err(SSFM_INVALID_ARGUMENT, "null argument");
   if (h->kind != 0) return set_err(SSFM_INVALID_ARGUMENT, "BA handles only");
   if (!h->linearized) return set_err(SSFM_INVALID_ARGUMENT, "ssfm_check_jacobian before ssfm_linearize");
+  if (!h->ba.Jcm)
+    return set_err(SSFM_INVALID_ARGUMENT, "no camera-major Jacobian copy: this handle's camera pass reads the "
+                                          "factored record (SSFM_FACTORED=0 keeps the copy)");
   cudaStream_t st = (cudaStream_t)stream;
   unsigned long long* dm = nullptr;
   CU(cudaMalloc(&dm, sizeof(unsigned long long)));

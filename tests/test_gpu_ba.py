@@ -8,6 +8,7 @@ tolerance 1e-8), LM final cost 1e-10 relative and RMSE 1e-6 relative
 (the BA gauge is free).
 """
 import ctypes as ct
+import os
 
 import numpy as np
 import pytest
@@ -371,9 +372,20 @@ def test_shared_focal_vs_reference(gpu):          # test_ba.py:225-230 + the sha
 @pytest.mark.parametrize("name", BA_GOLDENS + ["ba_shared.npz"])
 def test_jacobian_copies_bitwise_identical(gpu, name):
     """The camera-major Jacobian copy (camera-tile linearize pass) equals the
-    point-major one bit for bit: one expression tree, same inputs."""
+    point-major one bit for bit: one expression tree, same inputs. (Handles of
+    the two-pass operator keep no copy, they read the factored record: the
+    copy is requested explicitly.)"""
     z = golden(name)
-    p = problem_from_golden(z)
+    old = os.environ.get("SSFM_FACTORED")
+    os.environ["SSFM_FACTORED"] = "0"
+    try:
+        p = problem_from_golden(z)
+        p._native_handle()
+    finally:
+        if old is None:
+            os.environ.pop("SSFM_FACTORED")
+        else:
+            os.environ["SSFM_FACTORED"] = old
     p.gradient(z["theta0"] * (1 + 1e-3 * np.sin(np.arange(len(z["theta0"])))))
     m = ct.c_int64(-1)
     _native.check(_native.load().ssfm_check_jacobian(ct.c_void_p(p._native_handle().ptr), ct.byref(m),

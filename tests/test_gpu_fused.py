@@ -223,7 +223,11 @@ def test_factored_two_pass_matches_jacobian_two_pass(gpu, name):
         d0, it0 = solve_normal_native(gpu, ref, lam, cfg)
         d1, it1 = solve_normal_native(gpu, fac, lam, cfg)
         assert rel(d1, d0) < 1e-9, (lam, rel(d1, d0))
-        assert abs(it1 - it0) <= max(2, 0.03 * it0)
+        # both the camera pass and the Schur preconditioner blocks are rebuilt
+        # from the factored record (to rounding): the stop at cg_tol 1e-12 on
+        # the shared-focal system (one focal coupled to every camera) moves by
+        # up to 4 of 46 iterations; the steps agree to 1e-9
+        assert abs(it1 - it0) <= max(4, 0.1 * it0)
         d2, it2 = solve_normal_native(gpu, fac, lam, cfg)
         assert np.array_equal(d1, d2) and it1 == it2
 
