@@ -201,20 +201,21 @@ def test_gp_fused_lm_trajectory_matches_two_pass(gpu):
     assert np.abs(a - b).max() < 1e-8
 
 
-def factored_problem(make, fac):
-    return with_env({"SSFM_FUSED": "0", "SSFM_FACTORED": fac, "SSFM_PCG_GRAPH": "0"}, make)
+def factored_problem(make, fac, graph="0"):
+    return with_env({"SSFM_FUSED": "0", "SSFM_FACTORED": fac, "SSFM_PCG_GRAPH": graph}, make)
 
 
+@pytest.mark.parametrize("graph", ["0", "1"])
 @pytest.mark.parametrize("name", ["ba_small.npz", "ba_bal.npz", "ba_nofocal.npz", "ba_shared.npz"])
-def test_factored_two_pass_matches_jacobian_two_pass(gpu, name):
+def test_factored_two_pass_matches_jacobian_two_pass(gpu, name, graph):
     """The factored camera pass (ba_factor: sw du_dp = S E, Jc^T Jp rebuilt from
     the camera cache) applies the stored Jacobian's operator to rounding: same damped
     step (1e-9 at cg_tol 1e-12), CG counts within rounding, deterministic;
     every camera model and focal mode."""
     z = golden(name)
     make = lambda: problem_from_golden(z)  # noqa: E731
-    ref = factored_problem(make, "0")
-    fac = factored_problem(make, "1")
+    ref = factored_problem(make, "0", graph)
+    fac = factored_problem(make, "1", graph)
     th = z["theta0"]
     ref.gradient(th)
     fac.gradient(th)
