@@ -632,7 +632,10 @@ ba_k_pcg(BADev d, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg
 
 // Diagnostic wrappers: the two passes of the two-pass operator as standalone
 // kernels (per-pass timing and roofline, ssfm_bench_operator).
-__global__ void __launch_bounds__(PCG_THREADS, 4) k_op_point(BADev d, const double* v, double* y) {
+#ifndef PTP_MINB
+#define PTP_MINB 4
+#endif
+__global__ void __launch_bounds__(PCG_THREADS, PTP_MINB) k_op_point(BADev d, const double* v, double* y) {
   __shared__ double smp[PCG_THREADS / 32][SSFM_BATCH][3];
   ba_point_pass<true>(d, v, y, smp);
 }

@@ -84,7 +84,10 @@ __global__ void k_g_init2(Dev d, CGGraphDev g, int nblk) {
 }
 
 // ---- body kernels (each returns at once when the solve is done)
-__global__ void __launch_bounds__(PCG_THREADS, 4) k_g_point(BADev d, CGGraphDev g) {
+#ifndef PTP_MINB
+#define PTP_MINB 4       // CTAs per SM of the graph point pass
+#endif
+__global__ void __launch_bounds__(PCG_THREADS, PTP_MINB) k_g_point(BADev d, CGGraphDev g) {
   if (*(volatile int*)(g.ic + 3)) return;
   __shared__ double smp[PCG_THREADS / 32][SSFM_BATCH][3];
   ba_point_pass<true>(d, g.p, d.yv, smp);   // p is constant during this kernel
