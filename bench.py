@@ -243,13 +243,13 @@ def run_b200(args, ws, rank, local):
     from paper_2510_13310_b200 import dist as bdist
 
     is_gp = args.config in GP_CONFIGS
-    gp_base = b2.fix_gauge(b2.make_rays(arr, depth_mode=False, loss=loss, seed=0)) if is_gp else None
+    gp_base = b2.fix_gauge(b2.make_rays_device(arr, depth_mode=False, loss=loss, seed=0)) if is_gp else None
 
     def make_problem(a=None):
         a = arr if a is None else a
         if is_gp:
             return bdist.ShardedGPProblem(gp_base, rank=rank, world=ws) if ws > 1 else \
-                b2.fix_gauge(b2.make_rays(a, depth_mode=False, loss=loss, seed=0))
+                b2.fix_gauge(b2.make_rays_device(a, depth_mode=False, loss=loss, seed=0))
         if ws > 1:
             return bdist.ShardedBAProblem(a, loss, rank=rank, world=ws)
         return b2.BAProblem(a, loss)

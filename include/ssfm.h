@@ -286,6 +286,13 @@ int ssfm_center_moments(const double* x, const double* y, int32_t n, double* out
 int ssfm_apply_sim3(const double* rot, const double* trans, double scale, const double* rq_conj, double* quats,
                     double* centers, int32_t C, double* points, int64_t P, void* stream);
 
+/* ssfm_make_rays: gp.make_rays (gp.py:150-177) input preparation on the device,
+ * bit-identical to numpy: rays [n][3] = normalize(R(q)^T ((u-cx)/f, (v-cy)/f, 1));
+ * with depths (or NULL), ray_depths [n] = depth * |dirs|. Device pointers;
+ * cam_idx int64 [n], pixels [n][2], pps [C][2], focals [C], quats [C][4]. */
+int ssfm_make_rays(int64_t n, const int64_t* cam_idx, const double* pixels, const double* pps, const double* focals,
+                   const double* quats, const double* depths, double* rays, double* ray_depths, void* stream);
+
 /* ---- BAL problem files (io.read_bal, io.py:83-131) ------------------------
  * Array-native host reader: ssfm_bal_read parses `path` (the reference's token,
  * error-message and line-number rules) and returns counts[3] = C, P, N;

@@ -26,7 +26,7 @@ EXPORTS = (
     "ssfm_bench_operator", "ssfm_reproj_stats", "ssfm_block_jtj", "ssfm_block_jtr",
     "ssfm_block_scale_diag", "ssfm_dense_scatter", "ssfm_dense_solve",
     "ssfm_rotation_auc", "ssfm_center_moments", "ssfm_apply_sim3",
-    "ssfm_bal_read", "ssfm_bal_take", "ssfm_bal_free",
+    "ssfm_bal_read", "ssfm_bal_take", "ssfm_bal_free", "ssfm_make_rays",
 )
 
 TERMINATIONS = {0: "max_iter", 1: "converged_cost", 2: "converged_grad", 3: "solver_failure"}
@@ -108,6 +108,7 @@ def load(required: bool = True):
     lib.ssfm_apply_sim3.argtypes = [P, P, D, P, P, P, I32, P, I64, P]
     lib.ssfm_bal_read.argtypes = [ct.c_char_p, ct.POINTER(P), P]
     lib.ssfm_bal_take.argtypes = [P, P, P, P, P, P]
+    lib.ssfm_make_rays.argtypes = [I64, P, P, P, P, P, P, P, P, P]
     lib.ssfm_bal_free.argtypes = [P]
     lib.ssfm_bal_free.restype = None
     for fn in EXPORTS:

@@ -163,3 +163,46 @@ __global__ void k_met_apply_cameras(Sim3Args a, double* __restrict__ quats, doub
   for (int k = 0; k < 4; ++k) q[k] = o[k] / n;
   met_sim3(a, centers + 3ll * c);
 }
+
+// make_rays (gp.py:150-177) per observation, in numpy's operation order
+// (explicit round-to-nearest, no contraction): bit-identical to the host
+// restatement. dirs = ((u - cx) / f, (v - cy) / f, 1); world = rotate_many(
+// conj(q), dirs) (scene.py:126-132); rays = world / |world|; ray depth =
+// depth * |dirs|.
+__global__ void k_make_rays(long long n, const long long* __restrict__ cam, const double* __restrict__ pix,
+                            const double* __restrict__ pps, const double* __restrict__ foc,
+                            const double* __restrict__ quats, const double* __restrict__ depths,
+                            double* __restrict__ rays, double* __restrict__ ray_depths) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long c = cam[i];
+  const double f = foc[c];
+  const double d0 = __ddiv_rn(__dsub_rn(pix[2 * i], pps[2 * c]), f);
+  const double d1 = __ddiv_rn(__dsub_rn(pix[2 * i + 1], pps[2 * c + 1]), f);
+  const double d2 = 1.0;
+  const double* q = quats + 4 * c;
+  double qn[4] = {q[0], -q[1], -q[2], -q[3]};
+  const double qq = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(qn[0], qn[0]), __dmul_rn(qn[1], qn[1])),
+                                        __dmul_rn(qn[2], qn[2])), __dmul_rn(qn[3], qn[3]));
+  const double qnorm = __dsqrt_rn(qq);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) qn[k] = __ddiv_rn(qn[k], qnorm);
+  const double u0 = qn[1], u1 = qn[2], u2 = qn[3];
+  const double t0 = __dsub_rn(__dmul_rn(u1, d2), __dmul_rn(u2, d1));
+  const double t1 = __dsub_rn(__dmul_rn(u2, d0), __dmul_rn(u0, d2));
+  const double t2 = __dsub_rn(__dmul_rn(u0, d1), __dmul_rn(u1, d0));
+  const double c0 = __dsub_rn(__dmul_rn(u1, t2), __dmul_rn(u2, t1));
+  const double c1 = __dsub_rn(__dmul_rn(u2, t0), __dmul_rn(u0, t2));
+  const double c2 = __dsub_rn(__dmul_rn(u0, t1), __dmul_rn(u1, t0));
+  const double w0 = __dadd_rn(d0, __dmul_rn(2.0, __dadd_rn(__dmul_rn(qn[0], t0), c0)));
+  const double w1 = __dadd_rn(d1, __dmul_rn(2.0, __dadd_rn(__dmul_rn(qn[0], t1), c1)));
+  const double w2 = __dadd_rn(d2, __dmul_rn(2.0, __dadd_rn(__dmul_rn(qn[0], t2), c2)));
+  const double wn = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(w0, w0), __dmul_rn(w1, w1)), __dmul_rn(w2, w2)));
+  rays[3 * i] = __ddiv_rn(w0, wn);
+  rays[3 * i + 1] = __ddiv_rn(w1, wn);
+  rays[3 * i + 2] = __ddiv_rn(w2, wn);
+  if (depths) {
+    const double dn = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2)));
+    ray_depths[i] = __dmul_rn(depths[i], dn);
+  }
+}

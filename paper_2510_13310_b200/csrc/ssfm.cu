@@ -1829,3 +1829,16 @@ extern "C" int ssfm_apply_sim3(const double* rot, const double* trans, double sc
   CU(cudaGetLastError());
   return SSFM_OK;
 }
+
+extern "C" int ssfm_make_rays(int64_t n, const int64_t* cam_idx, const double* pixels, const double* pps,
+                              const double* focals, const double* quats, const double* depths, double* rays,
+                              double* ray_depths, void* stream) {
+  if (n < 0) return set_err(SSFM_INVALID_ARGUMENT, "negative observation count");
+  if (n == 0) return SSFM_OK;
+  if (!cam_idx || !pixels || !pps || !focals || !quats || !rays || (depths && !ray_depths))
+    return set_err(SSFM_INVALID_ARGUMENT, "null argument");
+  k_make_rays<<<nblk(n, 256), 256, 0, (cudaStream_t)stream>>>(n, (const long long*)cam_idx, pixels, pps, focals,
+                                                              quats, depths, rays, ray_depths);
+  CU(cudaGetLastError());
+  return SSFM_OK;
+}

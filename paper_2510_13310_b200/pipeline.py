@@ -18,7 +18,7 @@ import numpy as np
 
 from . import _native
 from .ba import BAProblem
-from .gp import fix_gauge, make_rays
+from .gp import fix_gauge, make_rays_device
 from .lm import LMConfig, SolveReport, _stream, _torch, lm_solve
 from .scene import RobustLoss, SceneArrays, as_arrays
 
@@ -62,7 +62,7 @@ def run_global_sfm(scene, gp_loss: RobustLoss | None = None, ba_loss: RobustLoss
     arr = as_arrays(scene)
     gp_loss = gp_loss or RobustLoss("huber", 0.1)
     ba_loss = ba_loss or RobustLoss("huber", 1.0)
-    gp = fix_gauge(make_rays(arr, depth_mode=False, loss=gp_loss, seed=seed))
+    gp = fix_gauge(make_rays_device(arr, depth_mode=False, loss=gp_loss, seed=seed))
     th_gp, rep_gp = lm_solve(gp, gp.initial_theta(), gp_config or LMConfig(max_iterations=20))
     centers, points, _ = gp.views(th_gp)
     mid = arr.copy()

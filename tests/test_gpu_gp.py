@@ -210,3 +210,23 @@ def test_gp_pattern_export(gpu):
     pat = p.export_pattern()
     assert np.array_equal(pat["off_keys"], z["off_keys"])
     assert np.array_equal(pat["schur_slots"], z["schur_slots"])
+
+
+@pytest.mark.parametrize("depth", [False, True])
+def test_make_rays_device_bit_identical(gpu, depth):
+    """k_make_rays (numpy operation order, no contraction) vs the host
+    restatement and the reference's rays (gp_small golden)."""
+    z = golden("gp_small.npz")
+    arr = b2.SceneArrays(z["quats"], z["centers"], z["focals"], z["pps"], z["dists"], "pinhole",
+                         z["points"], z["cam"], z["pt"], z["pixels"], None)
+    if not depth:
+        assert np.array_equal(b2.make_rays_device(arr).rays, z["rays"])
+    _, obs = synth.generate_arrays(synth.SynthConfig(num_cameras=40, num_points=3000, visibility_fraction=0.2,
+                                                     pixel_noise_sigma=1.0, seed=4))
+    if depth:
+        obs.depths = np.random.default_rng(1).uniform(1.0, 9.0, size=obs.num_observations)
+    h = b2.make_rays(obs, depth_mode=depth)
+    d = b2.make_rays_device(obs, depth_mode=depth)
+    assert np.array_equal(h.rays, d.rays)
+    if depth:
+        assert np.array_equal(h.depths, d.depths)
