@@ -249,6 +249,58 @@ int ssfm_dense_scatter(const double* data, const int64_t* dst, const int64_t* sr
                        double* A, void* stream);
 int ssfm_dense_solve(double* A, const double* b, double* x, int64_t n, void* stream);
 
+/* ---- Schur PCG on an explicit BlockNormalSystem ---------------------------
+ * ssfm_schur_solve replaces _solve_schur (lm.py:537-704) for a damped system
+ * held in the reference's block storage (sparse_block.py:162-216: `data`,
+ * `gradient` = -J^T r). The plan is the integer schedule of _SchurPlan
+ * (lm.py:236-483), built once per pattern by the caller (generic._SchurXPlan):
+ * retained blocks (pose / focal / gp_center) form the reduced system, point
+ * blocks (point / gp_point, width 3) are eliminated, and scale blocks
+ * (gp_scale, width 1) are eliminated first. All pointers are device pointers.
+ * Returns SSFM_OK, SSFM_SINGULAR_BLOCK (masked scale / point direction with a
+ * non-zero gradient, det <= 0, singular preconditioner block, masked retained
+ * direction with a non-zero reduced gradient) or SSFM_CG_STALL. */
+typedef struct {
+  int64_t n_params, n_ret, n_rblk, n_pt, n_u, n_slots, n_sc, n_direct;
+  const int64_t* ret_s_off;   /* [n_rblk+1] reduced offset of each retained block */
+  const int64_t* ret_theta;   /* [n_ret] theta row of each reduced scalar */
+  const int64_t* pre_off;     /* [n_rblk+1] offset of each w x w preconditioner block */
+  const int64_t* direct_dst;  /* [n_direct] S[dst[k]] = data[src[k]] (row-major n_ret x n_ret) */
+  const int64_t* direct_src;
+  const int64_t* pt_diag;     /* [n_pt] data offset of the point's 3x3 diagonal block */
+  const int64_t* pt_theta;    /* [n_pt] theta row of the point's first scalar */
+  const int32_t* u_w;         /* [n_u] U entry (retained x point coupling): retained width */
+  const int32_t* u_ret;       /*        retained block (local index) */
+  const int32_t* u_pt;        /*        point (local index) */
+  const int64_t* u_off;       /* [n_u+1] offset in the U store (w x 3 row-major per entry) */
+  const int64_t* u_gather;    /* [u_off[n_u]] data index of every U scalar */
+  const int32_t* u_by_ret;    /* [n_u] entries grouped by retained block, entry order */
+  const int64_t* ret_useg;    /* [n_rblk+1] */
+  const int32_t* u_by_pt;     /* [n_u] entries grouped by point, entry order */
+  const int64_t* pt_useg;     /* [n_pt+1] */
+  const int64_t* slot_seg;    /* [n_slots+1] contribution segment of each S slot */
+  const int32_t* slot_ra;     /* [n_slots] retained blocks of the slot, ra <= rb */
+  const int32_t* slot_rb;
+  const int32_t* con_ua;      /* [slot_seg[n_slots]] U entries (a, b) of each contribution */
+  const int32_t* con_ub;
+  const int64_t* sc_diag;     /* [n_sc] data offset of the scale's 1x1 diagonal */
+  const int64_t* sc_theta;    /* [n_sc] theta row of the scale */
+  const int64_t* sc_uc;       /* [n_sc] data offset of the 3 retained-scale couplings */
+  const int64_t* sc_up;       /* [n_sc] data offset of the 3 point-scale couplings */
+  const int32_t* sc_c;        /* [n_sc] retained block (width 3) */
+  const int32_t* sc_p;        /* [n_sc] point */
+  const int32_t* sc_u;        /* [n_sc] U entry joining (sc_c, sc_p) */
+  const int32_t* sc_by_c;     /* scales grouped by retained block */
+  const int64_t* c_scseg;     /* [n_rblk+1] */
+  const int32_t* sc_by_p;     /* scales grouped by point */
+  const int64_t* p_scseg;     /* [n_pt+1] */
+  const int32_t* sc_by_u;     /* scales grouped by U entry */
+  const int64_t* u_scseg;     /* [n_u+1] */
+} ssfm_schur_plan;
+
+int ssfm_schur_solve(const ssfm_schur_plan* plan, const double* data, const double* gradient,
+                     const ssfm_lm_config* cfg, double* delta, int32_t* cg_iters_host, void* stream);
+
 /* Diagnostic (BA): number of Jacobian entries where the camera-major copy
  * (written by the camera-tile linearize pass) differs bitwise from the
  * point-major copy, after ssfm_linearize. Expected 0. */

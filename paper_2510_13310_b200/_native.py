@@ -26,7 +26,7 @@ EXPORTS = (
     "ssfm_bench_operator", "ssfm_reproj_stats", "ssfm_block_jtj", "ssfm_block_jtr",
     "ssfm_block_scale_diag", "ssfm_dense_scatter", "ssfm_dense_solve",
     "ssfm_rotation_auc", "ssfm_center_moments", "ssfm_apply_sim3",
-    "ssfm_bal_read", "ssfm_bal_take", "ssfm_bal_free", "ssfm_make_rays",
+    "ssfm_bal_read", "ssfm_bal_take", "ssfm_bal_free", "ssfm_make_rays", "ssfm_schur_solve",
 )
 
 TERMINATIONS = {0: "max_iter", 1: "converged_cost", 2: "converged_grad", 3: "solver_failure"}
@@ -72,6 +72,23 @@ class GPDescC(ct.Structure):
     ]
 
 
+# ssfm_schur_plan (include/ssfm.h): sizes, then device pointers in header order
+SCHUR_PLAN_SIZES = ("n_params", "n_ret", "n_rblk", "n_pt", "n_u", "n_slots", "n_sc", "n_direct")
+SCHUR_PLAN_ARRAYS = (
+    ("ret_s_off", "i8"), ("ret_theta", "i8"), ("pre_off", "i8"), ("direct_dst", "i8"), ("direct_src", "i8"),
+    ("pt_diag", "i8"), ("pt_theta", "i8"), ("u_w", "i4"), ("u_ret", "i4"), ("u_pt", "i4"), ("u_off", "i8"),
+    ("u_gather", "i8"), ("u_by_ret", "i4"), ("ret_useg", "i8"), ("u_by_pt", "i4"), ("pt_useg", "i8"),
+    ("slot_seg", "i8"), ("slot_ra", "i4"), ("slot_rb", "i4"), ("con_ua", "i4"), ("con_ub", "i4"),
+    ("sc_diag", "i8"), ("sc_theta", "i8"), ("sc_uc", "i8"), ("sc_up", "i8"), ("sc_c", "i4"), ("sc_p", "i4"),
+    ("sc_u", "i4"), ("sc_by_c", "i4"), ("c_scseg", "i8"), ("sc_by_p", "i4"), ("p_scseg", "i8"),
+    ("sc_by_u", "i4"), ("u_scseg", "i8"),
+)
+
+
+class SchurPlanC(ct.Structure):
+    _fields_ = [(n, ct.c_int64) for n in SCHUR_PLAN_SIZES] + [(n, ct.c_void_p) for n, _ in SCHUR_PLAN_ARRAYS]
+
+
 _lib = None
 
 
@@ -110,6 +127,7 @@ def load(required: bool = True):
     lib.ssfm_bal_take.argtypes = [P, P, P, P, P, P]
     lib.ssfm_make_rays.argtypes = [I64, P, P, P, P, P, P, P, P, P]
     lib.ssfm_bal_free.argtypes = [P]
+    lib.ssfm_schur_solve.argtypes = [ct.POINTER(SchurPlanC), P, P, ct.POINTER(LMConfigC), P, ct.POINTER(I32), P]
     lib.ssfm_bal_free.restype = None
     for fn in EXPORTS:
         if fn not in ("ssfm_last_error", "ssfm_version", "ssfm_num_params", "ssfm_num_residuals",

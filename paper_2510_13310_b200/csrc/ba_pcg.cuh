@@ -564,11 +564,11 @@ ba_k_pcg(BADev d, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg
           }
         }
         block_reduce<1>(v, smred);
-        if (threadIdx.x == 0) part[2ll * blockIdx.x] = v[0];
+        if (threadIdx.x == 0) part[2ll * NP + blockIdx.x] = v[0];
       }
       grid.sync();
       if (tim) { const unsigned long long t1 = gtimer(); ph[2] += t1 - pt0; pt0 = t1; }
-      double pq = cta_partials_sum(part, NP, 2, 0, &smb[0]);
+      double pq = cta_partials_sum(part + 2ll * NP, NP, 1, 0, &smb[0]);
       if (shared) {   // every CTA sums the cameras' shares in the same order
         qf = (d.pinned[0] >> 7 & 1) ? pf : cta_partials_sum(d.fterm, d.bp.C, 1, 0, &smb[2]);
         pq += pf * qf;

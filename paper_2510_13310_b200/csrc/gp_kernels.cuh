@@ -811,10 +811,10 @@ gp_k_pcg(GPDev g, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg
           }
         }
         block_reduce<1>(v, smred);
-        if (threadIdx.x == 0) part[2ll * blockIdx.x] = v[0];
+        if (threadIdx.x == 0) part[2ll * NP + blockIdx.x] = v[0];
       }
       grid.sync();
-      const double pq = cta_partials_sum(part, NP, 2, 0, &smb[0]);
+      const double pq = cta_partials_sum(part + 2ll * NP, NP, 1, 0, &smb[0]);
       if (!isfinite(pq) || pq <= 0.0) { flag = ST_CG_BREAKDOWN; break; }
       const double alpha = rho / pq;
       {

@@ -12,6 +12,8 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <algorithm>
+#include <initializer_list>
 #include <map>
 #include <mutex>
 #include <string>
@@ -25,6 +27,7 @@
 #include "pattern.cuh"
 #include "block_algebra.cuh"
 #include "dense.cuh"
+#include "schur_explicit.cuh"
 #include "metrics.cuh"
 
 static thread_local std::string g_last_error;
@@ -594,7 +597,7 @@ extern "C" int ssfm_create_ba(const ssfm_ba_desc* desc, void* stream, ssfm_handl
   h->cam_blocks = nblk(C, 256);
   h->red_n = std::max<long long>(h->cost_blocks, (long long)h->lin_blocks * 8 + h->cam_blocks);
   if ((rc = dalloc(h, &h->red, h->red_n))) return fail(rc);
-  if ((rc = dalloc(h, &h->part, 2ll * h->pcg_grid + 2))) return fail(rc);
+  if ((rc = dalloc(h, &h->part, 3ll * h->pcg_grid + 2))) return fail(rc);
   d.partials = h->red;
   if (cudaMemsetAsync(h->misc, 0, sizeof(Misc), st) || cudaStreamSynchronize(st))
     return fail(set_err(SSFM_CUDA_ERROR, "init"));
@@ -682,7 +685,7 @@ extern "C" int ssfm_create_gp(const ssfm_gp_desc* desc, void* stream, ssfm_handl
   h->cam_blocks = nblk(C, 256);
   h->red_n = std::max<long long>(h->cost_blocks, (long long)h->lin_blocks * 8 + h->cam_blocks + nblk(N, 256));
   if ((rc = dalloc(h, &h->red, h->red_n))) return fail(rc);
-  if ((rc = dalloc(h, &h->part, 2ll * h->pcg_grid + 2))) return fail(rc);
+  if ((rc = dalloc(h, &h->part, 3ll * h->pcg_grid + 2))) return fail(rc);
   g.partials = h->red;
   if (cudaMemsetAsync(h->misc, 0, sizeof(Misc), st) || cudaStreamSynchronize(st))
     return fail(set_err(SSFM_CUDA_ERROR, "init"));
@@ -1685,6 +1688,110 @@ extern "C" int ssfm_block_scale_diag(double* data, const int64_t* diag_idx, int6
   k_block_scale_diag<<<nblk(n, 256), 256, 0, (cudaStream_t)stream>>>(data, (const long long*)diag_idx, n, factor);
   CU(cudaGetLastError());
   return SSFM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Schur PCG on an explicit block normal system (schur_explicit.cuh)
+// ---------------------------------------------------------------------------
+extern "C" int ssfm_schur_solve(const ssfm_schur_plan* plan, const double* data, const double* gradient,
+                                const ssfm_lm_config* cfg, double* delta, int32_t* cg_iters_host, void* stream) {
+  if (!plan || !data || !gradient || !cfg || !delta) return set_err(SSFM_INVALID_ARGUMENT, "null argument");
+  const XsPlan& pl = *plan;
+  if (pl.n_params <= 0 || pl.n_ret < 0 || pl.n_pt < 0 || pl.n_u < 0 || pl.n_sc < 0)
+    return set_err(SSFM_INVALID_ARGUMENT, "bad plan sizes");
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long n = pl.n_ret;
+  long long nu_sc = 0, npre = 0;
+  if (pl.n_u) CU(cudaMemcpyAsync(&nu_sc, pl.u_off + pl.n_u, sizeof(long long), cudaMemcpyDeviceToHost, st));
+  if (pl.n_rblk) CU(cudaMemcpyAsync(&npre, pl.pre_off + pl.n_rblk, sizeof(long long), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  // one stream-ordered scratch block: S | U | dpt | M | y | g | bred x r z p q | prec | ctl + status
+  const long long nd = n * n + nu_sc + 9 * pl.n_pt * 2 + 3 * pl.n_pt + pl.n_params + 6 * n + npre + 8;
+  double* base = nullptr;
+  CU(cudaMallocAsync((void**)&base, sizeof(double) * nd, st));
+  XsWork w{};
+  double* c = base;
+  w.S = c; c += n * n;
+  w.U = c; c += nu_sc;
+  w.dpt = c; c += 9 * pl.n_pt;
+  w.M = c; c += 9 * pl.n_pt;
+  w.y = c; c += 3 * pl.n_pt;
+  w.g = c; c += pl.n_params;
+  w.bred = c; c += n;
+  w.x = c; c += n;
+  w.r = c; c += n;
+  w.z = c; c += n;
+  w.p = c; c += n;
+  w.q = c; c += n;
+  w.prec = c; c += npre;
+  w.ctl = (XsWork::Ctl*)c;
+  w.status = (int*)(c + 6);
+  int rc = SSFM_OK;
+  auto finish = [&](int code) {
+    cudaFreeAsync(base, st);
+    return code;
+  };
+  if (cudaMemsetAsync(w.S, 0, sizeof(double) * n * n, st) || cudaMemsetAsync(c, 0, sizeof(double) * 8, st))
+    return finish(set_err(SSFM_CUDA_ERROR, "memset"));
+  const int T = 256;
+  const long long big = std::max(std::max<long long>(pl.n_direct, nu_sc), std::max<long long>(9 * pl.n_pt, std::max<long long>(pl.n_params, 1)));
+  k_xs_init<<<(int)std::min<long long>(nblk(big, T), 148 * 16), T, 0, st>>>(pl, data, gradient, w);
+  if (pl.n_sc) {
+    k_xs_sc_check<<<nblk(pl.n_sc, T), T, 0, st>>>(pl, data, gradient, w);
+    if (pl.n_rblk) k_xs_sc_cam<<<nblk(pl.n_rblk, T), T, 0, st>>>(pl, data, gradient, w);
+    if (pl.n_pt) k_xs_sc_pt<<<nblk(pl.n_pt, T), T, 0, st>>>(pl, data, gradient, w);
+    if (pl.n_u) k_xs_sc_u<<<nblk(pl.n_u, T), T, 0, st>>>(pl, data, w);
+  }
+  if (pl.n_pt) k_xs_ptinv<<<nblk(pl.n_pt, T), T, 0, st>>>(pl, w);
+  if (pl.n_rblk) k_xs_bred<<<nblk(pl.n_rblk, T), T, 0, st>>>(pl, w);
+  if (pl.n_slots) k_xs_fill<<<nblk(32 * pl.n_slots, T), T, 0, st>>>(pl, w);
+  if (n) k_xs_pin<<<nblk(n, T), T, 0, st>>>(pl, w);
+  if (pl.n_rblk) k_xs_prec<<<nblk(pl.n_rblk, 64), 64, 0, st>>>(pl, w);
+  int status = 0;
+  if (cudaGetLastError() != cudaSuccess) return finish(set_err(SSFM_CUDA_ERROR, "schur setup launch failed"));
+  if (cudaMemcpyAsync(&status, w.status, sizeof(int), cudaMemcpyDeviceToHost, st) || cudaStreamSynchronize(st))
+    return finish(set_err(SSFM_CUDA_ERROR, "schur setup failed"));
+  // the reference raises in this order (lm.py:569-575, 503-512, 631-633, 520-525)
+  if (status & ST_PIN_SCALE) return finish(set_err(SSFM_SINGULAR_BLOCK, "masked scale with non-zero coupling"));
+  if (status & ST_PIN_POINT)
+    return finish(set_err(SSFM_SINGULAR_BLOCK, "masked point direction with non-zero gradient"));
+  if (status & ST_SINGULAR_POINT)
+    return finish(set_err(SSFM_SINGULAR_BLOCK, "eliminable block singular after damping (det <= 0)"));
+  if (status & ST_PIN_RETAINED)
+    return finish(set_err(SSFM_SINGULAR_BLOCK, "masked retained direction with non-zero gradient"));
+  if (status & ST_SINGULAR_PRECOND)
+    return finish(set_err(SSFM_SINGULAR_BLOCK, "singular preconditioner block"));
+  // PCG: the iterations are enqueued in chunks; a finished solve turns the
+  // remaining kernels of the chunk into no-ops, so the count is exact
+  k_xs_cg_start<<<1, 1024, 0, st>>>(pl, w, gradient, cfg->cg_tol, cfg->cg_max_iters);
+  XsWork::Ctl hc{};
+  const int chunk = 16;
+  const int mv_blocks = nblk(32 * std::max<long long>(n, 1), T);
+  for (;;) {
+    if (cudaMemcpyAsync(&hc, w.ctl, sizeof(hc), cudaMemcpyDeviceToHost, st) || cudaStreamSynchronize(st))
+      return finish(set_err(SSFM_CUDA_ERROR, "schur PCG failed"));
+    if (hc.done) break;
+    for (int k = 0; k < chunk; ++k) {
+      k_xs_matvec<<<mv_blocks, T, 0, st>>>(pl, w);
+      k_xs_cg_step<<<1, 1024, 0, st>>>(pl, w);
+    }
+    if (cudaGetLastError() != cudaSuccess) return finish(set_err(SSFM_CUDA_ERROR, "schur PCG launch failed"));
+  }
+  if (cg_iters_host) *cg_iters_host = hc.iters;
+  char msg[160];
+  if (hc.done == 2) {
+    snprintf(msg, sizeof msg, "CG did not reach tolerance in %d iterations (|r| %.3e, tol %.3e)", hc.cg_max, hc.rn,
+             hc.tol);
+    return finish(set_err(SSFM_CG_STALL, msg));
+  }
+  if (hc.done == 3) return finish(set_err(SSFM_CG_STALL, "CG broke down (p.q <= 0 or non-finite)"));
+  k_xs_back_zero<<<(int)std::min<long long>(nblk(pl.n_params, T), 148 * 8), T, 0, st>>>(pl, delta);
+  if (n) k_xs_back_x<<<nblk(n, T), T, 0, st>>>(pl, w, delta);
+  if (pl.n_pt) k_xs_back_pt<<<nblk(pl.n_pt, T), T, 0, st>>>(pl, w, delta);
+  if (pl.n_sc) k_xs_back_sc<<<nblk(pl.n_sc, T), T, 0, st>>>(pl, data, gradient, delta);
+  if (cudaGetLastError() != cudaSuccess) return finish(set_err(SSFM_CUDA_ERROR, "schur back-substitution failed"));
+  rc = finish(SSFM_OK);
+  return rc;
 }
 
 extern "C" int ssfm_dense_scatter(const double* data, const int64_t* dst, const int64_t* src, int64_t m,
