@@ -44,7 +44,7 @@ sys.path.insert(0, ROOT)
 CONFIGS = {
     # name: (cameras, points, visibility k, sigma, loss delta, workload label)
     "c1": (50, 5000, 4, 1.0, 1.0, "synthetic BA 50 cams / 5k pts / 20k obs (C1)"),
-    "c3": (1700, 150000, 5, 1.0, 1.0, "synthetic BA 1.7k cams / 150k pts / 750k obs (C3 shape)"),
+    "c3": (1700, 150000, 5, 1.0, 1.0, "synthetic BA 1.7k cams / 150k pts / 680k obs (C3, BAL Ladybug shape)"),
     "c4ba": (1000, 500000, 8, 1.0, 1.0, "synthetic BA 1k cams / 500k pts / 4M obs (C4 BA stage)"),
     "c5": (5000, 2000000, 10, 1.0, 1.0, "synthetic large-scale BA 5000 cams / 2M pts / 20M obs (C5)"),
     # global positioning (gp.py): rays from the observed scene, Huber 0.1, seeded init
@@ -55,8 +55,14 @@ GP_CONFIGS = {"c2gp", "c4gp"}
 # C4: the GP -> BA global SfM stage: GP 20 iterations (Huber 0.1)
 # on the observed sigma=1 scene, then BA 10 iterations (Huber 1.0) on its output
 PIPELINE = {"c4": (1000, 500000, 8, 1.0, "synthetic GP+BA global SfM 1k cams / 500k pts / 4M obs (C4)")}
-# bounded CPU sample of the C5 shape for the reference (same k = 10 views per point)
-REF_SAMPLE = (1000, 40000, 10)
+# bounded CPU samples of the C5 shape for the reference, at C5's camera count
+# (same k = 10 views per point): the reference's dense reduced camera system
+# (40,000^2 at 5000 cameras) makes one LM iteration cost tens of seconds on the
+# host whatever the point count, so the point count is what is bounded
+REF_SAMPLE = (5000, 100000, 10)           # --impl reference, config c5
+CPU_BASELINE_SAMPLE = (5000, 20000, 10)   # cpu_baseline leg of the b200 line
+# C3: points >= 80,000 lose their highest-camera observation
+C3_TRIM = 80000
 METRIC = "BA/GP LM iteration time and observations/sec at 1/2/4/8 B200 vs CPU ref"
 
 
@@ -132,13 +138,52 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # workload
 # ---------------------------------------------------------------------------
-def make_arrays(cams, pts, k, sigma, seed=0):
+def make_arrays(cams, pts, k, sigma, seed=0, trim=None):
     from paper_2510_13310_b200 import synth
     cfg = synth.SynthConfig(num_cameras=cams, num_points=pts, visibility_fraction=k / cams,
                             pixel_noise_sigma=sigma, seed=seed)
     _, observed = synth.generate_arrays(cfg)
-    return synth.perturb_arrays(observed, rot_deg=1.0, center_frac=0.01, focal_frac=0.02,
-                                point_frac=0.005, seed=1)
+    arr = synth.perturb_arrays(observed, rot_deg=1.0, center_frac=0.01, focal_frac=0.02,
+                               point_frac=0.005, seed=1)
+    return synth.trim_points_arrays(arr, trim) if trim is not None else arr
+
+
+def host_info():
+    """CPU model, threads and RAM of this host"""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    ram = None
+    try:
+        with open("/proc/meminfo") as fh:
+            for ln in fh:
+                if ln.startswith("MemTotal"):
+                    ram = round(int(ln.split()[1]) / 2**20, 1)
+                    break
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count()
+    return {"cpu_model": model, "threads": usable, "ram_gib": ram}
+
+
+def profiled_traffic(config):
+    """DRAM bytes per CG iteration of the PCG solve from the committed ncu
+    capture of this config (profiles/traffic_<config>.json), or None"""
+    try:
+        with open(os.path.join(ROOT, "profiles", f"traffic_{config}.json")) as fh:
+            d = json.load(fh)
+        return d
+    except (OSError, ValueError):
+        return None
 
 
 def next_lambda(cfg, rec):
@@ -226,7 +271,7 @@ def run_b200(args, ws, rank, local):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cams, pts, k, sigma, delta, label = CONFIGS[args.config]
     t0 = time.time()
-    arr = make_arrays(cams, pts, k, sigma)
+    arr = make_arrays(cams, pts, k, sigma, trim=C3_TRIM if args.config == "c3" else None)
     N, P, C = arr.num_observations, arr.num_points, arr.num_cameras
     log(f"[rank {rank}] generated {label}: N={N} in {time.time() - t0:.1f}s")
     loss = b2.RobustLoss("huber", delta)
@@ -341,6 +386,14 @@ def run_b200(args, ws, rank, local):
                 "kernel_ms": round(pms.value, 3),
                 "algorithmic_bytes_per_cg_iter": bytes_per_cg,
                 "kernel_share_of_step": round(pms.value / max(ms_total, 1e-9), 4)}
+        prof = profiled_traffic(args.config) if ws == 1 else None
+        if prof is not None:
+            # ncu dram__bytes_read.sum + dram__bytes_write.sum of the PCG's
+            # kernels per CG iteration (profiles/traffic_<config>.json)
+            roof["traffic"] = prof["dram_bytes_per_cg_iter"]
+            roof["traffic_unit"] = "bytes per CG iteration (ncu, all PCG kernels)"
+            roof["traffic_over_algorithmic"] = round(prof["dram_bytes_per_cg_iter"] / bytes_per_cg, 3)
+            roof["traffic_source"] = prof.get("source")
         if not is_gp and sum(phase_sum) > 0:
             names = ["point_or_fused_pass", "camera_pass", "q_and_pq", "x_r_z_update", "p_update"]
             roof["phase_ms_per_cg_iter"] = {n: round(v / cgit.value, 4) for n, v in zip(names, phase_sum)}
@@ -350,10 +403,6 @@ def run_b200(args, ws, rank, local):
     e2e = None
     if not args.no_e2e:
         theta_host = theta_start(problem)
-        if ws == 1 and hasattr(problem, "release"):
-            # the device-timed handle is done: its device blocks go back to the
-            # library's block cache, as in an application solving problems in turn
-            problem.release()
         # the per-observation inputs live in pinned host memory (staged before
         # the timed region, as an application feeding the solver would)
         def pinned(x):
@@ -365,36 +414,56 @@ def run_b200(args, ws, rank, local):
                                                              pinned(np.asarray(arr.pt_idx)),
                                                              pinned(np.asarray(arr.pixels)))
         theta_host = pinned(np.asarray(theta_host))
-        barrier()
-        t_a = time.perf_counter()
-        e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e_a.record(stream)
-        p2 = make_problem(arr_host)
-        t_c = time.perf_counter()
-        th_out, rep_e = b2.lm_solve(p2, theta_host, b2.LMConfig(max_iterations=args.warmup + args.steps))
-        t_s = time.perf_counter()
-        e_b.record(stream)
-        barrier()
-        wall = time.perf_counter() - t_a
-        e_ms = e_a.elapsed_time(e_b)
-        log(f"[rank {rank}] e2e: problem {1e3 * (t_c - t_a):.0f} ms, lm_solve {1e3 * (t_s - t_c):.0f} ms "
-            f"({len(rep_e.iterations)} its, device {sum(i.device_ms for i in rep_e.iterations):.0f} ms)")
-        its = max(len(rep_e.iterations), 1)
-        if dist is not None:
-            t = torch.tensor([wall], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            wall = float(t.item())
-        # bytes moved host -> device: the per-observation inputs as stored on the
-        # host (indices narrowed to int32 on the device), camera intrinsics, theta
-        h2d = (Nl * (np.asarray(arr_host.cam_idx).itemsize + np.asarray(arr_host.pt_idx).itemsize
-                     + (24 if is_gp else 16)) + C * (16 + 16 + 8) + theta_host.nbytes)
-        e2e = {"value": N * its / wall, "unit": "obs/s",
-               "first_iteration_ms": round(rep_e.iterations[0].device_ms, 3) if rep_e.iterations else None,
-               "time_to_solution_s": round(wall, 3),
-               "h2d_bytes_per_step": int(h2d / its), "d2h_bytes_per_step": int(theta_host.nbytes / its),
-               "iterations": its, "wall_s": round(wall, 3), "device_ms": round(e_ms, 1),
-               "termination": rep_e.termination}
+
+        def one_e2e(tag):
+            barrier()
+            t_a = time.perf_counter()
+            e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e_a.record(stream)
+            p2 = make_problem(arr_host)
+            t_c = time.perf_counter()
+            th_out, rep_e = b2.lm_solve(p2, theta_host, b2.LMConfig(max_iterations=args.warmup + args.steps))
+            t_s = time.perf_counter()
+            e_b.record(stream)
+            barrier()
+            wall = time.perf_counter() - t_a
+            e_ms = e_a.elapsed_time(e_b)
+            log(f"[rank {rank}] e2e ({tag}): problem + handle {1e3 * (t_c - t_a):.0f} ms, lm_solve "
+                f"{1e3 * (t_s - t_c):.0f} ms ({len(rep_e.iterations)} its, device "
+                f"{sum(i.device_ms for i in rep_e.iterations):.0f} ms)")
+            its = max(len(rep_e.iterations), 1)
+            if dist is not None:
+                t = torch.tensor([wall], device="cuda")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                wall = float(t.item())
+            # bytes moved host -> device: the per-observation inputs as stored on
+            # the host (indices narrowed to int32 on the device), camera
+            # intrinsics, theta; device -> host: theta
+            h2d = (Nl * (np.asarray(arr_host.cam_idx).itemsize + np.asarray(arr_host.pt_idx).itemsize
+                         + (24 if is_gp else 16)) + C * (16 + 16 + 8) + theta_host.nbytes)
+            out = {"value": N * its / wall, "unit": "obs/s",
+                   "first_iteration_ms": round(rep_e.iterations[0].device_ms, 3) if rep_e.iterations else None,
+                   "time_to_solution_s": round(wall, 3), "setup_ms": round(1e3 * (t_c - t_a), 1),
+                   "h2d_bytes_per_step": int(h2d / its), "d2h_bytes_per_step": int(theta_host.nbytes / its),
+                   "iterations": its, "wall_s": round(wall, 3), "device_ms": round(e_ms, 1),
+                   "termination": rep_e.termination}
+            return out, p2
+
+        # cold: the device-timed handle is destroyed and the library's block
+        # cache emptied, so problem creation allocates HBM from scratch (an
+        # application's first solve). warm: the same solve again after that
+        # handle is released into the cache (an application solving problems of
+        # one shape in turn: creation skips cudaMalloc)
+        if ws == 1 and hasattr(problem, "release"):
+            problem.release(trim=True)
+        e2e, p2 = one_e2e("cold")
+        if ws == 1 and hasattr(p2, "release"):
+            p2.release()
         del p2
+        warm, p3 = one_e2e("warm")
+        del p3
+        e2e["cache"] = "cold (no reused device blocks)"
+        e2e["warm"] = {k: warm[k] for k in ("value", "time_to_solution_s", "setup_ms", "device_ms")}
     result = {
         "metric": METRIC, "value": value, "unit": "obs/s", "n_gpus": ws, "steps": steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -414,7 +483,7 @@ def run_b200(args, ws, rank, local):
         "roofline": roof, "e2e": e2e, "clocks": clocks, "gpu_launches": int(launches.value),
     }
     if rank == 0 and not args.no_cpu_baseline and not is_gp:
-        result["cpu_baseline"] = cpu_baseline_sample(max_iterations=4)
+        result["cpu_baseline"] = cpu_baseline_sample(max_iterations=2)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
@@ -437,13 +506,15 @@ def _import_reference():
     return sparsesfm, None
 
 
-def cpu_baseline_sample(max_iterations=4):
-    """Bounded sample: the reference on a C5-shaped reduction (k = 10)."""
+def cpu_baseline_sample(max_iterations=2):
+    """Bounded sample: the reference on a C5-shaped reduction at C5's camera
+    count (k = 10); value from the iterations after the first (which includes
+    the pattern build)."""
     ref, why = _import_reference()
     if ref is None:
         return {"value": None, "unit": "obs/s", "cores": 0, "kind": "reference", "sample": why}
     from sparsesfm import synth_metrics as rsm
-    cams, pts, k = REF_SAMPLE
+    cams, pts, k = CPU_BASELINE_SAMPLE
     truth, obs = rsm.generate(rsm.SynthConfig(num_cameras=cams, num_points=pts,
                                               visibility_fraction=k / cams, pixel_noise_sigma=1.0, seed=0))
     start = rsm.perturb(obs, rot_deg=1.0, center_frac=0.01, focal_frac=0.02, point_frac=0.005, seed=1)
@@ -461,7 +532,7 @@ def cpu_baseline_sample(max_iterations=4):
                       f"(C5 shape, k={k}), {len(its)} LM iterations, median of iterations 2..n "
                       f"({med:.2f} s/iter; first {its[0].wall_time_ns / 1e9:.2f} s incl. pattern build); "
                       f"total {wall:.1f} s",
-            "s_per_iter_median": med}
+            "s_per_iter_median": med, "host": host_info()}
 
 
 def run_reference(args, ws, rank):
@@ -489,6 +560,13 @@ def run_reference(args, ws, rank):
         n = obs.num_observations
     else:
         start = rsm.perturb(obs, rot_deg=1.0, center_frac=0.01, focal_frac=0.02, point_frac=0.005, seed=1)
+        if args.config == "c3":     # the same trimmed 680k-observation recipe as the b200 arm
+            top = {}
+            for o in start.observations:
+                top[o.point_id] = max(top.get(o.point_id, -1), o.camera_id)
+            start = ref.Scene(start.cameras, start.points,
+                              [o for o in start.observations
+                               if not (o.point_id >= C3_TRIM and o.camera_id == top[o.point_id])])
         prob = ref.BAProblem(start, ref.RobustLoss("huber", delta))
         th0 = prob.encode()
         n = start.num_observations
@@ -512,7 +590,8 @@ def run_reference(args, ws, rank):
                        "sample_observations": n},
             "impl": "reference",
             "cpu_baseline": {"value": value, "unit": "obs/s", "cores": cores, "kind": "reference",
-                             "sample": sample},
+                             "sample": sample, "host": host_info(),
+                             "s_per_iter": [round(i.wall_time_ns / 1e9, 3) for i in its]},
             "e2e": {"value": value, "unit": "obs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "termination": rep.termination}
 

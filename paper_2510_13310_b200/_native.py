@@ -27,6 +27,7 @@ EXPORTS = (
     "ssfm_block_scale_diag", "ssfm_dense_scatter", "ssfm_dense_solve",
     "ssfm_rotation_auc", "ssfm_center_moments", "ssfm_apply_sim3",
     "ssfm_bal_read", "ssfm_bal_take", "ssfm_bal_free", "ssfm_make_rays", "ssfm_schur_solve",
+    "ssfm_trim_cache", "ssfm_cache_bytes",
 )
 
 TERMINATIONS = {0: "max_iter", 1: "converged_cost", 2: "converged_grad", 3: "solver_failure"}
@@ -127,11 +128,14 @@ def load(required: bool = True):
     lib.ssfm_bal_take.argtypes = [P, P, P, P, P, P]
     lib.ssfm_make_rays.argtypes = [I64, P, P, P, P, P, P, P, P, P]
     lib.ssfm_bal_free.argtypes = [P]
+    lib.ssfm_trim_cache.argtypes = [I32, ct.POINTER(I64)]
+    lib.ssfm_cache_bytes.argtypes = []
+    lib.ssfm_cache_bytes.restype = I64
     lib.ssfm_schur_solve.argtypes = [ct.POINTER(SchurPlanC), P, P, ct.POINTER(LMConfigC), P, ct.POINTER(I32), P]
     lib.ssfm_bal_free.restype = None
     for fn in EXPORTS:
         if fn not in ("ssfm_last_error", "ssfm_version", "ssfm_num_params", "ssfm_num_residuals",
-                      "ssfm_device_bytes", "ssfm_bal_free"):
+                      "ssfm_device_bytes", "ssfm_bal_free", "ssfm_cache_bytes"):
             getattr(lib, fn).restype = ct.c_int
     _lib = lib
     return lib
@@ -148,6 +152,17 @@ def lm_config_c(cfg) -> LMConfigC:
                      float(cfg.lambda_down), float(cfg.lambda_min), float(cfg.lambda_max),
                      float(cfg.rel_cost_tol), float(cfg.grad_tol), int(cfg.cg_max_iters),
                      float(cfg.cg_tol))
+
+
+def trim_cache(device: int = -1) -> int:
+    """Free the device blocks that destroyed handles left in the library's
+    reuse cache (ssfm_trim_cache); returns the bytes freed."""
+    lib = load(required=False)
+    if lib is None:
+        return 0
+    freed = ct.c_int64(0)
+    check(lib.ssfm_trim_cache(int(device), ct.byref(freed)))
+    return int(freed.value)
 
 
 class Handle:

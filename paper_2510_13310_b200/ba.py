@@ -109,14 +109,18 @@ class _DeviceProblem:
             self._jac = BlockSparseJacobian.allocate(self.layout, self._res_ids(), self._param_ids())
         return self._jac
 
-    def release(self) -> None:
-        """Free the device arena now (instead of at garbage collection), e.g.
-        between the GP and BA stages of the pipeline."""
+    def release(self, trim: bool = False) -> None:
+        """Destroy the device handle now (instead of at garbage collection).
+        Its device blocks go to the library's reuse cache (ssfm_destroy), so
+        the next problem of the same shape skips cudaMalloc; trim=True returns
+        them to the CUDA allocator instead (also: _native.trim_cache())."""
         h = self._native_ptr
         self._native_ptr = None
         if h is not None and h.ptr:
             _native.load().ssfm_destroy(ct.c_void_p(h.ptr))
             h.ptr = 0
+        if trim:
+            _native.trim_cache()
 
     def device_bytes(self) -> int:
         return int(_native.load().ssfm_device_bytes(ct.c_void_p(self._native_handle().ptr)))

@@ -126,9 +126,31 @@ static BlockCache& block_cache() {
   static BlockCache c;
   return c;
 }
+// cap: SSFM_BLOCK_CACHE_GB, else a quarter of the device's HBM
 static size_t block_cache_cap() {
   const char* e = getenv("SSFM_BLOCK_CACHE_GB");
-  return (size_t)((e ? atof(e) : 48.0) * (double)(1ull << 30));
+  if (e) return (size_t)(atof(e) * (double)(1ull << 30));
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return 0;
+  return tot / 4;
+}
+
+// free the cached blocks of `device` (-1: every device); returns bytes freed
+static size_t block_cache_trim(int device) {
+  BlockCache& bc = block_cache();
+  std::lock_guard<std::mutex> lk(bc.mu);
+  size_t freed = 0;
+  for (auto it = bc.free_blocks.begin(); it != bc.free_blocks.end();) {
+    if (device < 0 || it->first.first == device) {
+      cudaFree(it->second);
+      freed += it->first.second;
+      bc.bytes -= it->first.second;
+      it = bc.free_blocks.erase(it);
+    } else {
+      ++it;
+    }
+  }
+  return freed;
 }
 
 template <typename T>
@@ -148,6 +170,10 @@ static int dalloc(ssfm_handle* h, T** ptr, size_t count) {
   }
   if (!p) {
     cudaError_t e = cudaMalloc(&p, b);
+    if (e == cudaErrorMemoryAllocation && block_cache_trim(h->device) > 0) {
+      cudaGetLastError();   // clear the failed allocation, retry with the cache released
+      e = cudaMalloc(&p, b);
+    }
     if (e != cudaSuccess)
       return set_err(SSFM_CUDA_ERROR, std::string("cudaMalloc: ") + cudaGetErrorString(e));
   }
@@ -1693,6 +1719,18 @@ extern "C" int ssfm_block_scale_diag(double* data, const int64_t* diag_idx, int6
 // ---------------------------------------------------------------------------
 // Schur PCG on an explicit block normal system (schur_explicit.cuh)
 // ---------------------------------------------------------------------------
+extern "C" int ssfm_trim_cache(int32_t device, int64_t* freed_bytes) {
+  const size_t f = block_cache_trim(device);
+  if (freed_bytes) *freed_bytes = (int64_t)f;
+  return SSFM_OK;
+}
+
+extern "C" int64_t ssfm_cache_bytes(void) {
+  BlockCache& bc = block_cache();
+  std::lock_guard<std::mutex> lk(bc.mu);
+  return (int64_t)bc.bytes;
+}
+
 extern "C" int ssfm_schur_solve(const ssfm_schur_plan* plan, const double* data, const double* gradient,
                                 const ssfm_lm_config* cfg, double* delta, int32_t* cg_iters_host, void* stream) {
   if (!plan || !data || !gradient || !cfg || !delta) return set_err(SSFM_INVALID_ARGUMENT, "null argument");

@@ -227,6 +227,23 @@ def perturb(scene, rot_deg=0.0, center_frac=0.0, focal_frac=0.0, point_frac=0.0,
     return arr if isinstance(scene, SceneArrays) else arrays_to_scene(arr)
 
 
+def trim_points_arrays(arr: SceneArrays, keep_full: int) -> SceneArrays:
+    """SURVEY.md 8(d) C3 recipe: every point j >= keep_full loses its
+    observation with the highest camera id (1700 / 150k / k=5 -> exactly
+    680,000 observations, the BAL Ladybug shape). Observation order kept."""
+    cam = np.asarray(arr.cam_idx, dtype=np.int64)
+    pt = np.asarray(arr.pt_idx, dtype=np.int64)
+    top = np.full(arr.num_points, -1, dtype=np.int64)
+    np.maximum.at(top, pt, cam)
+    keep = ~((pt >= keep_full) & (cam == top[pt]))
+    out = arr.copy()
+    out.cam_idx, out.pt_idx = arr.cam_idx[keep], arr.pt_idx[keep]
+    out.pixels = arr.pixels[keep]
+    if arr.depths is not None:
+        out.depths = arr.depths[keep]
+    return out
+
+
 def outlier_mask(truth, observed, sigma: float) -> np.ndarray:
     t, o = as_arrays(truth), as_arrays(observed)
     return np.linalg.norm(t.pixels - o.pixels, axis=1) > max(6.0 * sigma, 1.0)

@@ -40,3 +40,12 @@ def test_invalid_arguments_rejected_without_gpu_work():
     rc = lib.ssfm_create_ba(None, None, ct.byref(out))
     assert rc == 9
     assert b"null" in lib.ssfm_last_error()
+
+
+def test_schur_plan_struct_matches_header():
+    # ssfm_schur_plan: 8 int64 sizes then 34 device pointers, header order
+    assert ct.sizeof(_native.SchurPlanC) == 8 * 8 + 34 * 8
+    text = open(HEADER).read()
+    body = text[text.index("typedef struct {\n  int64_t n_params, n_ret"):text.index("} ssfm_schur_plan;")]
+    names = re.findall(r"\*\s*([a-z_0-9]+);", body)
+    assert tuple(names) == tuple(n for n, _ in _native.SCHUR_PLAN_ARRAYS)
