@@ -57,12 +57,8 @@ def solve_local_shards(gpu, st, world, cfg, fused="1", graph="0"):
             p = probs[r]
             out[r] = b2.lm_solve(p, p.encode(), cfg)
 
-    run_shards(work, world, 300)   # raises the first shard error (SameDeviceStall for a timeout)
+    run_shards(work, world, 300)   # raises the first shard error
     return probs, out
-
-
-class SameDeviceStall(Exception):
-    """A shard's exchange timed out while all shards share one GPU."""
 
 
 def run_shards(work, n, timeout):
@@ -70,8 +66,8 @@ def run_shards(work, n, timeout):
     tests are destroyed first and the garbage collector is paused meanwhile: a
     handle destroyed inside a shard's thread synchronises the device while the
     peer's PCG kernel waits on that shard (a same-device-only hazard; with one
-    process per GPU it cannot happen). A shard that still times out raises
-    SameDeviceStall (see same_device_retry)."""
+    process per GPU it cannot happen). Any shard error -- an exchange timeout
+    included -- fails the test on the first attempt."""
     errs = []
 
     def guarded(r):
@@ -90,33 +86,14 @@ def run_shards(work, n, timeout):
             t.join(timeout=timeout)
     finally:
         gc.enable()
-    stalls = [e for e in errs if isinstance(e, b2.errors.NativeError) and "peer" in str(e)]
-    if stalls:
-        raise SameDeviceStall(stalls[0])
+    assert not any(t.is_alive() for t in ts), "a shard did not finish"
     if errs:
         raise errs[0]
 
 
-def same_device_retry(fn):
-    """Shards that share the test GPU occasionally stall on scheduling (a
-    shard's kernel queued behind its peer's waiting PCG kernel; not a data or
-    protocol error, and impossible with one GPU per rank): retry once with
-    fresh handles."""
-    import functools
-
-    @functools.wraps(fn)
-    def wrapper(*a, **k):
-        try:
-            return fn(*a, **k)
-        except SameDeviceStall:
-            gc.collect()
-            return fn(*a, **k)
-    return wrapper
-
-
 @pytest.mark.parametrize("world,fused,graph", [(2, "1", "0"), (3, "1", "0"), (2, "0", "0"), (2, "0", "1"),
-                                              (3, "1", "1")])
-@same_device_retry
+                                              (3, "1", "1"), (4, "1", "0"), (4, "0", "1"), (8, "0", "0"),
+                                              (8, "0", "1")])
 def test_local_shards_match_single_gpu(gpu, world, fused, graph):
     st = scene()
     cfg = b2.LMConfig(max_iterations=15)
@@ -129,7 +106,8 @@ def test_local_shards_match_single_gpu(gpu, world, fused, graph):
     th1, rep1 = b2.lm_solve(single, single.encode(), cfg)
     probs, out = solve_local_shards(gpu, st, world, cfg, fused, graph)
     reps = [o[1] for o in out]
-    # identical on every shard (bitwise)
+    # identical on every shard (bitwise): every damped solve's CG count, cost and
+    # lambda, and the replicated camera block of theta
     for rep in reps[1:]:
         assert [(i.cost_after, i.step_accepted, i.cg_iters, i.lam) for i in rep.iterations] == \
                [(i.cost_after, i.step_accepted, i.cg_iters, i.lam) for i in reps[0].iterations]
@@ -138,14 +116,14 @@ def test_local_shards_match_single_gpu(gpu, world, fused, graph):
         assert np.array_equal(c, cams[0])
     # follows the single-GPU solve
     assert [i.step_accepted for i in reps[0].iterations] == [i.step_accepted for i in rep1.iterations]
-    for a, b in zip(reps[0].iterations, rep1.iterations):
-        assert a.cost_after == pytest.approx(b.cost_after, rel=1e-7)
+    dev = max(abs(a.cost_after - b.cost_after) / b.cost_after for a, b in zip(reps[0].iterations, rep1.iterations))
+    print(f"world {world}: max relative cost deviation from the single-GPU solve {dev:.2e}")
+    assert dev < 1e-7
     full = probs[0].gather_theta(out[0][0], shards=[(p, o[0]) for p, o in zip(probs, out)])
     assert full.shape == th1.shape
     assert np.abs(full - th1).max() <= 1e-6 * max(1.0, np.abs(th1).max())
 
 
-@same_device_retry
 def test_sharded_cost_and_gradient_are_global(gpu):
     st = scene(cams=12, pts=400, k=4, seed=3)
     single = b2.BAProblem(st, b2.RobustLoss("huber", 1.0))
@@ -196,7 +174,6 @@ def test_two_processes_ipc(gpu, tmp_path):
 
 
 @pytest.mark.parametrize("fused", ["0", "1"])
-@same_device_retry
 def test_local_gp_shards_match_single_gpu(gpu, fused):
     """GP (gp.py) sharded by point: scales follow their observations, centres
     are replicated, the mean-scale gauge is taken over every rank."""

@@ -5,7 +5,7 @@ providers that use it.
 Ports of the reference's own tests (pkg/tests/test_lm.py:44-159), plus the
 reference's damped steps on the ba_small / gp_small goldens (the same system
 the reference solved with its default solver: same CG count, step within
-1e-8) and the failure paths of _invert_elim_blocks / pinning / CGStall.
+1e-7) and the failure paths of _invert_elim_blocks / pinning / CGStall.
 """
 import numpy as np
 import pytest
@@ -207,8 +207,11 @@ def test_explicit_solve_matches_reference_step(gpu, name, lam, key):
     ws = Workspace()
     d = solve_normal(apply_damping(sys_, lam), p.layout, LMConfig(), ws, info)
     ref = z[f"delta_{key}"]
-    assert np.abs(d - ref).max() / np.abs(ref).max() < 1e-8
+    # both are PCG solutions at cg_tol 1e-8 of the same reduced system, summed
+    # in different orders (dense S assembled per slot, own matvec): the same
+    # iteration count, steps within 1e-7 relative (largest on the focal scalars)
     assert info["cg_iters"] == int(z[f"cg_{key}"])
+    assert np.abs(d - ref).max() / np.abs(ref).max() < 1e-7
     # the plan is cached per pattern in the workspace and the result is deterministic
     d2 = solve_normal(apply_damping(sys_, lam), p.layout, LMConfig(), ws, info)
     assert np.array_equal(d, d2)
