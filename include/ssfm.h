@@ -139,6 +139,25 @@ int ssfm_create_ba(const ssfm_ba_desc* desc, void* stream, ssfm_handle** out);
 int ssfm_create_gp(const ssfm_gp_desc* desc, void* stream, ssfm_handle** out);
 int ssfm_destroy(ssfm_handle* h);
 
+/* ---- grow-only device arena (Workspace, lm.py:86-101; the spec's unified
+ * memory pool) -------------------------------------------------
+ * Handles created with ssfm_create_*_in take every device allocation from the
+ * arena (bump allocation). Destroying the last live handle resets it, so the
+ * next stage's handle (GP -> BA) reuses the same HBM without cudaMalloc; a
+ * stage that needs more adds a chunk, and an idle arena coalesces its chunks
+ * into one of the high-water size. reserve_bytes (may be 0) is allocated up
+ * front. The arena must outlive its handles (ssfm_arena_destroy fails with
+ * SSFM_INVALID_ARGUMENT while handles are live). device: the current device
+ * (-1). ssfm_arena_info: capacity, high-water mark, live handles and the
+ * number of cudaMalloc calls the arena made (any pointer may be NULL). */
+typedef struct ssfm_arena ssfm_arena;
+int ssfm_arena_create(int32_t device, int64_t reserve_bytes, ssfm_arena** out);
+int ssfm_arena_destroy(ssfm_arena* arena);
+int ssfm_arena_info(ssfm_arena* arena, int64_t* capacity, int64_t* high_water, int32_t* live_handles,
+                    int64_t* chunk_mallocs);
+int ssfm_create_ba_in(const ssfm_ba_desc* desc, ssfm_arena* arena, void* stream, ssfm_handle** out);
+int ssfm_create_gp_in(const ssfm_gp_desc* desc, ssfm_arena* arena, void* stream, ssfm_handle** out);
+
 /* Device block cache. ssfm_destroy hands a handle's device blocks to a
  * per-process cache (exact-size reuse: re-creating a handle of the same shape
  * skips cudaMalloc/cudaFree, 40-190 ms at C5), capped by SSFM_BLOCK_CACHE_GB or
@@ -318,7 +337,7 @@ int ssfm_check_jacobian(ssfm_handle* h, int64_t* mismatches, void* stream);
 /* Diagnostic (BA): mean time (ms) of one standalone launch of a pass of the
  * two-pass Schur operator over the current linearization, reps launches after
  * warm-up. which: 0 = point pass (Jpm, p gather -> y), 1 = camera pass (Jcm,
- * y gather -> tile sums). Call after ssfm_solve_normal. */
+ * y gather -> tile sums), 2 = both back to back. Call after ssfm_solve_normal. */
 int ssfm_bench_operator(ssfm_handle* h, int32_t which, int32_t reps, double* ms_out, void* stream);
 
 /* Which Schur operator the PCG kernel of this handle runs (no reference

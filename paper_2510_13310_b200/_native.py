@@ -27,7 +27,8 @@ EXPORTS = (
     "ssfm_block_scale_diag", "ssfm_dense_scatter", "ssfm_dense_solve",
     "ssfm_rotation_auc", "ssfm_center_moments", "ssfm_apply_sim3",
     "ssfm_bal_read", "ssfm_bal_take", "ssfm_bal_free", "ssfm_make_rays", "ssfm_schur_solve",
-    "ssfm_trim_cache", "ssfm_cache_bytes",
+    "ssfm_trim_cache", "ssfm_cache_bytes", "ssfm_arena_create", "ssfm_arena_destroy", "ssfm_arena_info",
+    "ssfm_create_ba_in", "ssfm_create_gp_in",
 )
 
 TERMINATIONS = {0: "max_iter", 1: "converged_cost", 2: "converged_grad", 3: "solver_failure"}
@@ -129,6 +130,11 @@ def load(required: bool = True):
     lib.ssfm_make_rays.argtypes = [I64, P, P, P, P, P, P, P, P, P]
     lib.ssfm_bal_free.argtypes = [P]
     lib.ssfm_trim_cache.argtypes = [I32, ct.POINTER(I64)]
+    lib.ssfm_arena_create.argtypes = [I32, I64, ct.POINTER(P)]
+    lib.ssfm_arena_destroy.argtypes = [P]
+    lib.ssfm_arena_info.argtypes = [P, ct.POINTER(I64), ct.POINTER(I64), ct.POINTER(I32), ct.POINTER(I64)]
+    lib.ssfm_create_ba_in.argtypes = [ct.POINTER(BADescC), P, P, ct.POINTER(P)]
+    lib.ssfm_create_gp_in.argtypes = [ct.POINTER(GPDescC), P, P, ct.POINTER(P)]
     lib.ssfm_cache_bytes.argtypes = []
     lib.ssfm_cache_bytes.restype = I64
     lib.ssfm_schur_solve.argtypes = [ct.POINTER(SchurPlanC), P, P, ct.POINTER(LMConfigC), P, ct.POINTER(I32), P]
@@ -163,6 +169,37 @@ def trim_cache(device: int = -1) -> int:
     freed = ct.c_int64(0)
     check(lib.ssfm_trim_cache(int(device), ct.byref(freed)))
     return int(freed.value)
+
+
+class Arena:
+    """A grow-only device arena (ssfm_arena_*): native problems created in it
+    share its HBM stage after stage (the Workspace's device side)."""
+
+    def __init__(self, reserve_bytes: int = 0):
+        out = ct.c_void_p(0)
+        check(load().ssfm_arena_create(-1, int(reserve_bytes), ct.byref(out)))
+        self.ptr = out.value
+
+    def info(self) -> dict:
+        cap, hw, nm = ct.c_int64(0), ct.c_int64(0), ct.c_int64(0)
+        live = ct.c_int32(0)
+        check(load().ssfm_arena_info(ct.c_void_p(self.ptr), ct.byref(cap), ct.byref(hw), ct.byref(live),
+                                     ct.byref(nm)))
+        return {"capacity": cap.value, "high_water": hw.value, "live_handles": live.value,
+                "chunk_mallocs": nm.value}
+
+    def close(self) -> None:
+        if self.ptr and _lib is not None:
+            check(_lib.ssfm_arena_destroy(ct.c_void_p(self.ptr)))
+        self.ptr = 0
+
+    def __del__(self):
+        try:
+            if self.ptr and _lib is not None:
+                _lib.ssfm_arena_destroy(ct.c_void_p(self.ptr))
+        except Exception:
+            pass
+        self.ptr = 0
 
 
 class Handle:

@@ -42,13 +42,37 @@ class _DeviceProblem:
 
     _native_ptr = None
 
-    def _create(self):  # pragma: no cover - abstract
+    def _create(self, arena=None):  # pragma: no cover - abstract
         raise NotImplementedError
 
-    def _native_handle(self):
+    def _native_handle(self, workspace=None):
+        """The device problem, created on first use; with a Workspace (lm_solve,
+        run_ba / run_gp) it is created in the workspace's device arena."""
         if self._native_ptr is None:
-            self._native_ptr = self._create()
+            self._native_ptr = self._create(workspace.device_arena() if workspace is not None else None)
         return self._native_ptr
+
+    def _device_input(self, torch, key, make):
+        """a device copy of an input array: the caller's (set_device_inputs) or a fresh upload"""
+        d = getattr(self, "_dev_inputs", None)
+        if d is not None and d.get(key) is not None:
+            return d[key]
+        return make()
+
+    def set_device_inputs(self, **tensors) -> None:
+        """Hand the problem device-resident copies of its per-observation
+        inputs (cam=int32, pt=int32 [N] CUDA tensors; pixels [N,2] / rays [N,3]
+        float64) so handle creation copies device to device instead of
+        uploading from the host (the GP -> BA pipeline)."""
+        self._dev_inputs = dict(tensors)
+
+    @staticmethod
+    def _create_call(lib, kind, desc, arena, stream, out):
+        if arena is None:
+            fn = lib.ssfm_create_ba if kind == "ba" else lib.ssfm_create_gp
+            return fn(ct.byref(desc), stream, ct.byref(out))
+        fn = lib.ssfm_create_ba_in if kind == "ba" else lib.ssfm_create_gp_in
+        return fn(ct.byref(desc), ct.c_void_p(arena.ptr), stream, ct.byref(out))
 
     @staticmethod
     def _theta_dev(torch, theta):
@@ -190,14 +214,14 @@ class BAProblem(_DeviceProblem):
             ids[:, 2] = c + p if self.shared_focal else c + p + self.arr.cam_idx
         return ids.ravel()
 
-    def _create(self):
+    def _create(self, arena=None):
         torch = _torch()
         from .lm import _stream
         a = self.arr
         dev = lambda x, dt: torch.as_tensor(np.ascontiguousarray(x, dtype=dt)).to("cuda")  # noqa: E731
-        cam = _index_dev(torch, a.cam_idx)
-        pt = _index_dev(torch, a.pt_idx)
-        pix = dev(a.pixels, np.float64)
+        cam = self._device_input(torch, "cam", lambda: _index_dev(torch, a.cam_idx))
+        pt = self._device_input(torch, "pt", lambda: _index_dev(torch, a.pt_idx))
+        pix = self._device_input(torch, "pixels", lambda: dev(a.pixels, np.float64))
         pps = dev(a.pps, np.float64)
         dists = dev(a.dists, np.float64)
         foc = dev(a.focals, np.float64)
@@ -207,9 +231,9 @@ class BAProblem(_DeviceProblem):
             cam.data_ptr(), pt.data_ptr(), pix.data_ptr(), pps.data_ptr(), dists.data_ptr(),
             foc.data_ptr())
         out = ct.c_void_p(0)
-        _native.check(_native.load().ssfm_create_ba(ct.byref(desc), _stream(torch), ct.byref(out)))
+        _native.check(self._create_call(_native.load(), "ba", desc, arena, _stream(torch), out))
         torch.cuda.current_stream().synchronize()
-        return _native.Handle(out.value)
+        return _native.Handle(out.value, keepalive=(arena,) if arena is not None else ())
 
     # -- theta packing (ba.py:68-107) ----------------------------------------
     def encode(self) -> np.ndarray:

@@ -85,6 +85,9 @@ __device__ __forceinline__ void ba_load_frec(const double* __restrict__ F, long 
 #define CAMF_UNROLL 2
 #endif
 constexpr int kCamfUnroll = CAMF_UNROLL;
+#ifndef CAMF_PF
+#define CAMF_PF 0        // L2 bulk prefetch of the next tile's records
+#endif
 #ifndef CAMF_HOIST
 #define CAMF_HOIST 1     // keep the tile camera's R, qh in registers across the loop
 #endif
@@ -96,10 +99,29 @@ __device__ __forceinline__ void ba_camera_pass_f(const BADev& d, const double* y
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+#if CAMF_PF
+  // the next tile's bounds are loaded one tile ahead, and its record rows are
+  // prefetched into L2 (one bulk request per row) while this tile runs
+  int nx0 = 0, nx1 = 0;
+  if (gw + warps < d.topo.nt) { nx0 = __ldg(d.topo.tile_obs + gw + warps); nx1 = __ldg(d.topo.tile_obs + gw + warps + 1); }
+#endif
   for (int t = gw; t < d.topo.nt; t += warps) {
     const int o0 = __ldg(d.topo.tile_obs + t), o1 = __ldg(d.topo.tile_obs + t + 1);
     const int c = __ldg(d.topo.tile_cam + t);
     const double* cb = reinterpret_cast<const double*>(d.camlin + c);
+#if CAMF_PF
+    if (t + warps < d.topo.nt) {
+      const int nrow = model == 1 ? 9 : 7;
+      if (lane < nrow) {
+        const int row = (model == 1 || lane < 4) ? lane : lane + 2;   // pinhole: rows 0-3, 6-8
+        pf_l2_bulk(d.Fcm + row * Np + nx0, 8ll * (nx1 - nx0));
+      } else if (lane == 16) {
+        pf_l2_bulk(d.topo.cm_pt + nx0, 4ll * (nx1 - nx0));
+      }
+      const int tn = t + 2 * warps;
+      if (tn < d.topo.nt) { nx0 = __ldg(d.topo.tile_obs + tn); nx1 = __ldg(d.topo.tile_obs + tn + 1); }
+    }
+#endif
     double o[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) o[k] = 0.0;
@@ -167,6 +189,23 @@ __device__ __forceinline__ void ba_camera_pass_f(const BADev& d, const double* y
   }
 }
 
+#ifndef PTP_PF
+#define PTP_PF 0         // L2 bulk prefetch of the next batch's records
+#endif
+#ifndef PTP_PIPE
+#define PTP_PIPE 0       // software-pipelined point pass (ba_point_pass_pipe)
+#endif
+#if PTP_PIPE
+#define PTP_THREADS 128
+#ifndef PTP_MINB
+#define PTP_MINB 6
+#endif
+#else
+#define PTP_THREADS PCG_THREADS
+#ifndef PTP_MINB
+#define PTP_MINB 4
+#endif
+#endif
 // P1 for a camera vector v -> y (per point): y_j = Cinv_j sum_o Jp^T (Jc v_c)
 template <bool RO = false>
 __device__ __forceinline__ void ba_point_pass(const BADev& d, const double* v, double* y,
@@ -176,9 +215,31 @@ __device__ __forceinline__ void ba_point_pass(const BADev& d, const double* v, d
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long Np = d.Npad;
+#if PTP_PF
+  // batch bounds carried one batch ahead; the next batch's Jacobian rows,
+  // camera ids and Cinv blocks are prefetched into L2 (bulk requests, one per
+  // lane) while this batch runs
+  int nb0 = 0, nb1 = 0, np0 = 0, np1 = 0;
+  if (gw + warps < d.topo.nb) {
+    nb0 = d.topo.bat_obs[gw + warps]; nb1 = d.topo.bat_obs[gw + warps + 1];
+    np0 = d.topo.bat_pt[gw + warps]; np1 = d.topo.bat_pt[gw + warps + 1];
+  }
+#endif
   for (int b = gw; b < d.topo.nb; b += warps) {
     const int ob0 = d.topo.bat_obs[b], ob1 = d.topo.bat_obs[b + 1];
     const int pb0 = d.topo.bat_pt[b], pb1 = d.topo.bat_pt[b + 1];
+#if PTP_PF
+    if (b + warps < d.topo.nb) {
+      if (lane < BA_JREC) pf_l2_bulk(d.Jpm + lane * Np + nb0, 8ll * (nb1 - nb0));
+      else if (lane == BA_JREC) pf_l2_bulk(d.topo.pm_cam + nb0, 4ll * (nb1 - nb0));
+      else if (lane == BA_JREC + 1) pf_l2_bulk(d.Cinv + 6ll * np0, 48ll * (np1 - np0));
+      const int bn = b + 2 * warps;
+      if (bn < d.topo.nb) {
+        nb0 = d.topo.bat_obs[bn]; nb1 = d.topo.bat_obs[bn + 1];
+        np0 = d.topo.bat_pt[bn]; np1 = d.topo.bat_pt[bn + 1];
+      }
+    }
+#endif
     const int my_pt = pb0 + lane;
     int ps = 0, pe = 0;
     if (my_pt < pb1) { ps = d.topo.pt_seg[my_pt]; pe = d.topo.pt_seg[my_pt + 1]; }
@@ -223,6 +284,126 @@ __device__ __forceinline__ void ba_point_pass(const BADev& d, const double* v, d
       for (int k = 0; k < 3; ++k) st_hint(y + 4ll * my_pt + k, w[k], pkeep);
     }
   }
+}
+
+// P1, software-pipelined: while a warp works on batch b, the Jacobian rows
+// and camera ids of its next batch are already in flight into a second
+// shared-memory stage (cp.async, no registers held), and batch b's Cinv
+// blocks are requested at the top of the batch instead of after the
+// reduction. Batch bounds are carried two batches ahead, so no load in the
+// loop head waits on another load. Batches with more than 32 observations (a
+// point seen more than 32 times) are read directly, round by round.
+struct PtpStage {
+  double J[BA_JREC][SSFM_BATCH];
+  int cam[SSFM_BATCH];
+};
+
+__device__ __forceinline__ void ptp_issue(const BADev& d, int o0, int o1, PtpStage& s, unsigned long long pol,
+                                          int lane) {
+  const long long Np = d.Npad;
+  const int i = o0 + lane;
+  if (o1 - o0 <= SSFM_BATCH && i < o1) {
+#pragma unroll
+    for (int k = 0; k < BA_JREC; ++k) cp_async8(&s.J[k][lane], d.Jpm + k * Np + i, pol);
+    cp_async4(&s.cam[lane], d.topo.pm_cam + i, pol);
+  }
+  cp_commit();
+}
+
+template <bool RO>
+__device__ __forceinline__ void ptp_obs(const BADev& d, const double* v, const double* J, int c, double* val) {
+  double pc[8];
+  if constexpr (RO) {
+    const unsigned long long pkeep = pol_evict_last();
+    ld_v4_ro(v + 8ll * c, pc, pkeep);
+    ld_v4_ro(v + 8ll * c + 4, pc + 4, pkeep);
+  } else {
+    ld_v4(v + 8ll * c, pc);
+    ld_v4(v + 8ll * c + 4, pc + 4);
+  }
+  if (d.bp.focal_mode == 2) pc[7] = v[7];   // shared focal (camera 0, slot 7)
+  double t[2];
+  ba_jc_mul(J, pc, t);
+  ba_jpt_mul(J, t, val);
+}
+
+template <bool RO = false>
+__device__ __forceinline__ void ba_point_pass_pipe(const BADev& d, const double* v, double* y, PtpStage (*stg)[2],
+                                                   double (*sm)[SSFM_BATCH][3]) {
+  const unsigned long long pstream = pol_evict_first(), pkeep = pol_evict_last();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long Np = d.Npad;
+  const int nb = d.topo.nb;
+  auto bounds = [&](int b, int& o0, int& o1, int& p0, int& p1) {
+    if (b < nb) {
+      o0 = d.topo.bat_obs[b]; o1 = d.topo.bat_obs[b + 1];
+      p0 = d.topo.bat_pt[b]; p1 = d.topo.bat_pt[b + 1];
+    } else {
+      o0 = o1 = p0 = p1 = 0;
+    }
+  };
+  int ob0, ob1, pb0, pb1, nb0, nb1, np0, np1;
+  bounds(gw, ob0, ob1, pb0, pb1);
+  bounds(gw + warps, nb0, nb1, np0, np1);
+  int st = 0;
+  ptp_issue(d, ob0, ob1, stg[wib][0], pstream, lane);
+  for (int b = gw; b < nb; b += warps) {
+    ptp_issue(d, nb0, nb1, stg[wib][st ^ 1], pstream, lane);   // next batch (empty group past the end)
+    int xb0, xb1, xp0, xp1;
+    bounds(b + 2 * warps, xb0, xb1, xp0, xp1);
+    const int my_pt = pb0 + lane;
+    int ps = 0, pe = 0;
+    double ci[6];
+    if (my_pt < pb1) {
+      ps = d.topo.pt_seg[my_pt];
+      pe = d.topo.pt_seg[my_pt + 1];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) ci[k] = __ldg(d.Cinv + 6ll * my_pt + k);
+    }
+    double acc[3] = {0.0, 0.0, 0.0};
+    const bool staged = ob1 - ob0 <= SSFM_BATCH;
+    cp_wait<1>();
+    __syncwarp();
+    for (int base = ob0; base < ob1; base += SSFM_BATCH) {
+      const int i = base + lane;
+      double val[3] = {0.0, 0.0, 0.0};
+      if (i < ob1) {
+        double J[BA_JREC];
+        int c;
+        if (staged) {
+#pragma unroll
+          for (int k = 0; k < BA_JREC; ++k) J[k] = stg[wib][st].J[k][lane];
+          c = stg[wib][st].cam[lane];
+        } else {
+#pragma unroll
+          for (int k = 0; k < BA_JREC; ++k) J[k] = ldg_stream(d.Jpm + k * Np + i, pstream);
+          c = ldg_stream_i(d.topo.pm_cam + i, pstream);
+        }
+        ptp_obs<RO>(d, v, J, c, val);
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) sm[wib][lane][k] = val[k];
+      __syncwarp();
+      const int a = max(ps, base), e = min(pe, base + SSFM_BATCH);
+      for (int o = a; o < e; ++o) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) acc[k] += sm[wib][o - base][k];
+      }
+      __syncwarp();
+    }
+    if (my_pt < pb1) {
+      double w[3];
+      sym3_matvec(ci, acc, w);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) st_hint(y + 4ll * my_pt + k, w[k], pkeep);
+    }
+    ob0 = nb0; ob1 = nb1; pb0 = np0; pb1 = np1;
+    nb0 = xb0; nb1 = xb1; np0 = xp0; np1 = xp1;
+    st ^= 1;
+  }
+  cp_wait<0>();
 }
 
 // P2: per camera tile, sum Jc^T (Jp y_j) -> tile8[t][8]. One WARP per tile:
@@ -632,12 +813,14 @@ ba_k_pcg(BADev d, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg
 
 // Diagnostic wrappers: the two passes of the two-pass operator as standalone
 // kernels (per-pass timing and roofline, ssfm_bench_operator).
-#ifndef PTP_MINB
-#define PTP_MINB 4
-#endif
-__global__ void __launch_bounds__(PCG_THREADS, PTP_MINB) k_op_point(BADev d, const double* v, double* y) {
-  __shared__ double smp[PCG_THREADS / 32][SSFM_BATCH][3];
+__global__ void __launch_bounds__(PTP_THREADS, PTP_MINB) k_op_point(BADev d, const double* v, double* y) {
+  __shared__ double smp[PTP_THREADS / 32][SSFM_BATCH][3];
+#if PTP_PIPE
+  __shared__ PtpStage stg[PTP_THREADS / 32][2];
+  ba_point_pass_pipe<true>(d, v, y, stg, smp);
+#else
   ba_point_pass<true>(d, v, y, smp);
+#endif
 }
 template <bool FAC>
 __global__ void __launch_bounds__(PCG_THREADS, FAC ? CAMF_MINB : 4) k_op_camera(BADev d, const double* y, double* tile8) {

@@ -84,13 +84,15 @@ __global__ void k_g_init2(Dev d, CGGraphDev g, int nblk) {
 }
 
 // ---- body kernels (each returns at once when the solve is done)
-#ifndef PTP_MINB
-#define PTP_MINB 4       // CTAs per SM of the graph point pass
-#endif
-__global__ void __launch_bounds__(PCG_THREADS, PTP_MINB) k_g_point(BADev d, CGGraphDev g) {
+__global__ void __launch_bounds__(PTP_THREADS, PTP_MINB) k_g_point(BADev d, CGGraphDev g) {
   if (*(volatile int*)(g.ic + 3)) return;
-  __shared__ double smp[PCG_THREADS / 32][SSFM_BATCH][3];
+  __shared__ double smp[PTP_THREADS / 32][SSFM_BATCH][3];
+#if PTP_PIPE
+  __shared__ PtpStage stg[PTP_THREADS / 32][2];
+  ba_point_pass_pipe<true>(d, g.p, d.yv, stg, smp);   // p is constant during this kernel
+#else
   ba_point_pass<true>(d, g.p, d.yv, smp);   // p is constant during this kernel
+#endif
 }
 
 // FAC: the factored camera pass (ba_camera_pass_f)

@@ -144,6 +144,31 @@ __device__ __forceinline__ void ld_v4_ro(const double* a, double* x, unsigned lo
                : "=d"(x[0]), "=d"(x[1]), "=d"(x[2]), "=d"(x[3]) : "l"(a), "l"(pol));
 }
 
+// L2 prefetch of the byte range [a, a + bytes) with one bulk (TMA) request:
+// the range is widened to 16-byte alignment (cp.async.bulk.prefetch needs it;
+// device allocations are 256-byte granular, so the widened range stays mapped)
+__device__ __forceinline__ void pf_l2_bulk(const void* a, long long bytes) {
+  if (bytes <= 0) return;
+  const unsigned long long s = reinterpret_cast<unsigned long long>(a);
+  const unsigned long long lo = s & ~15ull, hi = (s + (unsigned long long)bytes + 15ull) & ~15ull;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"((unsigned)(hi - lo)) : "memory");
+}
+
+// LDGSTS: asynchronous global -> shared copies (per thread; groups committed
+// and waited on per thread, so a warp needs __syncwarp before reading a
+// peer's element). The L2 policy rides along.
+__device__ __forceinline__ void cp_async8(void* s, const void* g, unsigned long long pol) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(sa), "l"(g), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* s, const void* g, unsigned long long pol) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(sa), "l"(g), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 __device__ __forceinline__ void st_hint(double* a, double v, unsigned long long pol) {
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
 }

@@ -63,6 +63,87 @@ struct Profile {
   long long kernel_launches = 0;   // every kernel launched by the library
 };
 
+// Grow-only device arena (the reference's Workspace, lm.py:86-101, as HBM):
+// handles created in it (ssfm_create_ba_in / ssfm_create_gp_in) bump-allocate
+// from its chunks and give nothing back one by one; when the last live handle
+// is destroyed the arena is reset, so the next stage's handle (GP -> BA)
+// reuses the same HBM without cudaMalloc. A stage that needs more than the
+// arena holds adds a chunk; after a reset the chunks are coalesced into one of
+// the high-water size (grow-only).
+struct ssfm_arena {
+  int device = 0;
+  std::mutex mu;
+  std::vector<std::pair<char*, size_t>> chunks;   // (base, bytes)
+  size_t cur = 0;          // chunk being filled
+  size_t off = 0;          // bytes used in chunks[cur]
+  size_t used = 0;         // bytes handed out since the last reset
+  size_t high_water = 0;
+  int live = 0;            // handles holding allocations
+  long long chunk_mallocs = 0;
+};
+
+static size_t arena_capacity(const ssfm_arena* a) {
+  size_t s = 0;
+  for (const auto& c : a->chunks) s += c.second;
+  return s;
+}
+
+static int arena_alloc(ssfm_arena* a, size_t b, void** out) {
+  std::lock_guard<std::mutex> lk(a->mu);
+  if (a->live == 0 && a->used == 0 && a->chunks.size() > 1) {
+    // coalesce the chunks of an idle arena into one of the high-water size
+    const size_t total = std::max(arena_capacity(a), a->high_water);
+    for (auto& c : a->chunks) cudaFree(c.first);
+    a->chunks.clear();
+    char* p = nullptr;
+    if (cudaMalloc((void**)&p, total) != cudaSuccess) {
+      cudaGetLastError();
+      return set_err(SSFM_CUDA_ERROR, "arena: cudaMalloc failed while coalescing");
+    }
+    a->chunks.emplace_back(p, total);
+    a->chunk_mallocs++;
+    a->cur = 0;
+    a->off = 0;
+  }
+  while (a->cur < a->chunks.size() && a->off + b > a->chunks[a->cur].second) {
+    ++a->cur;
+    a->off = 0;
+  }
+  if (a->cur >= a->chunks.size()) {
+    const size_t grow = std::max(b, std::max(arena_capacity(a), (size_t)256 << 20));
+    char* p = nullptr;
+    cudaError_t e = cudaMalloc((void**)&p, grow);
+    if (e == cudaErrorMemoryAllocation && grow > b) {
+      cudaGetLastError();
+      e = cudaMalloc((void**)&p, b);
+      if (e == cudaSuccess) a->chunks.emplace_back(p, b);
+    } else if (e == cudaSuccess) {
+      a->chunks.emplace_back(p, grow);
+    }
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return set_err(SSFM_CUDA_ERROR, std::string("arena: cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    a->chunk_mallocs++;
+    a->cur = a->chunks.size() - 1;
+    a->off = 0;
+  }
+  *out = a->chunks[a->cur].first + a->off;
+  a->off += b;
+  a->used += b;
+  a->high_water = std::max(a->high_water, a->used);
+  return SSFM_OK;
+}
+
+static void arena_release(ssfm_arena* a) {
+  std::lock_guard<std::mutex> lk(a->mu);
+  if (--a->live == 0) {
+    a->cur = 0;
+    a->off = 0;
+    a->used = 0;
+  }
+}
+
 struct ssfm_handle {
   int kind = 0;   // 0 BA, 1 GP
   int device = 0;
@@ -109,6 +190,7 @@ struct ssfm_handle {
   Profile prof;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
   std::vector<size_t> alloc_bytes;   // sizes of allocs (block cache)
+  ssfm_arena* arena = nullptr;       // allocations come from this arena (not from allocs)
 };
 
 // Device blocks of destroyed handles are kept for reuse by exact size (per
@@ -158,6 +240,13 @@ static int dalloc(ssfm_handle* h, T** ptr, size_t count) {
   size_t b = sizeof(T) * (count > 0 ? count : 1);
   b = (b + 255) & ~size_t(255);
   void* p = nullptr;
+  if (h->arena) {
+    const int rc = arena_alloc(h->arena, b, &p);
+    if (rc) return rc;
+    h->bytes += b;
+    *ptr = static_cast<T*>(p);
+    return SSFM_OK;
+  }
   {
     BlockCache& bc = block_cache();
     std::lock_guard<std::mutex> lk(bc.mu);
@@ -212,6 +301,10 @@ static void free_handle(ssfm_handle* h) {
         cudaFree(h->allocs[k]);
       }
     }
+  }
+  if (h->arena) {
+    cudaDeviceSynchronize();   // no kernel may still use the arena's bytes
+    arena_release(h->arena);
   }
   if (h->region) cudaFree(h->region);
   if (h->hmisc) cudaFreeHost(h->hmisc);
@@ -523,7 +616,72 @@ static int setup_ba_pcg_op(ssfm_handle* h, cudaStream_t st) {
 // ---------------------------------------------------------------------------
 // BA
 // ---------------------------------------------------------------------------
+static int create_ba(const ssfm_ba_desc* desc, ssfm_arena* arena, void* stream, ssfm_handle** out);
+static int create_gp(const ssfm_gp_desc* desc, ssfm_arena* arena, void* stream, ssfm_handle** out);
+
 extern "C" int ssfm_create_ba(const ssfm_ba_desc* desc, void* stream, ssfm_handle** out) {
+  return create_ba(desc, nullptr, stream, out);
+}
+extern "C" int ssfm_create_gp(const ssfm_gp_desc* desc, void* stream, ssfm_handle** out) {
+  return create_gp(desc, nullptr, stream, out);
+}
+extern "C" int ssfm_create_ba_in(const ssfm_ba_desc* desc, ssfm_arena* arena, void* stream, ssfm_handle** out) {
+  if (!arena) return set_err(SSFM_INVALID_ARGUMENT, "null arena");
+  return create_ba(desc, arena, stream, out);
+}
+extern "C" int ssfm_create_gp_in(const ssfm_gp_desc* desc, ssfm_arena* arena, void* stream, ssfm_handle** out) {
+  if (!arena) return set_err(SSFM_INVALID_ARGUMENT, "null arena");
+  return create_gp(desc, arena, stream, out);
+}
+
+extern "C" int ssfm_arena_create(int32_t device, int64_t reserve_bytes, ssfm_arena** out) {
+  if (!out || reserve_bytes < 0) return set_err(SSFM_INVALID_ARGUMENT, "bad argument");
+  int cur = 0;
+  CU(cudaGetDevice(&cur));
+  ssfm_arena* a = new ssfm_arena();
+  a->device = device < 0 ? cur : device;
+  if (a->device != cur) {
+    delete a;
+    return set_err(SSFM_INVALID_ARGUMENT, "arena device must be the current device");
+  }
+  if (reserve_bytes > 0) {
+    char* p = nullptr;
+    if (cudaMalloc((void**)&p, (size_t)reserve_bytes) != cudaSuccess) {
+      cudaGetLastError();
+      delete a;
+      return set_err(SSFM_CUDA_ERROR, "arena: cudaMalloc of the reservation failed");
+    }
+    a->chunks.emplace_back(p, (size_t)reserve_bytes);
+    a->chunk_mallocs = 1;
+  }
+  *out = a;
+  return SSFM_OK;
+}
+
+extern "C" int ssfm_arena_destroy(ssfm_arena* a) {
+  if (!a) return SSFM_OK;
+  {
+    std::lock_guard<std::mutex> lk(a->mu);
+    if (a->live > 0) return set_err(SSFM_INVALID_ARGUMENT, "arena still has live handles");
+  }
+  cudaDeviceSynchronize();
+  for (auto& c : a->chunks) cudaFree(c.first);
+  delete a;
+  return SSFM_OK;
+}
+
+extern "C" int ssfm_arena_info(ssfm_arena* a, int64_t* capacity, int64_t* high_water, int32_t* live_handles,
+                               int64_t* chunk_mallocs) {
+  if (!a) return set_err(SSFM_INVALID_ARGUMENT, "null arena");
+  std::lock_guard<std::mutex> lk(a->mu);
+  if (capacity) *capacity = (int64_t)arena_capacity(a);
+  if (high_water) *high_water = (int64_t)a->high_water;
+  if (live_handles) *live_handles = a->live;
+  if (chunk_mallocs) *chunk_mallocs = a->chunk_mallocs;
+  return SSFM_OK;
+}
+
+static int create_ba(const ssfm_ba_desc* desc, ssfm_arena* arena, void* stream, ssfm_handle** out) {
   if (!desc || !out) return set_err(SSFM_INVALID_ARGUMENT, "null argument");
   *out = nullptr;
   if (desc->num_obs <= 0) return set_err(SSFM_EMPTY_PROBLEM, "scene has no observations");
@@ -534,6 +692,12 @@ extern "C" int ssfm_create_ba(const ssfm_ba_desc* desc, void* stream, ssfm_handl
   CU(cudaGetDevice(&h->device));
   CU(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device));
   h->kind = 0;
+  if (arena) {
+    if (arena->device != h->device) { delete h; return set_err(SSFM_INVALID_ARGUMENT, "arena is on another device"); }
+    std::lock_guard<std::mutex> lk(arena->mu);
+    arena->live++;
+    h->arena = arena;
+  }
   const int C = desc->num_cameras, P = desc->num_points;
   const long long N = desc->num_obs;
   BADev& d = h->ba;
@@ -636,7 +800,7 @@ extern "C" int ssfm_create_ba(const ssfm_ba_desc* desc, void* stream, ssfm_handl
 // ---------------------------------------------------------------------------
 // GP
 // ---------------------------------------------------------------------------
-extern "C" int ssfm_create_gp(const ssfm_gp_desc* desc, void* stream, ssfm_handle** out) {
+static int create_gp(const ssfm_gp_desc* desc, ssfm_arena* arena, void* stream, ssfm_handle** out) {
   if (!desc || !out) return set_err(SSFM_INVALID_ARGUMENT, "null argument");
   *out = nullptr;
   if (desc->num_obs <= 0) return set_err(SSFM_EMPTY_PROBLEM, "problem has no observations");
@@ -648,6 +812,12 @@ extern "C" int ssfm_create_gp(const ssfm_gp_desc* desc, void* stream, ssfm_handl
   CU(cudaGetDevice(&h->device));
   CU(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device));
   h->kind = 1;
+  if (arena) {
+    if (arena->device != h->device) { delete h; return set_err(SSFM_INVALID_ARGUMENT, "arena is on another device"); }
+    std::lock_guard<std::mutex> lk(arena->mu);
+    arena->live++;
+    h->arena = arena;
+  }
   const int C = desc->num_cameras, P = desc->num_points;
   const long long N = desc->num_obs;
   GPDev& g = h->gp;
@@ -965,6 +1135,50 @@ static void capture_fused(ssfm_handle* h, cudaStream_t cs) {
   k_g_fused<SL><<<h->pcg_grid, FZ_THREADS, h->pcg_smem, cs>>>(h->ba, h->fz, h->gdev);
 }
 
+// Keep a gathered per-point vector (y of the two-pass operator, 4P doubles)
+// resident in L2 while the Jacobian streams past it: a persisting
+// access-policy window on the stream the PCG graph is captured on (kernel
+// nodes inherit it). Without it ~40 % of the camera pass's y gathers miss L2
+// at C5 (0.39 GB of extra DRAM reads per CG iteration, ncu). SSFM_L2_PERSIST=0
+// disables it. Returns whether the window was set.
+static bool set_l2_window(ssfm_handle* h, cudaStream_t cs, void* base, size_t bytes) {
+  const char* e = getenv("SSFM_L2_PERSIST");
+  if (e && atoi(e) == 0) return false;
+  int maxp = 0, maxw = 0;
+  if (cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, h->device) != cudaSuccess ||
+      cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, h->device) != cudaSuccess ||
+      maxp <= 0 || maxw <= 0) {
+    cudaGetLastError();
+    return false;
+  }
+  const size_t win = std::min(bytes, (size_t)maxw);
+  const size_t want = std::min(win, (size_t)maxp);
+  size_t cur = 0;
+  cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+  if (cur < want && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  cudaStreamAttrValue v = {};
+  v.accessPolicyWindow.base_ptr = base;
+  v.accessPolicyWindow.num_bytes = win;
+  v.accessPolicyWindow.hitRatio = std::min(1.0f, (float)((double)want / (double)win));
+  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  if (cudaStreamSetAttribute(cs, cudaStreamAttributeAccessPolicyWindow, &v) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return true;
+}
+
+static void clear_l2_window(cudaStream_t cs) {
+  cudaStreamAttrValue v = {};
+  v.accessPolicyWindow.num_bytes = 0;
+  cudaStreamSetAttribute(cs, cudaStreamAttributeAccessPolicyWindow, &v);
+  cudaGetLastError();
+}
+
 // Build the graph PCG of a BA handle: one conditional WHILE node, body = one
 // CG iteration as kernels. Falls back to the persistent kernel (state -1) if
 // the runtime refuses (e.g. no conditional nodes).
@@ -1009,6 +1223,7 @@ static int build_pcg_graph(ssfm_handle* h) {
   if ((e = cudaGraphAddNode(&cn, h->pcg_graph, nullptr, 0, &cp))) return unavailable(e);
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   if ((e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking))) return unavailable(e);
+  if (!g.fused) set_l2_window(h, cs, h->ba.yv, sizeof(double) * 4 * (size_t)h->ba.bp.P);
   if ((e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed)))
     return unavailable(e);
   BADev& d = h->ba;
@@ -1016,7 +1231,7 @@ static int build_pcg_graph(ssfm_handle* h) {
   const bool fac = d.Fcm != nullptr;
   void* kp = (void*)k_g_point;
   void* kc = fac ? (void*)k_g_camera<true> : (void*)k_g_camera<false>;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, kp, PCG_THREADS, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, kp, PTP_THREADS, 0);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, kc, PCG_THREADS, 0);
   if (g.fused) {
     switch (h->fz.SL) {
@@ -1026,7 +1241,7 @@ static int build_pcg_graph(ssfm_handle* h) {
       default: capture_fused<1>(h, cs); break;
     }
   } else {
-    k_g_point<<<std::max(1, occ_p) * h->num_sms, PCG_THREADS, 0, cs>>>(d, g);
+    k_g_point<<<std::max(1, occ_p) * h->num_sms, PTP_THREADS, 0, cs>>>(d, g);
     if (d.topo.nt) {
       if (fac) k_g_camera<true><<<std::max(1, occ_c) * h->num_sms, PCG_THREADS, 0, cs>>>(d, g);
       else k_g_camera<false><<<std::max(1, occ_c) * h->num_sms, PCG_THREADS, 0, cs>>>(d, g);
@@ -1615,24 +1830,34 @@ extern "C" int ssfm_bench_operator(ssfm_handle* h, int32_t which, int32_t reps, 
   cudaStream_t st = (cudaStream_t)stream;
   BADev& d = h->ba;
   const bool fac = d.Fcm != nullptr;
-  const void* fn = which == 0 ? (const void*)k_op_point
+  const void* fn = which != 1 ? (const void*)k_op_point
                               : (fac ? (const void*)k_op_camera<true> : (const void*)k_op_camera<false>);
   int occ = 0;
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, PCG_THREADS, 0));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, which != 1 ? PTP_THREADS : PCG_THREADS, 0));
   const int grid = std::max(1, occ) * h->num_sms;
+  int occ2 = 0;
+  const void* fn2 = fac ? (const void*)k_op_camera<true> : (const void*)k_op_camera<false>;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, fn2, PCG_THREADS, 0));
+  const int grid2 = std::max(1, occ2) * h->num_sms;
   auto run = [&]() {
     if (which == 0) {
-      k_op_point<<<grid, PCG_THREADS, 0, st>>>(d, h->p, d.yv);
+      k_op_point<<<grid, PTP_THREADS, 0, st>>>(d, h->p, d.yv);
+    } else if (which == 2) {   // the operator's two passes back to back (as in the PCG)
+      k_op_point<<<grid, PTP_THREADS, 0, st>>>(d, h->p, d.yv);
+      if (fac) k_op_camera<true><<<grid2, PCG_THREADS, 0, st>>>(d, d.yv, d.tilebuf);
+      else k_op_camera<false><<<grid2, PCG_THREADS, 0, st>>>(d, d.yv, d.tilebuf);
     } else {
       if (fac) k_op_camera<true><<<grid, PCG_THREADS, 0, st>>>(d, d.yv, d.tilebuf);
       else k_op_camera<false><<<grid, PCG_THREADS, 0, st>>>(d, d.yv, d.tilebuf);
     }
   };
+  const bool win = set_l2_window(h, st, d.yv, sizeof(double) * 4 * (size_t)d.bp.P);
   for (int w = 0; w < 2; ++w) run();   // warm-up
   CU(cudaEventRecord(h->ev0, st));
   for (int k = 0; k < reps; ++k) run();
   CU(cudaEventRecord(h->ev1, st));
   CU(cudaEventSynchronize(h->ev1));
+  if (win) clear_l2_window(st);
   float ms = 0.f;
   CU(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
   *ms_out = ms / reps;

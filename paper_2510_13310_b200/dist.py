@@ -90,14 +90,14 @@ class _Sharded:
             _native.check(lib.ssfm_comm_connect(ct.c_void_p(h.ptr), ct.c_char_p(b"".join(handles)), None))
             self._connected = True
 
-    def _create(self):
-        h = super()._create()
+    def _create(self, arena=None):
+        h = super()._create(arena)
         self._native_ptr = h
         self._connect_torch(h)
         return h
 
-    def _native_handle(self):
-        h = super()._native_handle()
+    def _native_handle(self, workspace=None):
+        h = super()._native_handle(workspace)
         if not self._connected:
             raise RuntimeError("sharded problem not connected: call connect_local(problems) first")
         return h

@@ -79,13 +79,29 @@ class SolveReport:
 class Workspace:
     """Grow-only scratch arena shared across solver stages (lm.py:86-101).
 
-    Host arrays handed out by `take` mirror the reference; device memory for
-    native problems lives in the problem handle's arena.
+    Host arrays handed out by `take` mirror the reference. The device side is
+    a grow-only HBM arena (`device_arena`, csrc: ssfm_arena): a native problem
+    whose handle is first created through lm_solve / run_ba / run_gp with this
+    workspace allocates from it, and once that problem is released the next
+    stage's problem (GP -> BA) reuses the same HBM without cudaMalloc.
     """
 
     def __init__(self):
         self._arrays: dict = {}
         self.caches: dict = {}
+        self._arena = None
+
+    def device_arena(self):
+        if self._arena is None:
+            from . import _native
+            self._arena = _native.Arena()
+        return self._arena
+
+    def release_device(self) -> None:
+        """Free the device arena (every problem created in it must be released)."""
+        if self._arena is not None:
+            self._arena.close()
+            self._arena = None
 
     def take(self, name: str, shape, dtype=np.float64) -> np.ndarray:
         if isinstance(shape, (int, np.integer)):
@@ -155,7 +171,7 @@ def lm_solve(problem, theta0, config: LMConfig | None = None,
         raise DimensionMismatch("theta0 length does not match the problem layout")
     if not bool(torch.isfinite(theta).all()):
         raise ValueError("theta0 must be finite")
-    h = native()
+    h = native(workspace) if workspace is not None else native()
     lib = _native.load()
     cap = max(1, int(config.max_iterations))
     recs = (_native.IterRecordC * cap)()
