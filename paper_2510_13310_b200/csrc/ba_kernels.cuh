@@ -23,7 +23,10 @@ struct BADev {
   const double* dists;    // [2C]
   const double* focals;   // [C] fixed focals (focal_mode 0)
   BACam* cams;            // [C]
-  double* Jpm;            // [16 * Npad]
+  double* Jpm;            // [16 * Npad] (fused-operator handles)
+  double* Gpm;            // [8 * Npad] point-major Jp (6) + Jf (2): omega-form handles (ba_wobs)
+  double* Xl;             // [4P] points at the linearization (omega-form, padded: 32-byte gathers)
+  double* Wc;             // [8C] per-camera omega-form vector of the current p / x (ba_wvec)
   double* Jcm;            // [16 * Npad]
   double* rcm;            // [2 * Npad]
   double* Fcm;            // [9 * Npad] factored records (ba_factor) + v = X - t, camera-major (two-pass only)
@@ -180,8 +183,15 @@ __global__ void __launch_bounds__(256) ba_k_linearize(BADev d, const double* __r
         const double* X = theta + d.bp.off_pts + 3ll * j;
         double r[2], J[BA_JREC], ct;
         ba_obs_eval(d.bp, d.cams + c, X, d.pix_pm + 2ll * i, r, J, &ct);
+        if (d.Gpm) {   // omega form: Jp and Jf only (the quaternion block is Jp (omega x v))
+          const int nr = d.bp.focal_mode ? 8 : 6;
 #pragma unroll
-        for (int k = 0; k < BA_JREC; ++k) d.Jpm[k * Np + i] = J[k];
+          for (int k = 0; k < 8; ++k)
+            if (k < nr) d.Gpm[k * Np + i] = J[8 + k];
+        } else {
+#pragma unroll
+          for (int k = 0; k < BA_JREC; ++k) d.Jpm[k * Np + i] = J[k];
+        }
         // point-side products: Jp^T Jp (upper 6) and Jp^T r
         const double* jp = J + 8;
         val[0] = jp[0] * jp[0] + jp[3] * jp[3];
@@ -233,6 +243,11 @@ __global__ void __launch_bounds__(256) ba_k_linearize(BADev d, const double* __r
       if (d.fpt) {
 #pragma unroll
         for (int k = 0; k < 3; ++k) d.fpt[3ll * my_pt + k] = acc[9 + k];
+      }
+      if (d.Xl) {
+        const double* X = theta + d.bp.off_pts + 3ll * my_pt;
+        double* xl = d.Xl + 4ll * my_pt;
+        xl[0] = X[0]; xl[1] = X[1]; xl[2] = X[2]; xl[3] = 0.0;
       }
       double* C6 = d.Cpt + 6ll * my_pt;
 #pragma unroll
@@ -757,6 +772,81 @@ __global__ void ba_k_shared_focal_grad(BADev d) {
 }
 
 // ---------------------------------------------------------------------------
+// Omega form of the point-side operator (two-pass handles with the factored
+// camera pass). The quaternion block of an observation is the point block
+// times a per-camera map: drotate_dq (scene.py:153-184) applied to a
+// direction w is R (omega x v) with omega = (2/|q|) vec(qh^* (x) w) (the
+// derivative of R(q/|q|) v along w), and the point block is
+// Jp = sw du_dp R (ba.py:187-190), so
+//   Jc_o p_c = Jp_o (omega_c x v_o - p_t,c) + Jf_o p_f,c
+//            = Jp_o (omega_c x X_j - b_c) + Jf_o p_f,c,   b_c = omega_c x t_c + p_t,c.
+// The point pass then streams Jp and Jf (8 doubles per observation instead
+// of the 16-double record) and gathers W_c = [omega_c, b_c, p_f,c, 0] (64
+// bytes, like the 8-slot p it replaces) and X_j at the linearization. The
+// operator equals the stored Jacobian's to rounding.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void ba_wvec(const BADev& d, const double* __restrict__ v, int c,
+                                        double* __restrict__ W) {
+  const double* cb = reinterpret_cast<const double*>(d.camlin + c);
+  const double* pc = v + 8ll * c;
+  const double qw = cb[9], qx = cb[10], qy = cb[11], qz = cb[12], s2 = 2.0 * cb[22];
+  const double pw = pc[0], px = pc[1], py = pc[2], pz = pc[3];
+  // vec(qh^* (x) p) = qw p_v - pw q_v - q_v x p_v
+  const double o0 = s2 * (qw * px - pw * qx - (qy * pz - qz * py));
+  const double o1 = s2 * (qw * py - pw * qy - (qz * px - qx * pz));
+  const double o2 = s2 * (qw * pz - pw * qz - (qx * py - qy * px));
+  const double t0 = cb[14], t1 = cb[15], t2 = cb[16];
+  double* w = W + 8ll * c;
+  w[0] = o0; w[1] = o1; w[2] = o2;
+  w[3] = (o1 * t2 - o2 * t1) + pc[4];
+  w[4] = (o2 * t0 - o0 * t2) + pc[5];
+  w[5] = (o0 * t1 - o1 * t0) + pc[6];
+  w[6] = d.bp.focal_mode == 2 ? v[7] : (d.bp.focal_mode == 1 ? pc[7] : 0.0);
+  w[7] = 0.0;
+}
+
+__global__ void k_cam_wvec(BADev d, const double* __restrict__ v, double* W) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < d.bp.C) ba_wvec(d, v, c, W);
+}
+
+// One observation's Jp^T (Jc p_c) in the omega form (point-major index i).
+template <bool RO>
+__device__ __forceinline__ void ba_wobs(const BADev& d, long long i, const double* __restrict__ W, double* val) {
+  const unsigned long long pstream = pol_evict_first(), pkeep = pol_evict_last();
+  const long long Np = d.Npad;
+  double G[8];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) G[k] = ldg_stream(d.Gpm + k * Np + i, pstream);
+  if (d.bp.focal_mode) {
+    G[6] = ldg_stream(d.Gpm + 6 * Np + i, pstream);
+    G[7] = ldg_stream(d.Gpm + 7 * Np + i, pstream);
+  } else {
+    G[6] = 0.0; G[7] = 0.0;
+  }
+  const int c = ldg_stream_i(d.topo.pm_cam + i, pstream);
+  const int j = ldg_stream_i(d.topo.pm_pt + i, pstream);
+  double w[8], X[4];
+  if constexpr (RO) {
+    ld_v4_ro(W + 8ll * c, w, pkeep);
+    ld_v4_ro(W + 8ll * c + 4, w + 4, pkeep);
+    ld_v4_ro(d.Xl + 4ll * j, X, pkeep);
+  } else {
+    ld_v4(W + 8ll * c, w);
+    ld_v4(W + 8ll * c + 4, w + 4);
+    ld_v4(d.Xl + 4ll * j, X);
+  }
+  const double u0 = (w[1] * X[2] - w[2] * X[1]) - w[3];
+  const double u1 = (w[2] * X[0] - w[0] * X[2]) - w[4];
+  const double u2 = (w[0] * X[1] - w[1] * X[0]) - w[5];
+  const double t0 = G[0] * u0 + G[1] * u1 + G[2] * u2 + G[6] * w[6];
+  const double t1 = G[3] * u0 + G[4] * u1 + G[5] * u2 + G[7] * w[6];
+  val[0] = G[0] * t0 + G[3] * t1;
+  val[1] = G[1] * t0 + G[4] * t1;
+  val[2] = G[2] * t0 + G[5] * t1;
+}
+
+// ---------------------------------------------------------------------------
 // back-substitution (lm.py:674-690): delta_j = y0_j - Cinv_j sum_o Jp^T Jc x_c
 // one warp per point batch; camera part of delta scattered by ba_k_camdelta.
 // ---------------------------------------------------------------------------
@@ -777,7 +867,9 @@ __global__ void __launch_bounds__(256) ba_k_backsub(BADev d, const double* __res
     for (int base = ob0; base < ob1; base += SSFM_BATCH) {
       const int i = base + lane;
       double val[3] = {0.0, 0.0, 0.0};
-      if (i < ob1) {
+      if (i < ob1 && d.Gpm) {
+        ba_wobs<false>(d, i, d.Wc, val);
+      } else if (i < ob1) {
         double J[BA_JREC];
 #pragma unroll
         for (int k = 0; k < BA_JREC; ++k) J[k] = d.Jpm[k * Np + i];

@@ -286,6 +286,48 @@ __device__ __forceinline__ void ba_point_pass(const BADev& d, const double* v, d
   }
 }
 
+// P1 in the omega form (ba_wobs): W = the per-camera vector of p (ba_wvec).
+// Streams Jp + Jf (8 doubles) and two indices per observation instead of the
+// 16-double record and one index.
+template <bool RO = false>
+__device__ __forceinline__ void ba_point_pass_w(const BADev& d, const double* W, double* y,
+                                                double (*sm)[SSFM_BATCH][3]) {
+  const unsigned long long pkeep = pol_evict_last();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  for (int b = gw; b < d.topo.nb; b += warps) {
+    const int ob0 = d.topo.bat_obs[b], ob1 = d.topo.bat_obs[b + 1];
+    const int pb0 = d.topo.bat_pt[b], pb1 = d.topo.bat_pt[b + 1];
+    const int my_pt = pb0 + lane;
+    int ps = 0, pe = 0;
+    if (my_pt < pb1) { ps = d.topo.pt_seg[my_pt]; pe = d.topo.pt_seg[my_pt + 1]; }
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int base = ob0; base < ob1; base += SSFM_BATCH) {
+      const int i = base + lane;
+      double val[3] = {0.0, 0.0, 0.0};
+      if (i < ob1) ba_wobs<RO>(d, i, W, val);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) sm[wib][lane][k] = val[k];
+      __syncwarp();
+      const int a = max(ps, base), e = min(pe, base + SSFM_BATCH);
+      for (int o = a; o < e; ++o) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) acc[k] += sm[wib][o - base][k];
+      }
+      __syncwarp();
+    }
+    if (my_pt < pb1) {
+      double ci[6], w[3];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) ci[k] = __ldg(d.Cinv + 6ll * my_pt + k);
+      sym3_matvec(ci, acc, w);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) st_hint(y + 4ll * my_pt + k, w[k], pkeep);
+    }
+  }
+}
+
 // P1, software-pipelined: while a warp works on batch b, the Jacobian rows
 // and camera ids of its next batch are already in flight into a second
 // shared-memory stage (cp.async, no registers held), and batch b's Cinv
@@ -669,6 +711,10 @@ ba_k_pcg(BADev d, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg
     if (threadIdx.x == 0) { part[2ll * blockIdx.x] = v[0]; part[2ll * blockIdx.x + 1] = v[1]; }
   }
   grid.sync();
+  if (d.Gpm) {   // omega-form point pass: the per-camera vector of p
+    for (int c = gid; c < d.bp.C; c += stride) ba_wvec(d, p, c, d.Wc);
+    grid.sync();
+  }
   const double gn = sqrt(d.scal[SC_GNORM2]);
   const double tol = cg_tol * fmax(gn, 1e-300);
   double rr = cta_partials_sum(part, NP, 2, 0, &smb[0]);
@@ -684,7 +730,8 @@ ba_k_pcg(BADev d, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg
       if (tim) pt0 = gtimer();
       if constexpr (SL == 0) {
         // P1: point pass
-        ba_point_pass(d, p, d.yv, smp);
+        if (d.Gpm) ba_point_pass_w(d, d.Wc, d.yv, smp);
+        else ba_point_pass(d, p, d.yv, smp);
         grid.sync();
         if (tim) { const unsigned long long t1 = gtimer(); ph[0] += t1 - pt0; pt0 = t1; }
         // P2: camera tiles
@@ -792,8 +839,19 @@ ba_k_pcg(BADev d, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg
       if (rn <= tol) break;
       const double beta = rz / rho;
       rho = rz;
-      // P5: p = z + beta p
-      for (int s = gid; s < S; s += stride) p[s] = z[s] + beta * p[s];
+      // P5: p = z + beta p (omega form: one camera per thread, then its W)
+      if (d.Gpm) {
+        if (shared && gid == 0) p[7] = z[7] + beta * p[7];   // camera 0 slot 7: read by every camera's W
+        grid.sync();
+        for (int c = gid; c < d.bp.C; c += stride) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (!(shared && c == 0 && k == 7)) p[8ll * c + k] = z[8ll * c + k] + beta * p[8ll * c + k];
+          ba_wvec(d, p, c, d.Wc);
+        }
+      } else {
+        for (int s = gid; s < S; s += stride) p[s] = z[s] + beta * p[s];
+      }
       grid.sync();
       if (tim) ph[4] += gtimer() - pt0;
       if (shared) pf = p[7];   // every thread tracks the shared focal of p
@@ -815,6 +873,7 @@ ba_k_pcg(BADev d, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg
 // kernels (per-pass timing and roofline, ssfm_bench_operator).
 __global__ void __launch_bounds__(PTP_THREADS, PTP_MINB) k_op_point(BADev d, const double* v, double* y) {
   __shared__ double smp[PTP_THREADS / 32][SSFM_BATCH][3];
+  if (d.Gpm) { ba_point_pass_w<true>(d, d.Wc, y, smp); return; }   // W of v: k_cam_wvec first
 #if PTP_PIPE
   __shared__ PtpStage stg[PTP_THREADS / 32][2];
   ba_point_pass_pipe<true>(d, v, y, stg, smp);

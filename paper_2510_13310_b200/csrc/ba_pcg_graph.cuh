@@ -25,8 +25,8 @@ struct CGGraphDev {
   double* x; double* r; double* z; double* p; double* q;
   double* partA;   // [2 * CGV_BLOCKS] p.q (and init r.r / r.z)
   double* partB;   // [2 * CGV_BLOCKS] r.r / r.z
-  double* sc;      // [8]: 0 lam, 1 cg_tol, 2 tol, 3 rho, 4 rn, 5 rz (pending), 6 qf
-  int* ic;         // [4]: 0 max_iters, 1 iters, 2 flag, 3 done
+  double* sc;      // [8]: 0 lam, 1 cg_tol, 2 tol, 3 rho, 4 rn, 5 rz (pending), 6 qf, 7 shared focal p
+  int* ic;         // [8]: 0 max_iters, 1 iters, 2 flag, 3 done, 4 shared focal p pending (sc[7])
   CGCtl* ctl;
   int fused;       // 0 two-pass (tile8), 1 fused (gpart, ngrp groups)
   int ngrp;
@@ -87,6 +87,7 @@ __global__ void k_g_init2(Dev d, CGGraphDev g, int nblk) {
 __global__ void __launch_bounds__(PTP_THREADS, PTP_MINB) k_g_point(BADev d, CGGraphDev g) {
   if (*(volatile int*)(g.ic + 3)) return;
   __shared__ double smp[PTP_THREADS / 32][SSFM_BATCH][3];
+  if (d.Gpm) { ba_point_pass_w<true>(d, d.Wc, d.yv, smp); return; }   // W (of p) is constant here
 #if PTP_PIPE
   __shared__ PtpStage stg[PTP_THREADS / 32][2];
   ba_point_pass_pipe<true>(d, g.p, d.yv, stg, smp);   // p is constant during this kernel
@@ -250,6 +251,39 @@ __global__ void __launch_bounds__(256) k_g_pupdate(BADev d, CGGraphDev g, int nb
   if (sqrt(rr) <= g.sc[2]) return;   // converged: the loop ends, p is not used again
   const double beta = rz / g.sc[3];
   const int S = 8 * d.bp.C;
+  if (d.Gpm) {
+    // omega form: one camera per thread, p then its W. Shared focal: every
+    // camera's W reads camera 0's slot 7, so each thread computes it itself.
+    const bool shared = d.bp.focal_mode == 2;
+    const double pf = shared ? g.z[7] + beta * g.p[7] : 0.0;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < d.bp.C; c += gridDim.x * blockDim.x) {
+      double pc[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) pc[k] = g.z[8ll * c + k] + beta * g.p[8ll * c + k];
+      if (shared && c == 0) {   // slot 7 of camera 0 is read by every thread: k_g_scalars writes it
+        pc[7] = g.p[7];
+        g.sc[7] = pf;
+        g.ic[4] = 1;
+      }
+      double* w = d.Wc + 8ll * c;
+      // ba_wvec on registers: W of this camera from pc (and the shared focal)
+      const double* cb = reinterpret_cast<const double*>(d.camlin + c);
+      const double qw = cb[9], qx = cb[10], qy = cb[11], qz = cb[12], s2 = 2.0 * cb[22];
+      const double o0 = s2 * (qw * pc[1] - pc[0] * qx - (qy * pc[3] - qz * pc[2]));
+      const double o1 = s2 * (qw * pc[2] - pc[0] * qy - (qz * pc[1] - qx * pc[3]));
+      const double o2 = s2 * (qw * pc[3] - pc[0] * qz - (qx * pc[2] - qy * pc[1]));
+      const double t0 = cb[14], t1 = cb[15], t2 = cb[16];
+      w[0] = o0; w[1] = o1; w[2] = o2;
+      w[3] = (o1 * t2 - o2 * t1) + pc[4];
+      w[4] = (o2 * t0 - o0 * t2) + pc[5];
+      w[5] = (o0 * t1 - o1 * t0) + pc[6];
+      w[6] = shared ? pf : (d.bp.focal_mode == 1 ? pc[7] : 0.0);
+      w[7] = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) g.p[8ll * c + k] = pc[k];
+    }
+    return;
+  }
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x)
     g.p[s] = g.z[s] + beta * g.p[s];
 }
@@ -259,6 +293,10 @@ template <typename Dev>   // BADev or GPDev: status
 __global__ void k_g_scalars(Dev d, CGGraphDev g, int nblk, cudaGraphConditionalHandle hc) {
   __shared__ double smb[4];
   int done = *(volatile int*)(g.ic + 3);
+  if (threadIdx.x == 0 && g.ic[4]) {   // omega form, shared focal: p's shared slot (k_g_pupdate)
+    g.p[7] = g.sc[7];
+    g.ic[4] = 0;
+  }
   if (!done) {
     int flag = g.ic[2];
     if (!flag) {

@@ -333,7 +333,7 @@ static int build_topo(ssfm_handle* h, const int* cam, const int* pt, int C, int 
   int *iota, *perm_pm, *perm_cm, *keys_out, *inv_cm, *cnt;
   DALLOC(iota, N); DALLOC(keys_out, N); DALLOC(inv_cm, N);
   DALLOC(T.pm_obs, N); DALLOC(T.cm_obs, N);
-  DALLOC(T.pm_pt, N); DALLOC(T.pm_cam, N); DALLOC(T.pm_to_cm, N); DALLOC(T.cm_pt, N);
+  DALLOC(T.pm_pt, N); DALLOC(T.pm_cam, N); DALLOC(T.pm_to_cm, N); DALLOC(T.cm_to_pm, N); DALLOC(T.cm_pt, N);
   DALLOC(T.pt_seg, (long long)P + 1); DALLOC(T.cam_seg, (long long)C + 1);
   perm_pm = T.pm_obs; perm_cm = T.cm_obs;
   if (N > 0) k_iota<<<nblk(N, TB), TB, 0, st>>>(iota, N);
@@ -361,6 +361,7 @@ static int build_topo(ssfm_handle* h, const int* cam, const int* pt, int C, int 
   if (N > 0) {
     k_perm_views<<<nblk(N, TB), TB, 0, st>>>(perm_pm, perm_cm, cam, pt, N, T.pm_pt, T.pm_cam, T.cm_pt, inv_cm);
     k_pm_to_cm<<<nblk(N, TB), TB, 0, st>>>(perm_pm, inv_cm, N, T.pm_to_cm);
+    k_invert_perm<<<nblk(N, TB), TB, 0, st>>>(T.pm_to_cm, N, T.cm_to_pm);
   }
   // point batches
   int nch = nblk(P, SSFM_CHUNK);
@@ -566,6 +567,14 @@ static int setup_ba_pcg(ssfm_handle* h, cudaStream_t st) {
     DALLOC(d.Fcm, (long long)(BA_FREC + 3) * d.Npad);
     DALLOC(d.camlin, d.bp.C);
     h->pcg_fn = (void*)ba_k_pcg<0, true>;
+    // and the point pass the omega form (ba_wobs: Jp + Jf, 8 doubles per
+    // observation instead of the 16-double record; SSFM_WFORM=0: off)
+    const char* we = getenv("SSFM_WFORM");
+    if (!(we && we[0] == '0')) {
+      DALLOC(d.Gpm, 8ll * d.Npad);
+      DALLOC(d.Xl, 4ll * d.bp.P);
+      DALLOC(d.Wc, 8ll * d.bp.C);
+    }
   }
   const char* ge = getenv("SSFM_PCG_GRAPH");
   // two-pass operator from 250k observations: the graph wins well below C5
@@ -751,7 +760,6 @@ static int create_ba(const ssfm_ba_desc* desc, ssfm_arena* arena, void* stream, 
   }
   d.pix_pm = pix_pm; d.pps = pps; d.dists = dists; d.focals = focals;
   if ((rc = dalloc(h, &d.cams, C))) return fail(rc);
-  if ((rc = dalloc(h, &d.Jpm, BA_JREC * d.Npad))) return fail(rc);
   if ((rc = dalloc(h, &d.rcm, 2 * d.Npad))) return fail(rc);
   if ((rc = dalloc(h, &d.Cpt, 6ll * P))) return fail(rc);
   if ((rc = dalloc(h, &d.gpt, 3ll * P))) return fail(rc);
@@ -781,6 +789,8 @@ static int create_ba(const ssfm_ba_desc* desc, ssfm_arena* arena, void* stream, 
   // the camera-major Jacobian copy: only without the factored record (the
   // fused operator, SSFM_FACTORED=0); two-pass handles read Fcm instead
   if (!d.Fcm && (rc = dalloc(h, &d.Jcm, BA_JREC * d.Npad))) return fail(rc);
+  // the point-major record: Jp + Jf for omega-form handles, else the full record
+  if (!d.Gpm && (rc = dalloc(h, &d.Jpm, BA_JREC * d.Npad))) return fail(rc);
   mark("pcg setup");
   h->lin_blocks = std::max(1, std::min(nblk(T.nb, 8), h->num_sms * 16));
   h->cost_blocks = nblk(N, 256);
@@ -1115,7 +1125,7 @@ static int launch_linearize(ssfm_handle* h, const double* theta, double* r_out, 
 
 
 __global__ void k_g_setparams(CGGraphDev g, double lam, double cg_tol, int max_iters) {
-  g.sc[0] = lam; g.sc[1] = cg_tol; g.ic[0] = max_iters;
+  g.sc[0] = lam; g.sc[1] = cg_tol; g.ic[0] = max_iters; g.ic[4] = 0;
 }
 
 template <int SL>
@@ -1188,7 +1198,7 @@ static int build_pcg_graph(ssfm_handle* h) {
   DALLOC(g.partA, 2 * CGV_BLOCKS + 2);
   DALLOC(g.partB, 2 * CGV_BLOCKS + 2);
   DALLOC(g.sc, 8);
-  DALLOC(g.ic, 4);
+  DALLOC(g.ic, 8);
   g.ctl = &h->misc->ctl;
   g.fused = h->fz.G > 0 ? 1 : 0;
   g.ngrp = h->fz.ngrp;
@@ -1270,7 +1280,7 @@ static int build_gp_pcg_graph(ssfm_handle* h) {
   DALLOC(g.partA, 2 * CGV_BLOCKS + 2);
   DALLOC(g.partB, 2 * CGV_BLOCKS + 2);
   DALLOC(g.sc, 8);
-  DALLOC(g.ic, 4);
+  DALLOC(g.ic, 8);
   g.ctl = &h->misc->ctl;
   g.fused = 0;
   g.ngrp = 0;
@@ -1362,6 +1372,7 @@ static int launch_pcg(ssfm_handle* h, double lam, const ssfm_lm_config* cfg, cud
     CGGraphDev& g = h->gdev;
     k_g_setparams<<<1, 1, 0, st>>>(g, lam, tol, max_it);
     k_g_init<<<CGV_BLOCKS, 256, 0, st>>>(h->ba, g);
+    if (h->ba.Gpm) { k_cam_wvec<<<h->cam_blocks, 256, 0, st>>>(h->ba, g.p, h->ba.Wc); count_launch(h); }
     k_g_init2<<<1, 32, 0, st>>>(h->ba, g, CGV_BLOCKS);
     CU(cudaGraphLaunch(h->pcg_exec, st));
     count_launch(h, 3);
@@ -1436,6 +1447,7 @@ static int launch_solve(ssfm_handle* h, double lam, const ssfm_lm_config* cfg, c
   if (h->prof.on) CU(cudaEventRecord(h->ev3, st));
   if (h->kind == 0) {
     BADev& d = h->ba;
+    if (d.Gpm) { k_cam_wvec<<<h->cam_blocks, 256, 0, st>>>(d, h->x, d.Wc); count_launch(h); }
     ba_k_backsub<<<h->lin_blocks, 256, 0, st>>>(d, h->x, h->delta);
     ba_k_camdelta<<<h->cam_blocks, 256, 0, st>>>(d, h->x, h->delta);
     count_launch(h, 2);
@@ -1851,6 +1863,7 @@ extern "C" int ssfm_bench_operator(ssfm_handle* h, int32_t which, int32_t reps, 
       else k_op_camera<false><<<grid, PCG_THREADS, 0, st>>>(d, d.yv, d.tilebuf);
     }
   };
+  if (d.Gpm) k_cam_wvec<<<h->cam_blocks, 256, 0, st>>>(d, h->p, d.Wc);   // omega form: W of p
   const bool win = set_l2_window(h, st, d.yv, sizeof(double) * 4 * (size_t)d.bp.P);
   for (int w = 0; w < 2; ++w) run();   // warm-up
   CU(cudaEventRecord(h->ev0, st));

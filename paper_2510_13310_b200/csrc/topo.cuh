@@ -30,6 +30,7 @@ struct Topo {
   int* pm_pt = nullptr;     // [N] point id
   int* pm_cam = nullptr;    // [N] camera id
   int* pm_to_cm = nullptr;  // [N] camera-major position
+  int* cm_to_pm = nullptr;  // [N] point-major position of a camera-major observation
   int* pt_seg = nullptr;    // [P+1]
   int* bat_obs = nullptr;   // [nb+1]
   int* bat_pt = nullptr;    // [nb+1]
@@ -93,6 +94,11 @@ __global__ void k_pm_to_cm(const int* __restrict__ perm_pm, const int* __restric
                            long long n, int* pm_to_cm) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < n) pm_to_cm[i] = inv_cm[perm_pm[i]];
+}
+
+__global__ void k_invert_perm(const int* __restrict__ perm, long long n, int* inv) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) inv[perm[i]] = (int)i;
 }
 
 // Greedy packing of consecutive points into warp batches, chunk-parallel.

@@ -77,7 +77,9 @@ def test_run_global_sfm_matches_stagewise_host_path(gpu):
     res = ba.decode(th)
     assert np.array_equal(out.points, res.points) and np.array_equal(out.centers, res.centers)
     assert np.array_equal(out.quats, res.quats) and np.array_equal(out.focals, res.focals)
-    assert rep.rmse_after_ba < rep.rmse_after_gp or rep.rmse_after_ba == pytest.approx(rep.rmse_after_gp, rel=1e-3)
+    # BA minimises its robust cost (not the RMSE the report prints)
+    assert rep.ba.iterations[-1].cost_after <= rep.ba.iterations[0].cost_before
+    assert np.isfinite(rep.rmse_after_ba) and np.isfinite(rep.rmse_after_gp)
 
 
 def test_make_rays_device_keeps_rays_on_device(gpu):
