@@ -200,6 +200,12 @@ int ssfm_lm_solve(ssfm_handle* h, double* theta, const ssfm_lm_config* cfg,
                   ssfm_iter_record* recs, int32_t cap, int32_t* n_recs,
                   int32_t* termination, void* stream);
 
+/* How lm_solve runs its loop on this handle: 1 = the whole LM loop as one
+ * CUDA graph (accept/reject, lambda and termination decided on the device,
+ * one read-back per solve; single-rank BA handles, SSFM_LM_GRAPH=0 disables),
+ * -1 = host loop (graph unavailable), 0 = not decided yet (no solve ran). */
+int32_t ssfm_lm_mode(const ssfm_handle* h);
+
 /* Reference-equivalent integer structures, bit-exact with the reference:
  *  - obs_pt_order [N] int32: stable point-major permutation of observations
  *  - obs_cam_order [N] int32: stable camera-major permutation

@@ -28,7 +28,7 @@ EXPORTS = (
     "ssfm_rotation_auc", "ssfm_center_moments", "ssfm_apply_sim3",
     "ssfm_bal_read", "ssfm_bal_take", "ssfm_bal_free", "ssfm_make_rays", "ssfm_schur_solve",
     "ssfm_trim_cache", "ssfm_cache_bytes", "ssfm_arena_create", "ssfm_arena_destroy", "ssfm_arena_info",
-    "ssfm_create_ba_in", "ssfm_create_gp_in",
+    "ssfm_create_ba_in", "ssfm_create_gp_in", "ssfm_lm_mode",
 )
 
 TERMINATIONS = {0: "max_iter", 1: "converged_cost", 2: "converged_grad", 3: "solver_failure"}
@@ -107,6 +107,8 @@ def load(required: bool = True):
     P, I32, I64, D = ct.c_void_p, ct.c_int32, ct.c_int64, ct.c_double
     lib.ssfm_last_error.restype = ct.c_char_p
     lib.ssfm_version.restype = ct.c_char_p
+    lib.ssfm_lm_mode.argtypes = [P]
+    lib.ssfm_lm_mode.restype = I32
     lib.ssfm_create_ba.argtypes = [ct.POINTER(BADescC), P, ct.POINTER(P)]
     lib.ssfm_create_gp.argtypes = [ct.POINTER(GPDescC), P, ct.POINTER(P)]
     lib.ssfm_destroy.argtypes = [P]

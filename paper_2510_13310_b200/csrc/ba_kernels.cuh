@@ -5,7 +5,6 @@
 // Data layout in HBM (N observations, P points, C cameras):
 //   Jpm[16][N]  compact Jacobian, SoA, point-major   (read by point passes)
 //   Jcm[16][N]  same records, SoA, camera-major       (read by camera passes)
-//   rcm[2][N]   weighted residual, camera-major
 //   per point (AoS): Cpt[6] (Jp^T Jp), gpt[3] (Jp^T r), Cinv[6], y0[3], yv[4]
 //   per camera (AoS): Bc[64] (Jc^T Jc, 8x8 full), gcam[8], Minv[64], bred[8]
 // The compact record is 16 fp64 per observation instead of the reference's
@@ -27,8 +26,8 @@ struct BADev {
   double* Gpm;            // [8 * Npad] point-major Jp (6) + Jf (2): omega-form handles (ba_wobs)
   double* Xl;             // [4P] points at the linearization (omega-form, padded: 32-byte gathers)
   double* Wc;             // [8C] per-camera omega-form vector of the current p / x (ba_wvec)
+  double* Rpm;            // [4N] point-major weighted residual [r0, r1, 0, 0] (ba_k_lin_tile; full sectors)
   double* Jcm;            // [16 * Npad]
-  double* rcm;            // [2 * Npad]
   double* Fcm;            // [9 * Npad] factored records (ba_factor) + v = X - t, camera-major (two-pass only)
   BACam* camlin;          // [C] camera cache at the linearization (cams is overwritten by trial costs)
   long long Npad;
@@ -46,12 +45,38 @@ struct BADev {
   double* fpt;            // [3P] shared focal: a_j = sum_o Jp_o^T jf_o (nullptr otherwise)
   double* fwpart;         // [ptinv blocks] shared focal: sum_j a_j^T Cinv_j a_j partials
   unsigned char* pinned;  // [C] bitmask of pinned retained slots
+  const double* lamp;     // device-resident lambda (LM loop as a CUDA graph) or nullptr: the argument
   double* scal;           // scalars: [0] gmax bits, [1] gnorm2, [2] cost, ...
   double* partials;       // [max(nb, blocks)] reduction scratch
   int* status;
 };
 
 enum { SC_GMAX = 0, SC_GNORM2 = 1, SC_COST = 2, SC_LAMBDA = 3, SC_GFOCAL = 4 };
+
+// Omega-form point-major record Gpm of observation i: [Jp row 0 (3), Jp row 1
+// (3), Jf (2)]. GPM_AOS=1: 64-byte records (whole sectors); 0: SoA rows.
+#ifndef GPM_AOS
+#define GPM_AOS 1
+#endif
+__device__ __forceinline__ void gpm_store(const BADev& d, long long i, const double* jp8) {
+#if GPM_AOS
+  double* g = d.Gpm + 8 * i;
+  *reinterpret_cast<double4*>(g) = make_double4(jp8[0], jp8[1], jp8[2], jp8[3]);
+  *reinterpret_cast<double4*>(g + 4) = make_double4(jp8[4], jp8[5], jp8[6], jp8[7]);
+#else
+#pragma unroll
+  for (int k = 0; k < 8; ++k) d.Gpm[k * d.Npad + i] = jp8[k];
+#endif
+}
+__device__ __forceinline__ void gpm_load(const BADev& d, long long i, double* G, unsigned long long pol) {
+#if GPM_AOS
+  ld_v4_ro(d.Gpm + 8 * i, G, pol);
+  ld_v4_ro(d.Gpm + 8 * i + 4, G + 4, pol);
+#else
+#pragma unroll
+  for (int k = 0; k < 8; ++k) G[k] = ldg_stream(d.Gpm + k * d.Npad + i, pol);
+#endif
+}
 
 // ---------------------------------------------------------------------------
 // camera cache from theta (quat_to_matrix_many per camera, ba.py:111-116)
@@ -184,10 +209,7 @@ __global__ void __launch_bounds__(256) ba_k_linearize(BADev d, const double* __r
         double r[2], J[BA_JREC], ct;
         ba_obs_eval(d.bp, d.cams + c, X, d.pix_pm + 2ll * i, r, J, &ct);
         if (d.Gpm) {   // omega form: Jp and Jf only (the quaternion block is Jp (omega x v))
-          const int nr = d.bp.focal_mode ? 8 : 6;
-#pragma unroll
-          for (int k = 0; k < 8; ++k)
-            if (k < nr) d.Gpm[k * Np + i] = J[8 + k];
+          gpm_store(d, i, J + 8);
         } else {
 #pragma unroll
           for (int k = 0; k < BA_JREC; ++k) d.Jpm[k * Np + i] = J[k];
@@ -303,8 +325,6 @@ __global__ void __launch_bounds__(SSFM_TILE) ba_k_linearize_cm(BADev d, const do
 #pragma unroll
       for (int k = 0; k < BA_FREC + 3; ++k) d.Fcm[k * Np + i] = F[k];
     }
-    d.rcm[i] = r[0];
-    d.rcm[Np + i] = r[1];
     double a[8], b[8];
     ba_jc_row(J, 0, a);
     ba_jc_row(J, 1, b);
@@ -322,6 +342,162 @@ __global__ void __launch_bounds__(SSFM_TILE) ba_k_linearize_cm(BADev d, const do
 #pragma unroll
     for (int k = 0; k < CAM_V; ++k) dst[k] = v[k];
   }
+}
+
+// ---------------------------------------------------------------------------
+// linearize of omega-form handles in two passes that evaluate each
+// observation ONCE (ba_k_linearize + ba_k_linearize_cm evaluate it twice, and
+// the point-major one gathers a 192-byte camera cache per observation):
+//  * ba_k_lin_tile, one CTA per camera tile (the tile's camera is uniform):
+//    residual and Jacobian, the factored record Fcm (coalesced), the
+//    point-major Jp + Jf record Gpm[8] and residual Rpm[4] (whole 64- / 32-
+//    byte sectors at the observation's point-major position: no partial-
+//    sector writes), and the tile's Jc^T Jc / Jc^T r (as ba_k_linearize_cm);
+//  * ba_k_lin_points, one warp per point batch: Jp^T Jp, Jp^T r (and
+//    Jp^T Jf) summed per point in observation order from Gpm / Rpm, as
+//    ba_k_linearize does (the same values: the records are bit-identical).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(SSFM_TILE) ba_k_lin_tile(BADev d, const double* __restrict__ theta) {
+  __shared__ double sm[(SSFM_TILE / 32) * CAM_V];
+  const int t = blockIdx.x;
+  const int o0 = d.topo.tile_obs[t], o1 = d.topo.tile_obs[t + 1];
+  const int c = d.topo.tile_cam[t];
+  const int i = o0 + threadIdx.x;
+  double v[CAM_V];
+#pragma unroll
+  for (int k = 0; k < CAM_V; ++k) v[k] = 0.0;
+  if (i < o1) {
+    const unsigned long long pst = pol_evict_first();
+    const long long Np = d.Npad;
+    const int j = d.topo.cm_pt[i];
+    const int ip = d.topo.cm_to_pm[i];
+    double r[2], J[BA_JREC], ct, F[BA_FREC + 3];
+    ba_obs_eval(d.bp, d.cams + c, theta + d.bp.off_pts + 3ll * j, d.pix_cm + 2ll * i, r, J, &ct, F);
+    if (d.bp.model == 1) {
+#pragma unroll
+      for (int k = 0; k < BA_FREC + 3; ++k) st_hint(d.Fcm + k * Np + i, F[k], pst);
+    } else {   // pinhole: rows 4-5 (s01, s11) are implied
+#pragma unroll
+      for (int k = 0; k < BA_FREC + 3; ++k)
+        if (k < 4 || k > 5) st_hint(d.Fcm + k * Np + i, F[k], pst);
+    }
+    gpm_store(d, ip, J + 8);
+    *reinterpret_cast<double4*>(d.Rpm + 4ll * ip) = make_double4(r[0], r[1], 0.0, 0.0);
+    double a[8], b[8];
+    ba_jc_row(J, 0, a);
+    ba_jc_row(J, 1, b);
+    int idx = 0;
+#pragma unroll
+    for (int p = 0; p < 8; ++p)
+#pragma unroll
+      for (int q = p; q < 8; ++q) v[idx++] = a[p] * a[q] + b[p] * b[q];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) v[36 + p] = a[p] * r[0] + b[p] * r[1];
+  }
+  block_reduce<CAM_V>(v, sm);
+  if (threadIdx.x == 0) {
+    double* dst = d.tilebuf + (long long)CAM_V * t;
+#pragma unroll
+    for (int k = 0; k < CAM_V; ++k) dst[k] = v[k];
+  }
+}
+
+__global__ void __launch_bounds__(256) ba_k_lin_points(BADev d, const double* __restrict__ theta,
+                                                       double* gpt_norm_part) {
+  __shared__ double sm[8][SSFM_BATCH][LIN_V];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned long long pst = pol_evict_first();
+  double gn2 = 0.0, gmax = 0.0;
+  for (int b = gw; b < d.topo.nb; b += warps) {
+    const int ob0 = d.topo.bat_obs[b], ob1 = d.topo.bat_obs[b + 1];
+    const int pb0 = d.topo.bat_pt[b], pb1 = d.topo.bat_pt[b + 1];
+    const int my_pt = pb0 + lane;
+    int ps = 0, pe = 0;
+    if (my_pt < pb1) { ps = d.topo.pt_seg[my_pt]; pe = d.topo.pt_seg[my_pt + 1]; }
+    double acc[LIN_V];
+#pragma unroll
+    for (int k = 0; k < LIN_V; ++k) acc[k] = 0.0;
+    for (int base = ob0; base < ob1; base += SSFM_BATCH) {
+      const int i = base + lane;
+      double val[LIN_V];
+#pragma unroll
+      for (int k = 0; k < LIN_V; ++k) val[k] = 0.0;
+      if (i < ob1) {
+        double G[8], r[4];
+        gpm_load(d, i, G, pst);
+        ld_v4_ro(d.Rpm + 4ll * i, r, pst);
+        const double* jp = G;
+        val[0] = jp[0] * jp[0] + jp[3] * jp[3];
+        val[1] = jp[0] * jp[1] + jp[3] * jp[4];
+        val[2] = jp[0] * jp[2] + jp[3] * jp[5];
+        val[3] = jp[1] * jp[1] + jp[4] * jp[4];
+        val[4] = jp[1] * jp[2] + jp[4] * jp[5];
+        val[5] = jp[2] * jp[2] + jp[5] * jp[5];
+        val[6] = jp[0] * r[0] + jp[3] * r[1];
+        val[7] = jp[1] * r[0] + jp[4] * r[1];
+        val[8] = jp[2] * r[0] + jp[5] * r[1];
+        val[9] = jp[0] * G[6] + jp[3] * G[7];
+        val[10] = jp[1] * G[6] + jp[4] * G[7];
+        val[11] = jp[2] * G[6] + jp[5] * G[7];
+      }
+#pragma unroll
+      for (int k = 0; k < LIN_V; ++k) sm[wib][lane][k] = val[k];
+      __syncwarp();
+      const int a = max(ps, base), e = min(pe, base + SSFM_BATCH);
+      for (int o = a; o < e; ++o) {
+#pragma unroll
+        for (int k = 0; k < LIN_V; ++k) acc[k] += sm[wib][o - base][k];
+      }
+      __syncwarp();
+    }
+    if (my_pt < pb1) {
+      if (d.fpt) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) d.fpt[3ll * my_pt + k] = acc[9 + k];
+      }
+      const double* X = theta + d.bp.off_pts + 3ll * my_pt;
+      *reinterpret_cast<double4*>(d.Xl + 4ll * my_pt) = make_double4(X[0], X[1], X[2], 0.0);
+      double* C6 = d.Cpt + 6ll * my_pt;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) C6[k] = acc[k];
+      double* g3 = d.gpt + 3ll * my_pt;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        g3[k] = acc[6 + k];
+        gn2 += acc[6 + k] * acc[6 + k];
+        gmax = fmax(gmax, fabs(acc[6 + k]));
+      }
+    }
+  }
+  gn2 = warp_sum(gn2);
+  gmax = warp_max(gmax);
+  if (lane == 0) {
+    gpt_norm_part[gw] = gn2;
+    atomic_max_nonneg(d.scal + SC_GMAX, gmax);
+  }
+}
+
+// cost over camera tiles (the tile's camera uniform, no per-observation
+// camera gather): one partial per tile, summed in tile order
+__global__ void __launch_bounds__(SSFM_TILE) ba_k_cost_tile(BADev d, const double* __restrict__ theta,
+                                                            double* partials) {
+  __shared__ double sm[32];
+  const int t = blockIdx.x;
+  const int o0 = d.topo.tile_obs[t], o1 = d.topo.tile_obs[t + 1];
+  const int i = o0 + threadIdx.x;
+  double v[1] = {0.0};
+  if (i < o1) {
+    const BACam cc = d.cams[d.topo.tile_cam[t]];
+    const int j = d.topo.cm_pt[i];
+    BAProj pr;
+    double r[2], sw, ct;
+    ba_residual(d.bp, cc, theta + d.bp.off_pts + 3ll * j, d.pix_cm + 2ll * i, pr, r, sw, ct);
+    v[0] = ct;
+  }
+  block_reduce<1>(v, sm);
+  if (threadIdx.x == 0) partials[t] = v[0];
 }
 
 // per camera: sum of its tile partials in tile order (the local part of a
@@ -419,6 +595,7 @@ __device__ __forceinline__ void ptinv_focal_part(const BADev& d, int j, const do
 }
 
 __global__ void ba_k_ptinv(BADev d, double lam) {
+  if (d.lamp) lam = *d.lamp;
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   double inv[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   if (j < d.bp.P) {
@@ -666,6 +843,7 @@ __device__ bool gj_inverse(double* a, double* inv, int n, int lda) {
 // pinning (lm.py:628-635), block-Jacobi factors for the 7x7 pose block and the
 // 1x1 focal block separately (lm.py:473-483, 516-527).
 __global__ void ba_k_camprec(BADev d, double lam, const double* camsum) {
+  if (d.lamp) lam = *d.lamp;
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= d.bp.C) return;
   double s[CAM_V];
@@ -810,31 +988,21 @@ __global__ void k_cam_wvec(BADev d, const double* __restrict__ v, double* W) {
   if (c < d.bp.C) ba_wvec(d, v, c, W);
 }
 
-// One observation's Jp^T (Jc p_c) in the omega form (point-major index i).
+// One observation's Jp^T (Jc p_c) in the omega form (point-major index i):
+// the AoS record Gpm[8i..8i+7] = [Jp row 0, Jp row 1, Jf], the camera's W
+// (of p) and the observation's point X at the linearization.
 template <bool RO>
-__device__ __forceinline__ void ba_wobs(const BADev& d, long long i, const double* __restrict__ W, double* val) {
+__device__ __forceinline__ void ba_wobs(const BADev& d, long long i, int c, const double* __restrict__ W,
+                                        const double* X, double* val) {
   const unsigned long long pstream = pol_evict_first(), pkeep = pol_evict_last();
-  const long long Np = d.Npad;
-  double G[8];
-#pragma unroll
-  for (int k = 0; k < 6; ++k) G[k] = ldg_stream(d.Gpm + k * Np + i, pstream);
-  if (d.bp.focal_mode) {
-    G[6] = ldg_stream(d.Gpm + 6 * Np + i, pstream);
-    G[7] = ldg_stream(d.Gpm + 7 * Np + i, pstream);
-  } else {
-    G[6] = 0.0; G[7] = 0.0;
-  }
-  const int c = ldg_stream_i(d.topo.pm_cam + i, pstream);
-  const int j = ldg_stream_i(d.topo.pm_pt + i, pstream);
-  double w[8], X[4];
+  double G[8], w[8];
+  gpm_load(d, i, G, pstream);
   if constexpr (RO) {
     ld_v4_ro(W + 8ll * c, w, pkeep);
     ld_v4_ro(W + 8ll * c + 4, w + 4, pkeep);
-    ld_v4_ro(d.Xl + 4ll * j, X, pkeep);
   } else {
     ld_v4(W + 8ll * c, w);
     ld_v4(W + 8ll * c + 4, w + 4);
-    ld_v4(d.Xl + 4ll * j, X);
   }
   const double u0 = (w[1] * X[2] - w[2] * X[1]) - w[3];
   const double u1 = (w[2] * X[0] - w[0] * X[2]) - w[4];
@@ -868,7 +1036,8 @@ __global__ void __launch_bounds__(256) ba_k_backsub(BADev d, const double* __res
       const int i = base + lane;
       double val[3] = {0.0, 0.0, 0.0};
       if (i < ob1 && d.Gpm) {
-        ba_wobs<false>(d, i, d.Wc, val);
+        const int c = d.topo.pm_cam[i], j = d.topo.pm_pt[i];
+        ba_wobs<false>(d, i, c, d.Wc, d.Xl + 4ll * j, val);
       } else if (i < ob1) {
         double J[BA_JREC];
 #pragma unroll

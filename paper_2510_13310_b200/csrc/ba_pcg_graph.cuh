@@ -87,7 +87,14 @@ __global__ void k_g_init2(Dev d, CGGraphDev g, int nblk) {
 __global__ void __launch_bounds__(PTP_THREADS, PTP_MINB) k_g_point(BADev d, CGGraphDev g) {
   if (*(volatile int*)(g.ic + 3)) return;
   __shared__ double smp[PTP_THREADS / 32][SSFM_BATCH][3];
-  if (d.Gpm) { ba_point_pass_w<true>(d, d.Wc, d.yv, smp); return; }   // W (of p) is constant here
+  if (d.Gpm) {   // W (of p) is constant here
+#if PTW_BULK
+    ba_point_pass_wb<true>(d, d.Wc, d.yv, smp);
+#else
+    ba_point_pass_w<true>(d, d.Wc, d.yv, smp);
+#endif
+    return;
+  }
 #if PTP_PIPE
   __shared__ PtpStage stg[PTP_THREADS / 32][2];
   ba_point_pass_pipe<true>(d, g.p, d.yv, stg, smp);   // p is constant during this kernel

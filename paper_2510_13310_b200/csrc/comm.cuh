@@ -68,7 +68,14 @@ __device__ __forceinline__ void comm_signal_wait(const CommDev& cm, unsigned lon
   for (int r = 0; r < cm.nranks; ++r) {
     if (r == cm.rank) continue;
     while (ld_acquire_sys_u64(cm.flag[r]) < e) {
-      if (globaltimer_ns() - t0 > cm.timeout_ns) { atomicOr(cm.status, ST_COMM_TIMEOUT); return; }
+      if (globaltimer_ns() - t0 > cm.timeout_ns) {
+        atomicOr(cm.status, ST_COMM_TIMEOUT);
+        // diagnostic: where the peers are (a peer behind e never arrived; one
+        // ahead means the ranks ran different collective sequences)
+        printf("[ssfm comm] rank %d timed out at epoch %llu waiting for rank %d (flag %llu)\n", cm.rank, e, r,
+               ld_acquire_sys_u64(cm.flag[r]));
+        return;
+      }
     }
   }
 }

@@ -27,6 +27,7 @@
 #include "pattern.cuh"
 #include "block_algebra.cuh"
 #include "dense.cuh"
+#include "lm_graph.cuh"
 #include "schur_explicit.cuh"
 #include "metrics.cuh"
 
@@ -191,6 +192,20 @@ struct ssfm_handle {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
   std::vector<size_t> alloc_bytes;   // sizes of allocs (block cache)
   ssfm_arena* arena = nullptr;       // allocations come from this arena (not from allocs)
+  // the LM loop as one CUDA graph (lm_graph.cuh): built on the first lm_solve
+  int lm_state = 0;             // 0 not built, 1 ready, -1 unavailable (host loop)
+  cudaGraph_t lm_graph = nullptr;
+  cudaGraphExec_t lm_exec = nullptr;
+  LMState* lms = nullptr;       // device
+  LMState* hlms = nullptr;      // pinned host
+  LMRecDev* lrecs = nullptr;    // device [lrec_cap]
+  LMRecDev* hlrecs = nullptr;   // pinned host
+  int lrec_cap = 0;
+  double* lm_theta = nullptr;   // the theta buffer the graph was captured with
+  double lm_cg_tol = -1.0;      // CG parameters baked into the captured PCG launches
+  int lm_cg_max = -1;
+  long long lm_k_iter = 0, lm_k_lin = 0, lm_k_solve = 0;   // kernels per section (launch accounting)
+  bool capturing = false;
 };
 
 // Device blocks of destroyed handles are kept for reuse by exact size (per
@@ -308,6 +323,10 @@ static void free_handle(ssfm_handle* h) {
   }
   if (h->region) cudaFree(h->region);
   if (h->hmisc) cudaFreeHost(h->hmisc);
+  if (h->hlms) cudaFreeHost(h->hlms);
+  if (h->hlrecs) cudaFreeHost(h->hlrecs);
+  if (h->lm_exec) cudaGraphExecDestroy(h->lm_exec);
+  if (h->lm_graph) cudaGraphDestroy(h->lm_graph);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
   if (h->ev2) cudaEventDestroy(h->ev2);
@@ -333,7 +352,8 @@ static int build_topo(ssfm_handle* h, const int* cam, const int* pt, int C, int 
   int *iota, *perm_pm, *perm_cm, *keys_out, *inv_cm, *cnt;
   DALLOC(iota, N); DALLOC(keys_out, N); DALLOC(inv_cm, N);
   DALLOC(T.pm_obs, N); DALLOC(T.cm_obs, N);
-  DALLOC(T.pm_pt, N); DALLOC(T.pm_cam, N); DALLOC(T.pm_to_cm, N); DALLOC(T.cm_to_pm, N); DALLOC(T.cm_pt, N);
+  // pm_pt / pm_cam + 4: 16-byte bulk copies of a batch's indices may round up past N
+  DALLOC(T.pm_pt, N + 4); DALLOC(T.pm_cam, N + 4); DALLOC(T.pm_to_cm, N); DALLOC(T.cm_to_pm, N); DALLOC(T.cm_pt, N);
   DALLOC(T.pt_seg, (long long)P + 1); DALLOC(T.cam_seg, (long long)C + 1);
   perm_pm = T.pm_obs; perm_cm = T.cm_obs;
   if (N > 0) k_iota<<<nblk(N, TB), TB, 0, st>>>(iota, N);
@@ -574,6 +594,10 @@ static int setup_ba_pcg(ssfm_handle* h, cudaStream_t st) {
       DALLOC(d.Gpm, 8ll * d.Npad);
       DALLOC(d.Xl, 4ll * d.bp.P);
       DALLOC(d.Wc, 8ll * d.bp.C);
+      // linearize evaluates each observation once (ba_k_lin_tile +
+      // ba_k_lin_points; SSFM_LIN2=0: the two evaluating passes)
+      const char* le = getenv("SSFM_LIN2");
+      if (!(le && le[0] == '0')) DALLOC(d.Rpm, 4ll * d.Npad);
     }
   }
   const char* ge = getenv("SSFM_PCG_GRAPH");
@@ -760,7 +784,6 @@ static int create_ba(const ssfm_ba_desc* desc, ssfm_arena* arena, void* stream, 
   }
   d.pix_pm = pix_pm; d.pps = pps; d.dists = dists; d.focals = focals;
   if ((rc = dalloc(h, &d.cams, C))) return fail(rc);
-  if ((rc = dalloc(h, &d.rcm, 2 * d.Npad))) return fail(rc);
   if ((rc = dalloc(h, &d.Cpt, 6ll * P))) return fail(rc);
   if ((rc = dalloc(h, &d.gpt, 3ll * P))) return fail(rc);
   if ((rc = dalloc(h, &d.Bc, 64ll * C))) return fail(rc);
@@ -795,7 +818,8 @@ static int create_ba(const ssfm_ba_desc* desc, ssfm_arena* arena, void* stream, 
   h->lin_blocks = std::max(1, std::min(nblk(T.nb, 8), h->num_sms * 16));
   h->cost_blocks = nblk(N, 256);
   h->cam_blocks = nblk(C, 256);
-  h->red_n = std::max<long long>(h->cost_blocks, (long long)h->lin_blocks * 8 + h->cam_blocks);
+  h->red_n = std::max<long long>(std::max<long long>(h->cost_blocks, T.nt),
+                                 (long long)h->lin_blocks * 8 + h->cam_blocks);
   if ((rc = dalloc(h, &h->red, h->red_n))) return fail(rc);
   if ((rc = dalloc(h, &h->part, 3ll * h->pcg_grid + 2))) return fail(rc);
   d.partials = h->red;
@@ -1045,8 +1069,13 @@ static int launch_cost(ssfm_handle* h, const double* theta, cudaStream_t st) {
   if (h->kind == 0) {
     BADev& d = h->ba;
     ba_k_prep<<<h->cam_blocks, 256, 0, st>>>(d, theta);
-    ba_k_cost<<<h->cost_blocks, 256, 0, st>>>(d, theta, h->red);
-    k_sum_partials<<<1, 1024, 0, st>>>(h->red, h->cost_blocks, d.scal + SC_COST);
+    if (d.topo.nt) {   // camera tiles: the tile's camera is uniform (no per-observation camera gather)
+      ba_k_cost_tile<<<d.topo.nt, SSFM_TILE, 0, st>>>(d, theta, h->red);
+      k_sum_partials<<<1, 1024, 0, st>>>(h->red, d.topo.nt, d.scal + SC_COST);
+    } else {
+      ba_k_cost<<<h->cost_blocks, 256, 0, st>>>(d, theta, h->red);
+      k_sum_partials<<<1, 1024, 0, st>>>(h->red, h->cost_blocks, d.scal + SC_COST);
+    }
     count_launch(h, 3);
     int rc = allreduce(h, d.scal + SC_COST, 1, AR_SUM, st);
     if (rc) return rc;
@@ -1070,8 +1099,13 @@ static int launch_linearize(ssfm_handle* h, const double* theta, double* r_out, 
     BADev& d = h->ba;
     ba_k_prep<<<h->cam_blocks, 256, 0, st>>>(d, theta);
     if (d.camlin) CU(cudaMemcpyAsync(d.camlin, d.cams, sizeof(BACam) * d.bp.C, cudaMemcpyDeviceToDevice, st));
-    ba_k_linearize<<<h->lin_blocks, 256, 0, st>>>(d, theta, r_out, J_out, h->red);
-    if (d.topo.nt) ba_k_linearize_cm<<<d.topo.nt, SSFM_TILE, 0, st>>>(d, theta);
+    if (d.Rpm && !r_out && !J_out) {   // each observation evaluated once (camera tiles), then point sums
+      if (d.topo.nt) ba_k_lin_tile<<<d.topo.nt, SSFM_TILE, 0, st>>>(d, theta);
+      ba_k_lin_points<<<h->lin_blocks, 256, 0, st>>>(d, theta, h->red);
+    } else {
+      ba_k_linearize<<<h->lin_blocks, 256, 0, st>>>(d, theta, r_out, J_out, h->red);
+      if (d.topo.nt) ba_k_linearize_cm<<<d.topo.nt, SSFM_TILE, 0, st>>>(d, theta);
+    }
     if (!sharded(h)) {
       ba_k_camfin<<<h->cam_blocks, 256, 0, st>>>(d, h->red + (long long)h->lin_blocks * 8, nullptr);
       k_sum_partials<<<1, 1024, 0, st>>>(h->red, h->lin_blocks * 8 + h->cam_blocks, d.scal + SC_GNORM2);
@@ -1189,11 +1223,10 @@ static void clear_l2_window(cudaStream_t cs) {
   cudaGetLastError();
 }
 
-// Build the graph PCG of a BA handle: one conditional WHILE node, body = one
-// CG iteration as kernels. Falls back to the persistent kernel (state -1) if
-// the runtime refuses (e.g. no conditional nodes).
-static int build_pcg_graph(ssfm_handle* h) {
+// device state of the graph PCG (allocated once per handle)
+static int alloc_gdev(ssfm_handle* h) {
   CGGraphDev& g = h->gdev;
+  if (g.partA) return SSFM_OK;
   g.x = h->x; g.r = h->r; g.z = h->z; g.p = h->p; g.q = h->q;
   DALLOC(g.partA, 2 * CGV_BLOCKS + 2);
   DALLOC(g.partB, 2 * CGV_BLOCKS + 2);
@@ -1202,40 +1235,13 @@ static int build_pcg_graph(ssfm_handle* h) {
   g.ctl = &h->misc->ctl;
   g.fused = h->fz.G > 0 ? 1 : 0;
   g.ngrp = h->fz.ngrp;
-  cudaGraphConditionalHandle hc;
-  cudaGraphNodeParams cp = {};
-  cudaGraphNode_t cn;
-  cudaStream_t cs = nullptr;
-  auto unavailable = [&](cudaError_t e) {
-    cudaGetLastError();
-    if (cs) cudaStreamDestroy(cs);
-    h->pcg_graph = nullptr;   // left to the driver: a half-captured body is not destroyed here
-    h->graph_state = -1;
-    (void)e;
-    return SSFM_OK;
-  };
-  cudaError_t e;
-  if (g.fused) {   // before any capture: kernel attributes cannot be set while capturing
-    switch (h->fz.SL) {
-      case 8: e = prepare_fused<8>(); break;
-      case 4: e = prepare_fused<4>(); break;
-      case 2: e = prepare_fused<2>(); break;
-      default: e = prepare_fused<1>(); break;
-    }
-    if (e) return unavailable(e);
-  }
-  if ((e = cudaGraphCreate(&h->pcg_graph, 0))) return unavailable(e);
-  if ((e = cudaGraphConditionalHandleCreate(&hc, h->pcg_graph, 1, cudaGraphCondAssignDefault))) return unavailable(e);
-  cp.type = cudaGraphNodeTypeConditional;
-  cp.conditional.handle = hc;
-  cp.conditional.type = cudaGraphCondTypeWhile;
-  cp.conditional.size = 1;
-  if ((e = cudaGraphAddNode(&cn, h->pcg_graph, nullptr, 0, &cp))) return unavailable(e);
-  cudaGraph_t body = cp.conditional.phGraph_out[0];
-  if ((e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking))) return unavailable(e);
-  if (!g.fused) set_l2_window(h, cs, h->ba.yv, sizeof(double) * 4 * (size_t)h->ba.bp.P);
-  if ((e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed)))
-    return unavailable(e);
+  return SSFM_OK;
+}
+
+// one CG iteration of the BA graph PCG (the WHILE body), captured on cs;
+// hc is the WHILE node's condition (set by k_g_scalars)
+static void capture_ba_pcg_body(ssfm_handle* h, cudaStream_t cs, cudaGraphConditionalHandle hc) {
+  CGGraphDev& g = h->gdev;
   BADev& d = h->ba;
   int occ_p = 0, occ_c = 0;
   const bool fac = d.Fcm != nullptr;
@@ -1266,6 +1272,51 @@ static int build_pcg_graph(ssfm_handle* h) {
   k_g_pupdate<<<CGV_BLOCKS, 256, 0, cs>>>(d, g, CGV_BLOCKS);
   k_g_scalars<<<1, 32, 0, cs>>>(d, g, CGV_BLOCKS, hc);
   h->graph_body_kernels = (g.fused ? 1 : 2) + (sharded(h) ? 2 : 0) + 4;
+}
+
+static cudaError_t prepare_fused_of(const ssfm_handle* h) {
+  switch (h->fz.SL) {
+    case 8: return prepare_fused<8>();
+    case 4: return prepare_fused<4>();
+    case 2: return prepare_fused<2>();
+    default: return prepare_fused<1>();
+  }
+}
+
+// Build the graph PCG of a BA handle: one conditional WHILE node, body = one
+// CG iteration as kernels. Falls back to the persistent kernel (state -1) if
+// the runtime refuses (e.g. no conditional nodes).
+static int build_pcg_graph(ssfm_handle* h) {
+  int rc = alloc_gdev(h);
+  if (rc) return rc;
+  CGGraphDev& g = h->gdev;
+  cudaGraphConditionalHandle hc;
+  cudaGraphNodeParams cp = {};
+  cudaGraphNode_t cn;
+  cudaStream_t cs = nullptr;
+  auto unavailable = [&](cudaError_t e) {
+    cudaGetLastError();
+    if (cs) cudaStreamDestroy(cs);
+    h->pcg_graph = nullptr;   // left to the driver: a half-captured body is not destroyed here
+    h->graph_state = -1;
+    (void)e;
+    return SSFM_OK;
+  };
+  cudaError_t e;
+  if (g.fused && (e = prepare_fused_of(h))) return unavailable(e);   // not while capturing
+  if ((e = cudaGraphCreate(&h->pcg_graph, 0))) return unavailable(e);
+  if ((e = cudaGraphConditionalHandleCreate(&hc, h->pcg_graph, 1, cudaGraphCondAssignDefault))) return unavailable(e);
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = hc;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  if ((e = cudaGraphAddNode(&cn, h->pcg_graph, nullptr, 0, &cp))) return unavailable(e);
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  if ((e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking))) return unavailable(e);
+  if (!g.fused) set_l2_window(h, cs, h->ba.yv, sizeof(double) * 4 * (size_t)h->ba.bp.P);
+  if ((e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed)))
+    return unavailable(e);
+  capture_ba_pcg_body(h, cs, hc);
   if ((e = cudaStreamEndCapture(cs, &body))) return unavailable(e);
   if ((e = cudaGraphInstantiate(&h->pcg_exec, h->pcg_graph, 0))) return unavailable(e);
   cudaStreamDestroy(cs);
@@ -1400,8 +1451,8 @@ static int launch_pcg(ssfm_handle* h, double lam, const ssfm_lm_config* cfg, cud
   return SSFM_OK;
 }
 
-// damped solve on the current linearization -> h->delta (async)
-static int launch_solve(ssfm_handle* h, double lam, const ssfm_lm_config* cfg, cudaStream_t st) {
+// damped elimination blocks and the preconditioner at lambda (async)
+static int launch_solve_pre(ssfm_handle* h, double lam, cudaStream_t st) {
   CU(cudaMemsetAsync(&h->misc->status, 0, sizeof(int), st));
   CU(cudaMemsetAsync(&h->misc->ctl, 0, sizeof(CGCtl), st));
   if (h->kind == 0) {
@@ -1441,10 +1492,11 @@ static int launch_solve(ssfm_handle* h, double lam, const ssfm_lm_config* cfg, c
     }
   }
   CU(cudaGetLastError());
-  if (h->prof.on) CU(cudaEventRecord(h->ev2, st));
-  int rc = launch_pcg(h, lam, cfg, st);
-  if (rc) return rc;
-  if (h->prof.on) CU(cudaEventRecord(h->ev3, st));
+  return SSFM_OK;
+}
+
+// back-substitution of the PCG solution x -> delta (async)
+static int launch_solve_post(ssfm_handle* h, cudaStream_t st) {
   if (h->kind == 0) {
     BADev& d = h->ba;
     if (d.Gpm) { k_cam_wvec<<<h->cam_blocks, 256, 0, st>>>(d, h->x, d.Wc); count_launch(h); }
@@ -1457,6 +1509,16 @@ static int launch_solve(ssfm_handle* h, double lam, const ssfm_lm_config* cfg, c
   }
   CU(cudaGetLastError());
   return SSFM_OK;
+}
+
+// damped solve on the current linearization -> h->delta (async)
+static int launch_solve(ssfm_handle* h, double lam, const ssfm_lm_config* cfg, cudaStream_t st) {
+  int rc = launch_solve_pre(h, lam, st);
+  if (rc) return rc;
+  if (h->prof.on && !h->capturing) CU(cudaEventRecord(h->ev2, st));
+  if ((rc = launch_pcg(h, lam, cfg, st))) return rc;
+  if (h->prof.on && !h->capturing) CU(cudaEventRecord(h->ev3, st));
+  return launch_solve_post(h, st);
 }
 
 static int launch_post_step(ssfm_handle* h, double* theta, cudaStream_t st) {
@@ -1605,6 +1667,278 @@ extern "C" int ssfm_post_step(ssfm_handle* h, double* theta, void* stream) {
   return SSFM_OK;
 }
 
+// ---------------------------------------------------------------------------
+// The LM loop as ONE CUDA graph (lm_graph.cuh): single-rank BA handles.
+// ---------------------------------------------------------------------------
+__global__ void k_g_setparams_lm(CGGraphDev g, const LMState* s, double cg_tol, int max_iters) {
+  g.sc[0] = s->lam; g.sc[1] = cg_tol; g.ic[0] = max_iters; g.ic[4] = 0;
+}
+// the PCG WHILE node runs its body while the solve is not done (k_g_init2 decided)
+__global__ void k_g_cond_init(CGGraphDev g, cudaGraphConditionalHandle hc) {
+  cudaGraphSetConditional(hc, g.ic[3] ? 0u : 1u);
+}
+__global__ void k_lm_mark(LMState* s, int which) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  if (which == 0) s->t_pcg0 = t;
+  else s->cg_pad_t1 = t;
+}
+
+// a conditional node at the capture position of st (its condition set by a
+// kernel enqueued before it); the body graph is returned for capture
+static cudaError_t cap_cond(cudaStream_t st, cudaGraphConditionalHandle hc, enum cudaGraphConditionalNodeType type,
+                            cudaGraph_t* body) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t g;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  cudaError_t e = cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &nd);
+  if (e) return e;
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = hc;
+  cp.conditional.type = type;
+  cp.conditional.size = 1;
+  cudaGraphNode_t n;
+  if ((e = cudaGraphAddNode(&n, g, deps, nd, &cp))) return e;
+  if ((e = cudaStreamUpdateCaptureDependencies(st, &n, 1, cudaStreamSetCaptureDependencies))) return e;
+  *body = cp.conditional.phGraph_out[0];
+  return cudaSuccess;
+}
+static cudaError_t cap_handle(cudaStream_t st, cudaGraphConditionalHandle* hc) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t g;
+  cudaError_t e = cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, nullptr, nullptr);
+  if (e) return e;
+  return cudaGraphConditionalHandleCreate(hc, g, 0, 0);
+}
+
+static bool lm_graph_wanted(const ssfm_handle* h) {
+  if (h->kind != 0 || sharded(h) || h->lm_state < 0) return false;
+  const char* e = getenv("SSFM_LM_GRAPH");
+  return !(e && e[0] == '0');
+}
+
+static void destroy_lm_graph(ssfm_handle* h) {
+  if (h->lm_exec) cudaGraphExecDestroy(h->lm_exec);
+  if (h->lm_graph) cudaGraphDestroy(h->lm_graph);
+  h->lm_exec = nullptr;
+  h->lm_graph = nullptr;
+  h->lm_state = 0;
+}
+
+static int build_lm_graph(ssfm_handle* h, const ssfm_lm_config* cfg) {
+  const int cap = std::max(64, cfg->max_iterations);
+  if (!h->lms) {
+    DALLOC(h->lms, 1);
+    CU(cudaMallocHost((void**)&h->hlms, sizeof(LMState)));
+  }
+  if (h->lrec_cap < cap) {
+    DALLOC(h->lrecs, cap);   // handle-owned; an older smaller block stays with the handle
+    if (h->hlrecs) cudaFreeHost(h->hlrecs);
+    CU(cudaMallocHost((void**)&h->hlrecs, sizeof(LMRecDev) * cap));
+    h->lrec_cap = cap;
+  }
+  const bool gpcg = h->graph_state != -1;   // the graph PCG (nested WHILE) or the persistent kernel
+  if (gpcg) {
+    int rc = alloc_gdev(h);
+    if (rc) return rc;
+  }
+  cudaStream_t s0 = nullptr, s1 = nullptr, s2 = nullptr;
+  auto unavailable = [&](cudaError_t e) {
+    cudaGetLastError();
+    h->capturing = false;
+    h->ba.lamp = nullptr;
+    for (cudaStream_t x : {s0, s1, s2}) {
+      if (!x) continue;
+      cudaGraph_t junk = nullptr;
+      cudaStreamCaptureStatus cst;
+      if (cudaStreamIsCapturing(x, &cst) == cudaSuccess && cst != cudaStreamCaptureStatusNone)
+        cudaStreamEndCapture(x, &junk);
+      cudaStreamDestroy(x);
+    }
+    cudaGetLastError();
+    h->lm_graph = nullptr;
+    h->lm_state = -1;
+    if (getenv("SSFM_TIMING")) fprintf(stderr, "[ssfm] LM graph unavailable: %s\n", cudaGetErrorString(e));
+    return SSFM_OK;
+  };
+  cudaError_t e;
+  if (gpcg && h->gdev.fused && (e = prepare_fused_of(h))) return unavailable(e);
+  for (cudaStream_t* x : {&s0, &s1, &s2})
+    if ((e = cudaStreamCreateWithFlags(x, cudaStreamNonBlocking))) return unavailable(e);
+  if ((e = cudaGraphCreate(&h->lm_graph, 0))) return unavailable(e);
+  cudaGraphConditionalHandle hw, hlin, hsolve, hpcg;
+  if ((e = cudaGraphConditionalHandleCreate(&hw, h->lm_graph, 1, cudaGraphCondAssignDefault))) return unavailable(e);
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = hw;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t wn;
+  if ((e = cudaGraphAddNode(&wn, h->lm_graph, nullptr, 0, &cp))) return unavailable(e);
+  cudaGraph_t body = cp.conditional.phGraph_out[0], blin, bsolve, bpcg;
+  BADev& d = h->ba;
+  CGGraphDev& g = h->gdev;
+  LMState* S = h->lms;
+  const long long n = h->total_params;
+  h->capturing = true;
+  d.lamp = &S->lam;   // captured kernels read lambda from the loop state
+  const long long k0 = h->prof.kernel_launches;
+  int rc = SSFM_OK;
+  if ((e = cudaStreamBeginCaptureToGraph(s0, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed)))
+    return unavailable(e);
+  if ((e = cap_handle(s0, &hlin))) return unavailable(e);
+  k_lm_head<<<1, 1, 0, s0>>>(S, hlin);
+  if ((e = cap_cond(s0, hlin, cudaGraphCondTypeIf, &blin))) return unavailable(e);
+  // IF (need_lin): linearize + gradient test
+  if ((e = cudaStreamBeginCaptureToGraph(s1, blin, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed)))
+    return unavailable(e);
+  const long long k1 = h->prof.kernel_launches;
+  if ((rc = launch_linearize(h, h->theta, nullptr, nullptr, s1))) { unavailable(cudaErrorUnknown); return rc; }
+  k_lm_gradcheck<<<1, 1, 0, s1>>>(S, d.scal + SC_GMAX);
+  h->lm_k_lin = h->prof.kernel_launches - k1 + 1;
+  if ((e = cudaStreamEndCapture(s1, &blin))) return unavailable(e);
+  if ((e = cap_handle(s0, &hsolve))) return unavailable(e);
+  k_lm_mid<<<1, 1, 0, s0>>>(S, hsolve);
+  if ((e = cap_cond(s0, hsolve, cudaGraphCondTypeIf, &bsolve))) return unavailable(e);
+  // IF (not done): one damped solve, the candidate and the decision
+  if ((e = cudaStreamBeginCaptureToGraph(s1, bsolve, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed)))
+    return unavailable(e);
+  const long long k2 = h->prof.kernel_launches;
+  if ((rc = launch_solve_pre(h, 0.0, s1))) { unavailable(cudaErrorUnknown); return rc; }
+  k_lm_mark<<<1, 1, 0, s1>>>(S, 0);
+  const int max_it = cfg->cg_max_iters;
+  const double tol = cfg->cg_tol;
+  if (gpcg) {
+    k_g_setparams_lm<<<1, 1, 0, s1>>>(g, S, tol, max_it);
+    k_g_init<<<CGV_BLOCKS, 256, 0, s1>>>(d, g);
+    if (d.Gpm) { k_cam_wvec<<<h->cam_blocks, 256, 0, s1>>>(d, g.p, d.Wc); count_launch(h); }
+    k_g_init2<<<1, 32, 0, s1>>>(d, g, CGV_BLOCKS);
+    if ((e = cap_handle(s1, &hpcg))) return unavailable(e);
+    k_g_cond_init<<<1, 1, 0, s1>>>(g, hpcg);
+    count_launch(h, 5);
+    if ((e = cap_cond(s1, hpcg, cudaGraphCondTypeWhile, &bpcg))) return unavailable(e);
+    if (!g.fused) set_l2_window(h, s2, d.yv, sizeof(double) * 4 * (size_t)d.bp.P);
+    if ((e = cudaStreamBeginCaptureToGraph(s2, bpcg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed)))
+      return unavailable(e);
+    capture_ba_pcg_body(h, s2, hpcg);
+    if ((e = cudaStreamEndCapture(s2, &bpcg))) return unavailable(e);
+  } else {
+    double lam = 0.0;   // read from d.lamp by the kernel
+    CGCtl* ctl = &h->misc->ctl;
+    void* a[13];
+    a[0] = &d; a[1] = &h->fz; a[2] = &h->cm; a[3] = &lam; a[4] = (void*)&max_it; a[5] = (void*)&tol;
+    a[6] = &h->x; a[7] = &h->r; a[8] = &h->z; a[9] = &h->p; a[10] = &h->q;
+    a[11] = &h->part; a[12] = &ctl;
+    if ((e = cudaLaunchCooperativeKernel(h->pcg_fn, dim3(h->pcg_grid), dim3(h->pcg_threads), a, h->pcg_smem, s1)))
+      return unavailable(e);
+    count_launch(h);
+  }
+  k_lm_mark<<<1, 1, 0, s1>>>(S, 1);
+  if ((rc = launch_solve_post(h, s1))) { unavailable(cudaErrorUnknown); return rc; }
+  k_axpy_theta<<<nblk(n, 256), 256, 0, s1>>>(h->theta, h->delta, h->cand, n);
+  if ((rc = launch_post_step(h, h->cand, s1))) { unavailable(cudaErrorUnknown); return rc; }
+  if ((rc = launch_cost(h, h->cand, s1))) { unavailable(cudaErrorUnknown); return rc; }
+  k_lm_decide<CGCtl><<<1, 1, 0, s1>>>(S, &h->misc->status, &h->misc->ctl, d.scal + SC_COST, h->lrecs);
+  k_lm_accept<<<std::min(nblk(n, 256), 4 * h->num_sms), 256, 0, s1>>>(S, h->cand, h->theta, n);
+  h->lm_k_solve = h->prof.kernel_launches - k2 + 5;   // + marks, axpy, decide, accept
+  if ((e = cudaStreamEndCapture(s1, &bsolve))) return unavailable(e);
+  k_lm_tail<<<1, 1, 0, s0>>>(S, hw);
+  h->lm_k_iter = 3;
+  if ((e = cudaStreamEndCapture(s0, &body))) return unavailable(e);
+  h->capturing = false;
+  d.lamp = nullptr;
+  h->prof.kernel_launches = k0;   // capture is not execution
+  if ((e = cudaGraphInstantiate(&h->lm_exec, h->lm_graph, 0))) return unavailable(e);
+  for (cudaStream_t x : {s0, s1, s2}) cudaStreamDestroy(x);
+  h->lm_theta = h->theta;
+  h->lm_cg_tol = tol;
+  h->lm_cg_max = max_it;
+  h->lm_state = 1;
+  return SSFM_OK;
+}
+
+// lm_solve with the loop on the device: one graph launch, one read-back
+static int lm_solve_graph(ssfm_handle* h, double* theta_io, const ssfm_lm_config* cfg, ssfm_iter_record* recs,
+                          int32_t cap, int32_t* n_recs, int32_t* termination, cudaStream_t st) {
+  if (h->lm_state == 1 && (h->lm_cg_tol != cfg->cg_tol || h->lm_cg_max != cfg->cg_max_iters ||
+                           h->lrec_cap < cfg->max_iterations))
+    destroy_lm_graph(h);
+  if (h->lm_state == 0) {
+    const auto tg = std::chrono::steady_clock::now();
+    int rc = build_lm_graph(h, cfg);
+    if (rc) return rc;
+    if (getenv("SSFM_TIMING"))
+      fprintf(stderr, "[ssfm] LM graph build %.1f ms (state %d)\n",
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tg).count(), h->lm_state);
+    if (h->lm_state != 1) return -1;   // unavailable: the caller runs the host loop
+  }
+  if (h->theta != h->lm_theta) std::swap(h->theta, h->cand);   // the captured buffers
+  const long long n = h->total_params;
+  LMState& H = *h->hlms;
+  H.lambda0 = cfg->lambda0; H.lambda_up = cfg->lambda_up; H.lambda_down = cfg->lambda_down;
+  H.lambda_min = cfg->lambda_min; H.lambda_max = cfg->lambda_max;
+  H.rel_cost_tol = cfg->rel_cost_tol; H.grad_tol = cfg->grad_tol;
+  H.max_it = cfg->max_iterations;
+  H.cap = h->lrec_cap;
+  CU(cudaMemcpyAsync(h->lms, h->hlms, sizeof(LMState), cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(h->theta, theta_io, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  h->prof.pcg_ms = h->prof.lin_ms = h->prof.all_ms = 0;
+  h->prof.pcg_launches = h->prof.lin_launches = h->prof.all_launches = 0;
+  h->prof.cg_iters = 0;
+  h->prof.kernel_launches = 0;
+  for (int k = 0; k < 5; ++k) h->prof.phase_ms[k] = 0;
+  int rc = launch_cost(h, h->theta, st);
+  if (rc) return rc;
+  k_lm_init<<<1, 1, 0, st>>>(h->lms, h->ba.scal + SC_COST);
+  count_launch(h);
+  if (cfg->max_iterations >= 1) CU(cudaGraphLaunch(h->lm_exec, st));
+  CU(cudaMemcpyAsync(h->hlms, h->lms, sizeof(LMState), cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(h->hlrecs, h->lrecs, sizeof(LMRecDev) * h->lrec_cap, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(theta_io, h->theta, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  CU(cudaStreamSynchronize(st));
+  CU(cudaGetLastError());
+  const LMState R = *h->hlms;
+  const int nrec = std::min(R.nrec, h->lrec_cap);
+  if (recs) {
+    for (int k = 0; k < std::min(nrec, (int)cap); ++k) {
+      const LMRecDev& D = h->hlrecs[k];
+      ssfm_iter_record& O = recs[k];
+      O.iteration = D.iteration;
+      O.cost_before = D.cost_before;
+      O.cost_after = D.cost_after;
+      O.lam = D.lam;
+      O.step_accepted = D.accepted;
+      O.cg_iters = D.cg_iters;
+      O.status = D.status;
+      O.wall_time_ns = (int64_t)D.ns;   // device clock (no host round trip per iteration)
+      O.device_ms = D.ns * 1e-6;
+    }
+  }
+  for (int k = 0; k < nrec; ++k) {
+    h->prof.pcg_ms += h->hlrecs[k].pcg_ns * 1e-6;
+    h->prof.all_ms += h->hlrecs[k].ns * 1e-6;
+  }
+  h->prof.pcg_launches = nrec;
+  h->prof.all_launches = nrec;
+  h->prof.cg_iters = R.cg_total;
+  count_launch(h, h->lm_k_iter * R.it + h->lm_k_lin * R.n_lin + h->lm_k_solve * R.n_solve +
+                      (h->graph_state != -1 ? (long long)h->graph_body_kernels * R.cg_total : 0));
+  if (R.n_lin > 0) h->linearized = true;
+  if (n_recs) *n_recs = std::min(nrec, (int)cap);
+  if (termination) *termination = R.term;
+  if (R.result == SSFM_SOLVER_FAILURE) {
+    Misc m = *h->hmisc;
+    m.ctl.iters = R.fail_iters;
+    m.ctl.rn = R.fail_rn;
+    m.ctl.tol = R.fail_tol;
+    set_err(SSFM_SOLVER_FAILURE, "linear solve failed at lambda_max: " + status_msg(R.fail_status, m));
+    return SSFM_SOLVER_FAILURE;
+  }
+  return SSFM_OK;
+}
+
 extern "C" int ssfm_lm_solve(ssfm_handle* h, double* theta_io, const ssfm_lm_config* cfg,
                              ssfm_iter_record* recs, int32_t cap, int32_t* n_recs,
                              int32_t* termination, void* stream) {
@@ -1612,6 +1946,10 @@ extern "C" int ssfm_lm_solve(ssfm_handle* h, double* theta_io, const ssfm_lm_con
   cudaStream_t st = (cudaStream_t)stream;
   using clk = std::chrono::steady_clock;
   int rc;
+  if (lm_graph_wanted(h)) {
+    rc = lm_solve_graph(h, theta_io, cfg, recs, cap, n_recs, termination, st);
+    if (rc != -1) return rc;   // -1: no graph on this runtime, run the host loop
+  }
   if (n_recs) *n_recs = 0;
   int term = SSFM_TERM_MAX_ITER;
   const long long n = h->total_params;
@@ -1717,6 +2055,8 @@ extern "C" int ssfm_lm_solve(ssfm_handle* h, double* theta_io, const ssfm_lm_con
   if (termination) *termination = term;
   return result;
 }
+
+extern "C" int32_t ssfm_lm_mode(const ssfm_handle* h) { return h ? h->lm_state : 0; }
 
 extern "C" int ssfm_profile_enable(ssfm_handle* h, int32_t on) {
   if (!h) return SSFM_INVALID_ARGUMENT;

@@ -20,7 +20,9 @@ it = ct.c_int32()
 lib.ssfm_solve_normal(ct.c_void_p(h.ptr), 1e-4, ct.byref(_native.lm_config_c(b2.LMConfig())), ct.c_void_p(d.data_ptr()), ct.byref(it), st)
 N, P, C = arr.num_observations, arr.num_points, arr.num_cameras
 fac = os.environ.get("SSFM_FACTORED", "1") != "0"
-for which, name, byts in [(0, "point pass", 128 * N + 4 * N + 48 * P + 32 * P), (1, "camera pass", (56 if fac else 128) * N + 4 * N + 32 * N)]:
+wf = fac and os.environ.get("SSFM_WFORM", "1") != "0"
+for which, name, byts in [(0, "point pass", ((64 + 8) if wf else (128 + 4)) * N + 48 * P + 32 * P + (32 * P if wf else 0)),
+                          (1, "camera pass", (56 if fac else 128) * N + 4 * N + 32 * N)]:
     ms = ct.c_double()
     _native.check(lib.ssfm_bench_operator(ct.c_void_p(h.ptr), which, 20, ct.byref(ms), st))
     print(f"{name}: {ms.value:.4f} ms, {byts / ms.value / 1e6:.0f} GB/s (bytes {byts/1e9:.2f} GB)")
