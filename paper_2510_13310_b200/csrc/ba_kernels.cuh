@@ -27,6 +27,7 @@ struct BADev {
   double* Xl;             // [4P] points at the linearization (omega-form, padded: 32-byte gathers)
   double* Wc;             // [8C] per-camera omega-form vector of the current p / x (ba_wvec)
   double* Rpm;            // [4N] point-major weighted residual [r0, r1, 0, 0] (ba_k_lin_tile; full sectors)
+  double* Kcm;            // [8N] camera-major [Jp Cinv Jp^T (3), Jp y0 (2), 0 x3] per damped solve (ba_k_kobs)
   double* Jcm;            // [16 * Npad]
   double* Fcm;            // [9 * Npad] factored records (ba_factor) + v = X - t, camera-major (two-pass only)
   BACam* camlin;          // [C] camera cache at the linearization (cams is overwritten by trial costs)
@@ -655,27 +656,38 @@ __device__ __forceinline__ void ba_precond_f(const BADev& d, int t, double* v) {
   else { f[4] = 0.0; f[5] = f[0]; }
 #pragma unroll
   for (int k = 0; k < 3; ++k) vv[k] = d.Fcm[(6 + k) * Np + i];
-  const int j = d.topo.cm_pt[i];
-  double ci[6], y[3], qh[4];
-#pragma unroll
-  for (int k = 0; k < 6; ++k) ci[k] = d.Cinv[6ll * j + k];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) y[k] = d.y0[3ll * j + k];
+  double qh[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) qh[k] = cb[9 + k];
   const double se[2][3] = {{f[0], f[4], -(f[0] * f[1] + f[4] * f[2])},
                            {f[4], f[5], -(f[4] * f[1] + f[5] * f[2])}};
-  double jp[2][3];
+  double k00, k01, k11, ty0, ty1;
+  if (d.Kcm) {   // per-observation point terms from ba_k_kobs (coalesced, no per-point gathers)
+    double K[8];
+    ld_v4_ro(d.Kcm + 8ll * i, K, pol_evict_first());
+    ld_v4_ro(d.Kcm + 8ll * i + 4, K + 4, pol_evict_first());
+    k00 = K[0]; k01 = K[1]; k11 = K[2]; ty0 = K[3]; ty1 = K[4];
+  } else {
+    const int j = d.topo.cm_pt[i];
+    double ci[6], y[3];
 #pragma unroll
-  for (int r = 0; r < 2; ++r)
+    for (int k = 0; k < 6; ++k) ci[k] = d.Cinv[6ll * j + k];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) jp[r][k] = se[r][0] * cb[k] + se[r][1] * cb[3 + k] + se[r][2] * cb[6 + k];
-  double w0[3], w1[3];
-  sym3_matvec(ci, jp[0], w0);
-  sym3_matvec(ci, jp[1], w1);
-  const double k00 = jp[0][0] * w0[0] + jp[0][1] * w0[1] + jp[0][2] * w0[2];
-  const double k01 = jp[1][0] * w0[0] + jp[1][1] * w0[1] + jp[1][2] * w0[2];
-  const double k11 = jp[1][0] * w1[0] + jp[1][1] * w1[1] + jp[1][2] * w1[2];
+    for (int k = 0; k < 3; ++k) y[k] = d.y0[3ll * j + k];
+    double jp[2][3];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) jp[r][k] = se[r][0] * cb[k] + se[r][1] * cb[3 + k] + se[r][2] * cb[6 + k];
+    double w0[3], w1[3];
+    sym3_matvec(ci, jp[0], w0);
+    sym3_matvec(ci, jp[1], w1);
+    k00 = jp[0][0] * w0[0] + jp[0][1] * w0[1] + jp[0][2] * w0[2];
+    k01 = jp[1][0] * w0[0] + jp[1][1] * w0[1] + jp[1][2] * w0[2];
+    k11 = jp[1][0] * w1[0] + jp[1][1] * w1[1] + jp[1][2] * w1[2];
+    ty0 = jp[0][0] * y[0] + jp[0][1] * y[1] + jp[0][2] * y[2];
+    ty1 = jp[1][0] * y[0] + jp[1][1] * y[1] + jp[1][2] * y[2];
+  }
   double a[8], b[8];
   ba_dqt_mul(qh, vv, se[0], a);
   ba_dqt_mul(qh, vv, se[1], b);
@@ -691,10 +703,38 @@ __device__ __forceinline__ void ba_precond_f(const BADev& d, int t, double* v) {
   for (int p = 0; p < 8; ++p)
 #pragma unroll
     for (int q = p; q < 8; ++q) v[idx++] = a[p] * ka[q] + b[p] * kb[q];
-  const double ty0 = jp[0][0] * y[0] + jp[0][1] * y[1] + jp[0][2] * y[2];
-  const double ty1 = jp[1][0] * y[0] + jp[1][1] * y[1] + jp[1][2] * y[2];
 #pragma unroll
   for (int p = 0; p < 8; ++p) v[36 + p] = a[p] * ty0 + b[p] * ty1;
+}
+
+// Point terms of the preconditioner per observation (omega-form handles):
+// K_o = Jp_o Cinv_j Jp_o^T and Jp_o y0_j from the point-major record, stored
+// as a whole 64-byte record at the observation's camera-major position, so
+// ba_k_precond streams them instead of gathering Cinv_j and y0_j per
+// observation (the gathers missed L2: 6.3 GB of DRAM per C5 launch).
+__global__ void ba_k_kobs(BADev d) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= d.topo.N) return;
+  const unsigned long long pst = pol_evict_first();
+  double G[8];
+  gpm_load(d, i, G, pst);
+  const int j = d.topo.pm_pt[i];
+  double ci[6], y[3];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) ci[k] = __ldg(d.Cinv + 6ll * j + k);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) y[k] = __ldg(d.y0 + 3ll * j + k);
+  double w0[3], w1[3];
+  sym3_matvec(ci, G, w0);
+  sym3_matvec(ci, G + 3, w1);
+  const double k00 = G[0] * w0[0] + G[1] * w0[1] + G[2] * w0[2];
+  const double k01 = G[3] * w0[0] + G[4] * w0[1] + G[5] * w0[2];
+  const double k11 = G[3] * w1[0] + G[4] * w1[1] + G[5] * w1[2];
+  const double ty0 = G[0] * y[0] + G[1] * y[1] + G[2] * y[2];
+  const double ty1 = G[3] * y[0] + G[4] * y[1] + G[5] * y[2];
+  double* dst = d.Kcm + 8ll * d.topo.pm_to_cm[i];
+  *reinterpret_cast<double4*>(dst) = make_double4(k00, k01, k11, ty0);
+  *reinterpret_cast<double4*>(dst + 4) = make_double4(ty1, 0.0, 0.0, 0.0);
 }
 
 // W = T W~ T^T, u = T u~ for the tile's camera, T = diag(Pi, R^T, 1): one
@@ -903,20 +943,23 @@ __global__ void ba_k_camprec(BADev d, double lam, const double* camsum) {
 // the sum of the cameras' shares. Summed in fixed order (one block); pinned if
 // the diagonal is exactly zero
 // (lm.py:628-635), and set its 1x1 block-Jacobi factor (lm.py:516-527).
-__global__ void ba_k_shared_focal_prec(BADev d, int nwpart) {
+// wsum != nullptr: the point part summed over every rank's points (sharded).
+__global__ void ba_k_shared_focal_prec(BADev d, int nwpart, const double* wsum) {
   __shared__ double sm[96];
   double v[3] = {0.0, 0.0, 0.0};
   const int C = d.bp.C;
   const int per = (C + blockDim.x - 1) / blockDim.x;
   const int a = threadIdx.x * per, b = min(C, a + per);
   for (int c = a; c < b; ++c) { v[0] += d.fterm[2ll * c]; v[1] += d.fterm[2ll * c + 1]; }
-  const int perw = (nwpart + blockDim.x - 1) / blockDim.x;
-  const int aw = threadIdx.x * perw, bw = min(nwpart, aw + perw);
-  for (int k = aw; k < bw; ++k) v[2] += d.fwpart[k];
+  if (!wsum) {
+    const int perw = (nwpart + blockDim.x - 1) / blockDim.x;
+    const int aw = threadIdx.x * perw, bw = min(nwpart, aw + perw);
+    for (int k = aw; k < bw; ++k) v[2] += d.fwpart[k];
+  }
   block_reduce<3>(v, sm);
   if (threadIdx.x == 0) {
     // S_ff = A_ff (1 + lam) - sum_j a_j^T Cinv_j a_j  (lm.py:608-626 for the focal row)
-    const double sff = v[0] - v[2], bf = v[1];
+    const double sff = v[0] - (wsum ? *wsum : v[2]), bf = v[1];
     if (sff == 0.0) {
       if (bf != 0.0) atomicOr(d.status, ST_PIN_RETAINED);
       d.pinned[0] |= 0x80;

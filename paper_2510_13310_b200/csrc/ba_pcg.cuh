@@ -288,13 +288,13 @@ __device__ __forceinline__ void ba_point_pass(const BADev& d, const double* v, d
   }
 }
 
+#ifndef PTW_CIEARLY
+#define PTW_CIEARLY 0
+#endif
 // P1 in the omega form (ba_wobs): W = the per-camera vector of p (ba_wvec).
 // Streams the 64-byte Jp + Jf record and the camera and point indices per
 // observation (the 16-double record and one index before), gathers W_c (64
 // bytes, L2-resident) and X_j (32 bytes).
-#ifndef PTW_OWNERX
-#define PTW_OWNERX 0   // 1: X from the owner lanes through shared memory (lost: C5 0.52 vs 0.47 ms); 0: gather by pm_pt
-#endif
 template <bool RO = false>
 __device__ __forceinline__ void ba_point_pass_w(const BADev& d, const double* W, double* y,
                                                 double (*sm)[SSFM_BATCH][3]) {
@@ -302,47 +302,32 @@ __device__ __forceinline__ void ba_point_pass_w(const BADev& d, const double* W,
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-#if PTW_OWNERX
-  __shared__ double smx[PTP_THREADS / 32][SSFM_BATCH][3];
-  __shared__ unsigned char smo[PTP_THREADS / 32][SSFM_BATCH];
-#endif
   for (int b = gw; b < d.topo.nb; b += warps) {
     const int ob0 = d.topo.bat_obs[b], ob1 = d.topo.bat_obs[b + 1];
     const int pb0 = d.topo.bat_pt[b], pb1 = d.topo.bat_pt[b + 1];
     const int my_pt = pb0 + lane;
     const bool own = my_pt < pb1;
     int ps = 0, pe = 0;
+#if PTW_CIEARLY
+    double ci[6];
+#endif
     if (own) {
       ps = d.topo.pt_seg[my_pt]; pe = d.topo.pt_seg[my_pt + 1];
-#if PTW_OWNERX
-      const bool single = ob1 - ob0 <= SSFM_BATCH;
-      double X[4];
-      ld_v4_ro(d.Xl + 4ll * my_pt, X, pkeep);
-      smx[wib][lane][0] = X[0]; smx[wib][lane][1] = X[1]; smx[wib][lane][2] = X[2];
-      // owner lane of each observation position (a batch is <= 32
-      // observations of whole points, or one point with more: lane 0)
-      if (single)
-        for (int o = ps; o < pe; ++o) smo[wib][o - ob0] = (unsigned char)lane;
+#if PTW_CIEARLY   // the owner's Cinv in flight during the batch (not after its reduction)
+#pragma unroll
+      for (int k = 0; k < 6; ++k) ci[k] = __ldg(d.Cinv + 6ll * my_pt + k);
 #endif
     }
-#if PTW_OWNERX
-    __syncwarp();
-    const int owner = ob1 - ob0 <= SSFM_BATCH ? smo[wib][lane] : 0;
-#endif
     double acc[3] = {0.0, 0.0, 0.0};
     for (int base = ob0; base < ob1; base += SSFM_BATCH) {
       const int i = base + lane;
       double val[3] = {0.0, 0.0, 0.0};
       if (i < ob1) {
         const int c = ldg_stream_i(d.topo.pm_cam + i, pstream);
-#if PTW_OWNERX
-        ba_wobs<RO>(d, i, c, W, smx[wib][owner], val);
-#else
         const int j = ldg_stream_i(d.topo.pm_pt + i, pstream);
         double X[4];
         ld_v4_ro(d.Xl + 4ll * j, X, pkeep);
         ba_wobs<RO>(d, i, c, W, X, val);
-#endif
       }
 #pragma unroll
       for (int k = 0; k < 3; ++k) sm[wib][lane][k] = val[k];
@@ -355,166 +340,16 @@ __device__ __forceinline__ void ba_point_pass_w(const BADev& d, const double* W,
       __syncwarp();
     }
     if (own) {
-      double ci[6], w[3];
+      double w[3];
+#if !PTW_CIEARLY
+      double ci[6];
 #pragma unroll
       for (int k = 0; k < 6; ++k) ci[k] = __ldg(d.Cinv + 6ll * my_pt + k);
+#endif
       sym3_matvec(ci, acc, w);
 #pragma unroll
       for (int k = 0; k < 3; ++k) st_hint(y + 4ll * my_pt + k, w[k], pkeep);
     }
-  }
-}
-
-// P1 in the omega form with TMA bulk staging (PTW_BULK): each warp keeps two
-// shared-memory stages; while it works on batch b, one elected lane has the
-// next batch's records (one contiguous 64-byte-per-observation block) and its
-// camera / point indices in flight as three 1-D bulk copies completing on the
-// stage's mbarrier. Batches with more than 32 observations (one point) are
-// read directly.
-#ifndef PTW_BULK
-#define PTW_BULK 0
-#endif
-#ifndef PTW_BULK_CI
-#define PTW_BULK_CI 0   // the batch's Cinv blocks ride in the stage too
-#endif
-struct PtwStage {
-  double G[SSFM_BATCH * 8];
-  int cam[SSFM_BATCH + 8];
-  int pt[SSFM_BATCH + 8];
-#if PTW_BULK_CI
-  double Ci[SSFM_BATCH * 6];
-#endif
-};
-template <bool RO = false>
-__device__ __forceinline__ void ba_point_pass_wb(const BADev& d, const double* W, double* y,
-                                                 double (*sm)[SSFM_BATCH][3]) {
-  const unsigned long long pstream = pol_evict_first(), pkeep = pol_evict_last();
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  __shared__ __align__(128) PtwStage stg[PTP_THREADS / 32][2];
-  __shared__ __align__(8) unsigned long long bar[PTP_THREADS / 32][2];
-  const int nb = d.topo.nb;
-  if (lane == 0) {
-    mbar_init(&bar[wib][0], 1);
-    mbar_init(&bar[wib][1], 1);
-    fence_mbar_init();
-  }
-  __syncwarp();
-  auto issue = [&](int o0, int o1, int p0, int p1, int s) {
-    const int a0 = o0 & ~3, a1 = (o1 + 3) & ~3;
-    const unsigned gb = 64u * (unsigned)(o1 - o0), ib = 4u * (unsigned)(a1 - a0);
-#if PTW_BULK_CI
-    const unsigned cb = 48u * (unsigned)(p1 - p0);
-#else
-    const unsigned cb = 0;
-    (void)p0; (void)p1;
-#endif
-    fence_proxy_async_smem();
-    mbar_expect_tx(&bar[wib][s], gb + 2 * ib + cb);
-    bulk_g2s(stg[wib][s].G, d.Gpm + 8ll * o0, gb, &bar[wib][s], pstream);
-    bulk_g2s(stg[wib][s].cam, d.topo.pm_cam + a0, ib, &bar[wib][s], pstream);
-    bulk_g2s(stg[wib][s].pt, d.topo.pm_pt + a0, ib, &bar[wib][s], pstream);
-#if PTW_BULK_CI
-    bulk_g2s(stg[wib][s].Ci, d.Cinv + 6ll * p0, cb, &bar[wib][s], pstream);
-#endif
-  };
-  int ob0 = 0, ob1 = 0, pb0 = 0, pb1 = 0;
-  if (gw < nb) {
-    ob0 = d.topo.bat_obs[gw]; ob1 = d.topo.bat_obs[gw + 1];
-    pb0 = d.topo.bat_pt[gw]; pb1 = d.topo.bat_pt[gw + 1];
-    if (lane == 0 && ob1 - ob0 <= SSFM_BATCH) issue(ob0, ob1, pb0, pb1, 0);
-  }
-  int st = 0;
-  unsigned ph = 0;
-  for (int b = gw; b < nb; b += warps) {
-    const int bn = b + warps;
-    int nb0 = 0, nb1 = 0, np0 = 0, np1 = 0;
-    if (bn < nb) {
-      nb0 = d.topo.bat_obs[bn]; nb1 = d.topo.bat_obs[bn + 1];
-      np0 = d.topo.bat_pt[bn]; np1 = d.topo.bat_pt[bn + 1];
-    }
-    __syncwarp();   // every lane is done with stage st ^ 1 (the batch before)
-    if (lane == 0 && bn < nb && nb1 - nb0 <= SSFM_BATCH) issue(nb0, nb1, np0, np1, st ^ 1);
-    const int my_pt = pb0 + lane;
-    const bool own = my_pt < pb1;
-    int ps = 0, pe = 0;
-    if (own) { ps = d.topo.pt_seg[my_pt]; pe = d.topo.pt_seg[my_pt + 1]; }
-    double acc[3] = {0.0, 0.0, 0.0};
-    const bool single = ob1 - ob0 <= SSFM_BATCH;
-    if (single) {
-      mbar_wait(&bar[wib][st], (ph >> st) & 1u);
-      ph ^= 1u << st;
-      const int i = ob0 + lane;
-      double val[3] = {0.0, 0.0, 0.0};
-      if (i < ob1) {
-        const PtwStage& S = stg[wib][st];
-        const int a0 = ob0 & ~3;
-        double G[8];
-        const double2* g2 = reinterpret_cast<const double2*>(S.G + 8 * lane);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) { const double2 t = g2[k]; G[2 * k] = t.x; G[2 * k + 1] = t.y; }
-        const int c = S.cam[i - a0], j = S.pt[i - a0];
-        double w[8], X[4];
-        ld_v4_ro(W + 8ll * c, w, pkeep);
-        ld_v4_ro(W + 8ll * c + 4, w + 4, pkeep);
-        ld_v4_ro(d.Xl + 4ll * j, X, pkeep);
-        const double u0 = (w[1] * X[2] - w[2] * X[1]) - w[3];
-        const double u1 = (w[2] * X[0] - w[0] * X[2]) - w[4];
-        const double u2 = (w[0] * X[1] - w[1] * X[0]) - w[5];
-        const double t0 = G[0] * u0 + G[1] * u1 + G[2] * u2 + G[6] * w[6];
-        const double t1 = G[3] * u0 + G[4] * u1 + G[5] * u2 + G[7] * w[6];
-        val[0] = G[0] * t0 + G[3] * t1;
-        val[1] = G[1] * t0 + G[4] * t1;
-        val[2] = G[2] * t0 + G[5] * t1;
-      }
-#pragma unroll
-      for (int k = 0; k < 3; ++k) sm[wib][lane][k] = val[k];
-      __syncwarp();
-      for (int o = ps; o < pe; ++o) {
-#pragma unroll
-        for (int k = 0; k < 3; ++k) acc[k] += sm[wib][o - ob0][k];
-      }
-    } else {
-      for (int base = ob0; base < ob1; base += SSFM_BATCH) {
-        const int i = base + lane;
-        double val[3] = {0.0, 0.0, 0.0};
-        if (i < ob1) {
-          const int c = ldg_stream_i(d.topo.pm_cam + i, pstream);
-          const int j = ldg_stream_i(d.topo.pm_pt + i, pstream);
-          double X[4];
-          ld_v4_ro(d.Xl + 4ll * j, X, pkeep);
-          ba_wobs<RO>(d, i, c, W, X, val);
-        }
-#pragma unroll
-        for (int k = 0; k < 3; ++k) sm[wib][lane][k] = val[k];
-        __syncwarp();
-        const int a = max(ps, base), e = min(pe, base + SSFM_BATCH);
-        for (int o = a; o < e; ++o) {
-#pragma unroll
-          for (int k = 0; k < 3; ++k) acc[k] += sm[wib][o - base][k];
-        }
-        __syncwarp();
-      }
-    }
-    if (own) {
-      double ci[6], wv[3];
-#if PTW_BULK_CI
-      if (single) {
-#pragma unroll
-        for (int k = 0; k < 6; ++k) ci[k] = stg[wib][st].Ci[6 * lane + k];
-      } else
-#endif
-      {
-#pragma unroll
-        for (int k = 0; k < 6; ++k) ci[k] = __ldg(d.Cinv + 6ll * my_pt + k);
-      }
-      sym3_matvec(ci, acc, wv);
-#pragma unroll
-      for (int k = 0; k < 3; ++k) st_hint(y + 4ll * my_pt + k, wv[k], pkeep);
-    }
-    st ^= 1;
-    ob0 = nb0; ob1 = nb1; pb0 = np0; pb1 = np1;
   }
 }
 
@@ -1107,14 +942,7 @@ ba_k_pcg(BADev d, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg
 // kernels (per-pass timing and roofline, ssfm_bench_operator).
 __global__ void __launch_bounds__(PTP_THREADS, PTP_MINB) k_op_point(BADev d, const double* v, double* y) {
   __shared__ double smp[PTP_THREADS / 32][SSFM_BATCH][3];
-  if (d.Gpm) {   // W of v: k_cam_wvec first
-#if PTW_BULK
-    ba_point_pass_wb<true>(d, d.Wc, y, smp);
-#else
-    ba_point_pass_w<true>(d, d.Wc, y, smp);
-#endif
-    return;
-  }
+  if (d.Gpm) { ba_point_pass_w<true>(d, d.Wc, y, smp); return; }   // W of v: k_cam_wvec first
 #if PTP_PIPE
   __shared__ PtpStage stg[PTP_THREADS / 32][2];
   ba_point_pass_pipe<true>(d, v, y, stg, smp);

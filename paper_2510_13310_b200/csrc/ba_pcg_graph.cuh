@@ -87,14 +87,7 @@ __global__ void k_g_init2(Dev d, CGGraphDev g, int nblk) {
 __global__ void __launch_bounds__(PTP_THREADS, PTP_MINB) k_g_point(BADev d, CGGraphDev g) {
   if (*(volatile int*)(g.ic + 3)) return;
   __shared__ double smp[PTP_THREADS / 32][SSFM_BATCH][3];
-  if (d.Gpm) {   // W (of p) is constant here
-#if PTW_BULK
-    ba_point_pass_wb<true>(d, d.Wc, d.yv, smp);
-#else
-    ba_point_pass_w<true>(d, d.Wc, d.yv, smp);
-#endif
-    return;
-  }
+  if (d.Gpm) { ba_point_pass_w<true>(d, d.Wc, d.yv, smp); return; }   // W (of p) is constant here
 #if PTP_PIPE
   __shared__ PtpStage stg[PTP_THREADS / 32][2];
   ba_point_pass_pipe<true>(d, g.p, d.yv, stg, smp);   // p is constant during this kernel
@@ -293,6 +286,193 @@ __global__ void __launch_bounds__(256) k_g_pupdate(BADev d, CGGraphDev g, int nb
   }
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x)
     g.p[s] = g.z[s] + beta * g.p[s];
+}
+
+// ---------------------------------------------------------------------------
+// The vector phases of one CG iteration (q = S p and p.q, alpha, x / r / z
+// and r.r / r.z, beta, p (+ its omega-form W), the scalars and the loop
+// condition) as ONE kernel: a thread-block cluster of GV_CL CTAs, each owning
+// a contiguous range of cameras. The only cross-CTA dependencies are the
+// three scalar reductions; they go through distributed shared memory (each
+// CTA's partial in its own shared memory, every CTA sums the GV_CL partials in
+// rank order after a cluster barrier), so every CTA takes identical
+// decisions. Replaces k_g_q, k_g_update, k_g_pupdate and k_g_scalars (four
+// launches and their grid-wide gaps per CG iteration).
+// ---------------------------------------------------------------------------
+#ifndef GV_CL
+#define GV_CL 8
+#endif
+#define GV_THREADS 1024
+
+template <int NV>
+__device__ __forceinline__ void gv_cluster_sum(cg::cluster_group& cl, double (&v)[NV], double* smred, double* slot) {
+  block_reduce<NV>(v, smred);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) slot[k] = v[k];
+  }
+  cl.sync();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = 0.0;
+  for (int r = 0; r < GV_CL; ++r) {
+    const double* rs = cl.map_shared_rank(slot, r);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] += rs[k];
+  }
+}
+
+__global__ void __cluster_dims__(GV_CL, 1, 1) __launch_bounds__(GV_THREADS, 1)
+k_g_vec(BADev d, FusedTopo fz, CGGraphDev g, CommDev cm, cudaGraphConditionalHandle hc) {
+  if (*(volatile int*)(g.ic + 3)) {   // solved before this iteration (uniform over the cluster):
+    if (blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(hc, 0u);   // end the WHILE loop
+    return;
+  }
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ double smred[(GV_THREADS / 32) * 2];
+  __shared__ double slot_pq[2], slot_rr[2];
+  const int rank = (int)cl.block_rank();
+  const int C = d.bp.C;
+  const int c0 = (int)((long long)C * rank / GV_CL), c1 = (int)((long long)C * (rank + 1) / GV_CL);
+  const int s0 = 8 * c0, s1 = 8 * c1;
+  const long long xoff = cm.nranks > 1 ? (long long)(*cm.epoch & 1) * cm.cap : 0;
+  const double lam = g.sc[0];
+  const bool shared = d.bp.focal_mode == 2;
+  const double pf = shared ? g.p[7] : 0.0;
+  // ---- q = S p (slot-major: 8 consecutive lanes hold one camera), p.q
+  double v1[2] = {0.0, 0.0};
+  for (int base = s0; base < s1; base += GV_THREADS) {
+    const int s = base + threadIdx.x;
+    if (base + (int)(threadIdx.x & ~31u) >= s1) continue;
+    const bool ok = s < s1;
+    const int c = ok ? s >> 3 : c0, k = s & 7;
+    const double pk = ok ? g.p[s] : 0.0;
+    const double pkt = (shared && k == 7) ? pf : pk;
+    double bp = 0.0;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const double pm = grp8_get(pkt, m);
+      if (ok) bp += d.Bc[64ll * c + 8 * k + m] * pm;
+    }
+    if (ok) {
+      double acc = 0.0;
+      if (cm.nranks > 1) {
+        acc = comm_peer_load(cm.buf[0] + xoff + s);
+        for (int rk = 1; rk < cm.nranks; ++rk) acc += comm_peer_load(cm.buf[rk] + xoff + s);
+      } else if (!g.fused) {
+        const int t0 = d.topo.cam_tile[c], t1 = d.topo.cam_tile[c + 1];
+        for (int t = t0; t < t1; ++t) acc += d.tilebuf[8ll * t + k];
+      } else {
+        for (int gq = 0; gq < g.ngrp; ++gq) acc += fz.gpart[(long long)gq * (8 * C) + s];
+      }
+      if (shared && k == 7) {
+        const double ft = bp + lam * d.Bc[64ll * c + 63] * pf - acc;
+        v1[1] += ft;             // the shared focal row: the cameras' shares
+        if (c) g.q[s] = 0.0;
+      } else {
+        double qk = bp + lam * d.Bc[64ll * c + 9 * k] * pk - acc;
+        if ((d.pinned[c] >> k) & 1) qk = pk;
+        g.q[s] = qk;
+        v1[0] += pk * qk;
+      }
+    }
+  }
+  gv_cluster_sum<2>(cl, v1, smred, slot_pq);
+  double pq = v1[0], qf = 0.0;
+  if (shared) {
+    qf = (d.pinned[0] >> 7 & 1) ? pf : v1[1];
+    pq += pf * qf;
+  }
+  if (!isfinite(pq) || pq <= 0.0) {
+    if (rank == 0 && threadIdx.x == 0) {
+      g.ic[2] = ST_CG_BREAKDOWN;
+      g.ic[3] = 1;
+      CGCtl* ctl = g.ctl;
+      ctl->tol = g.sc[2]; ctl->rho = g.sc[3]; ctl->rn = g.sc[4];
+      ctl->iters = g.ic[1]; ctl->flag = ST_CG_BREAKDOWN;
+      atomicOr(d.status, ST_CG_BREAKDOWN);
+      cudaGraphSetConditional(hc, 0u);
+    }
+    cl.sync();   // no CTA may exit while its shared slots are read
+    return;
+  }
+  const double alpha = g.sc[3] / pq;
+  // ---- x += a p, r -= a q, z = M r; r.r, r.z
+  double v2[2] = {0.0, 0.0};
+  for (int base = s0; base < s1; base += GV_THREADS) {
+    const int s = base + threadIdx.x;
+    if (base + (int)(threadIdx.x & ~31u) >= s1) continue;
+    const bool ok = s < s1;
+    const int c = ok ? s >> 3 : c0, k = s & 7;
+    double rk = 0.0;
+    if (ok) {
+      g.x[s] += alpha * g.p[s];
+      rk = g.r[s] - alpha * ((shared && s == 7) ? qf : g.q[s]);
+      g.r[s] = rk;
+    }
+    double zk = 0.0;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const double rm = grp8_get(rk, m);
+      if (ok) zk += d.Minv[64ll * c + 8 * k + m] * rm;
+    }
+    if (ok) g.z[s] = zk;
+    v2[0] += rk * rk;
+    v2[1] += rk * zk;
+  }
+  gv_cluster_sum<2>(cl, v2, smred, slot_rr);
+  const double rr = v2[0], rz = v2[1];
+  const int iters = g.ic[1] + 1;
+  const double rn = sqrt(rr);
+  int flag = 0, done = 0;
+  if (rn <= g.sc[2]) done = 1;
+  else if (iters >= g.ic[0]) { flag = ST_CG_MAXITER; done = 1; }
+  if (!done) {
+    // ---- p = z + beta p (+ W of p for the omega-form point pass)
+    const double beta = rz / g.sc[3];
+    const double pf_new = shared ? g.z[7] + beta * pf : 0.0;   // pf: p[7] read at entry
+    for (int base = s0; base < s1; base += GV_THREADS) {
+      const int s = base + threadIdx.x;
+      if (base + (int)(threadIdx.x & ~31u) >= s1) continue;
+      const bool ok = s < s1;
+      const int c = ok ? s >> 3 : c0, k = s & 7;
+      double pk = ok ? g.z[s] + beta * g.p[s] : 0.0;
+      if (ok) g.p[s] = pk;
+      if (d.Gpm) {
+        const double pc0 = grp8_get(pk, 0), pc1 = grp8_get(pk, 1), pc2 = grp8_get(pk, 2), pc3 = grp8_get(pk, 3);
+        const double pc4 = grp8_get(pk, 4), pc5 = grp8_get(pk, 5), pc6 = grp8_get(pk, 6), pc7 = grp8_get(pk, 7);
+        if (ok && k == 0) {
+          const double* cb = reinterpret_cast<const double*>(d.camlin + c);
+          const double qw = cb[9], qx = cb[10], qy = cb[11], qz = cb[12], s2 = 2.0 * cb[22];
+          const double o0 = s2 * (qw * pc1 - pc0 * qx - (qy * pc3 - qz * pc2));
+          const double o1 = s2 * (qw * pc2 - pc0 * qy - (qz * pc1 - qx * pc3));
+          const double o2 = s2 * (qw * pc3 - pc0 * qz - (qx * pc2 - qy * pc1));
+          const double t0 = cb[14], t1 = cb[15], t2 = cb[16];
+          double* w = d.Wc + 8ll * c;
+          w[0] = o0; w[1] = o1; w[2] = o2;
+          w[3] = (o1 * t2 - o2 * t1) + pc4;
+          w[4] = (o2 * t0 - o0 * t2) + pc5;
+          w[5] = (o0 * t1 - o1 * t0) + pc6;
+          w[6] = shared ? pf_new : (d.bp.focal_mode == 1 ? pc7 : 0.0);
+          w[7] = 0.0;
+        }
+      }
+    }
+  }
+  if (rank == 0 && threadIdx.x == 0) {
+    g.ic[1] = iters;
+    g.sc[4] = rn;
+    if (!done) g.sc[3] = rz;   // rho of the next iteration
+    g.ic[2] = flag;
+    g.ic[3] = done;
+    if (done) {
+      CGCtl* ctl = g.ctl;
+      ctl->tol = g.sc[2]; ctl->rho = g.sc[3]; ctl->rn = rn;
+      ctl->iters = iters; ctl->flag = flag;
+      if (flag) atomicOr(d.status, flag);
+    }
+    cudaGraphSetConditional(hc, done ? 0u : 1u);
+  }
+  cl.sync();   // the shared slots stay valid until every CTA has read them
 }
 
 // scalars of the iteration and the loop condition (one block)

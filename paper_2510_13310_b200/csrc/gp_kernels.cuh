@@ -64,6 +64,7 @@ struct GPDev {
   double* partials;
   int* status;
   double lam;
+  const double* lamp;     // device-resident lambda (LM loop as a CUDA graph) or nullptr: lam / the argument
 };
 
 __device__ __forceinline__ double gp_at(const GPDev& g, int cam, double a) {
@@ -300,6 +301,7 @@ __global__ void gp_k_scale_norm(GPDev g, double* part) {
 // per lambda: stage 1 (scales) folded into the point blocks + stage 2 inverse
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) gp_k_pt_elim(GPDev g, double lam) {
+  if (g.lamp) lam = *g.lamp;
   __shared__ double sm[8][SSFM_BATCH][9];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int warps = (gridDim.x * blockDim.x) >> 5;
@@ -385,6 +387,7 @@ __device__ __forceinline__ void gp_u_mul(double at, double a, double inv, const 
 // sum U' M U'^T (6), sum U' y0 (3)
 #define GPE_V 18
 __global__ void __launch_bounds__(SSFM_TILE) gp_k_cam_elim(GPDev g, double lam) {
+  if (g.lamp) lam = *g.lamp;
   __shared__ double sm[(SSFM_TILE / 32) * GPE_V];
   const int t = blockIdx.x;
   const int o0 = g.topo.tile_obs[t], o1 = g.topo.tile_obs[t + 1];
@@ -448,6 +451,7 @@ __global__ void __launch_bounds__(SSFM_TILE) gp_k_cam_elim(GPDev g, double lam) 
 }
 
 __global__ void gp_k_camprec(GPDev g, double lam, const double* camsum) {
+  if (g.lamp) lam = *g.lamp;
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= g.gp.C) return;
   double s[GPE_V];
@@ -716,6 +720,7 @@ gp_k_pcg(GPDev g, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg
   __shared__ double smred[(NT / 32) * 8];
   __shared__ double smb[4];
   extern __shared__ double gdyn[];
+  if (g.lamp) lam = *g.lamp;
   g.lam = lam;
   const int S = 4 * g.gp.C;
   const int stride = gridDim.x * blockDim.x;
@@ -867,7 +872,7 @@ __global__ void __launch_bounds__(256) gp_k_backsub(GPDev g, const double* __res
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long Np = g.Npad;
-  const double lam = g.lam;
+  const double lam = g.lamp ? *g.lamp : g.lam;   // LM graph: lambda on the device
   for (int b = gw; b < g.topo.nb; b += warps) {
     const int ob0 = g.topo.bat_obs[b], ob1 = g.topo.bat_obs[b + 1];
     const int pb0 = g.topo.bat_pt[b], pb1 = g.topo.bat_pt[b + 1];

@@ -296,6 +296,17 @@ static int dalloc(ssfm_handle* h, T** ptr, size_t count) {
 
 static inline int nblk(long long n, int t) { return (int)((n + t - 1) / t); }
 
+// zero / copy on the stream as kernels (see k_fill_u32 in common.cuh)
+static cudaError_t zero_async(void* p, size_t bytes, cudaStream_t st) {
+  const long long n = (long long)(bytes / 4);
+  k_fill_u32<<<std::max(1, std::min(nblk(n, 256), 1184)), 256, 0, st>>>(static_cast<unsigned*>(p), n, 0u);
+  return cudaGetLastError();
+}
+static cudaError_t copy_async(double* dst, const double* src, long long n, cudaStream_t st) {
+  k_copy_f64<<<std::max(1, std::min(nblk(n, 256), 1184)), 256, 0, st>>>(dst, src, n);
+  return cudaGetLastError();
+}
+
 static void free_handle(ssfm_handle* h) {
   if (!h) return;
   for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
@@ -598,6 +609,9 @@ static int setup_ba_pcg(ssfm_handle* h, cudaStream_t st) {
       // ba_k_lin_points; SSFM_LIN2=0: the two evaluating passes)
       const char* le = getenv("SSFM_LIN2");
       if (!(le && le[0] == '0')) DALLOC(d.Rpm, 4ll * d.Npad);
+      // preconditioner point terms streamed camera-major (SSFM_KOBS=0: gathered)
+      const char* ke = getenv("SSFM_KOBS");
+      if (!(ke && ke[0] == '0')) DALLOC(d.Kcm, 8ll * d.Npad);
     }
   }
   const char* ge = getenv("SSFM_PCG_GRAPH");
@@ -1094,11 +1108,12 @@ static int launch_cost(ssfm_handle* h, const double* theta, cudaStream_t st) {
 // linearize(theta) on device (async); grad max / norm into misc.scal
 static int launch_linearize(ssfm_handle* h, const double* theta, double* r_out, double* J_out,
                             cudaStream_t st) {
-  CU(cudaMemsetAsync(h->misc->scal + SC_GMAX, 0, sizeof(double), st));
+  CU(zero_async(h->misc->scal + SC_GMAX, sizeof(double), st));
   if (h->kind == 0) {
     BADev& d = h->ba;
     ba_k_prep<<<h->cam_blocks, 256, 0, st>>>(d, theta);
-    if (d.camlin) CU(cudaMemcpyAsync(d.camlin, d.cams, sizeof(BACam) * d.bp.C, cudaMemcpyDeviceToDevice, st));
+    if (d.camlin) CU(copy_async(reinterpret_cast<double*>(d.camlin), reinterpret_cast<const double*>(d.cams),
+                                (long long)(sizeof(BACam) / 8) * d.bp.C, st));
     if (d.Rpm && !r_out && !J_out) {   // each observation evaluated once (camera tiles), then point sums
       if (d.topo.nt) ba_k_lin_tile<<<d.topo.nt, SSFM_TILE, 0, st>>>(d, theta);
       ba_k_lin_points<<<h->lin_blocks, 256, 0, st>>>(d, theta, h->red);
@@ -1122,6 +1137,8 @@ static int launch_linearize(ssfm_handle* h, const double* theta, double* r_out, 
       if ((rc = allreduce(h, h->ar_tmp + 1, 1, AR_SUM, st))) return rc;
       k_sum_partials<<<1, 1024, 0, st>>>(h->red + (long long)h->lin_blocks * 8, h->cam_blocks, h->ar_tmp + 2);
       k_add2<<<1, 1, 0, st>>>(h->ar_tmp + 1, h->ar_tmp + 2, d.scal + SC_GNORM2);
+      // shared focal: its gradient from the (replicated) camera sums
+      if (d.bp.focal_mode == 2) { ba_k_shared_focal_grad<<<1, 256, 0, st>>>(d); count_launch(h); }
       if ((rc = allreduce(h, d.scal + SC_GMAX, 1, AR_MAX, st))) return rc;
       count_launch(h, 8);
     }
@@ -1233,8 +1250,8 @@ static int alloc_gdev(ssfm_handle* h) {
   DALLOC(g.sc, 8);
   DALLOC(g.ic, 8);
   g.ctl = &h->misc->ctl;
-  g.fused = h->fz.G > 0 ? 1 : 0;
-  g.ngrp = h->fz.ngrp;
+  g.fused = (h->kind == 0 && h->fz.G > 0) ? 1 : 0;
+  g.ngrp = h->kind == 0 ? h->fz.ngrp : 0;
   return SSFM_OK;
 }
 
@@ -1267,11 +1284,19 @@ static void capture_ba_pcg_body(ssfm_handle* h, cudaStream_t cs, cudaGraphCondit
     k_gx_post<<<CGV_BLOCKS, 256, 0, cs>>>(d, h->fz, g, h->cm);
     k_gx_barrier<<<1, 32, 0, cs>>>(g, h->cm);
   }
-  k_g_q<<<CGV_BLOCKS, 256, 0, cs>>>(d, h->fz, g, h->cm);
-  k_g_update<<<CGV_BLOCKS, 256, 0, cs>>>(d, g, CGV_BLOCKS);
-  k_g_pupdate<<<CGV_BLOCKS, 256, 0, cs>>>(d, g, CGV_BLOCKS);
-  k_g_scalars<<<1, 32, 0, cs>>>(d, g, CGV_BLOCKS, hc);
-  h->graph_body_kernels = (g.fused ? 1 : 2) + (sharded(h) ? 2 : 0) + 4;
+  // the vector phases: one thread-block cluster kernel (k_g_vec), or four
+  // grid-wide kernels (SSFM_GVEC=0)
+  const char* gv = getenv("SSFM_GVEC");
+  const bool cluster = !(gv && gv[0] == '0');
+  if (cluster) {
+    k_g_vec<<<GV_CL, GV_THREADS, 0, cs>>>(d, h->fz, g, h->cm, hc);
+  } else {
+    k_g_q<<<CGV_BLOCKS, 256, 0, cs>>>(d, h->fz, g, h->cm);
+    k_g_update<<<CGV_BLOCKS, 256, 0, cs>>>(d, g, CGV_BLOCKS);
+    k_g_pupdate<<<CGV_BLOCKS, 256, 0, cs>>>(d, g, CGV_BLOCKS);
+    k_g_scalars<<<1, 32, 0, cs>>>(d, g, CGV_BLOCKS, hc);
+  }
+  h->graph_body_kernels = (g.fused ? 1 : 2) + (sharded(h) ? 2 : 0) + (cluster ? 1 : 4);
 }
 
 static cudaError_t prepare_fused_of(const ssfm_handle* h) {
@@ -1325,16 +1350,32 @@ static int build_pcg_graph(ssfm_handle* h) {
 }
 
 // GP: the PCG as a CUDA graph (gp_pcg_graph.cuh); single-rank two-pass handles
-static int build_gp_pcg_graph(ssfm_handle* h) {
+// one CG iteration of the GP graph PCG (the WHILE body), captured on cs
+static void capture_gp_pcg_body(ssfm_handle* h, cudaStream_t cs, cudaGraphConditionalHandle hc) {
   CGGraphDev& g = h->gdev;
-  g.x = h->x; g.r = h->r; g.z = h->z; g.p = h->p; g.q = h->q;
-  DALLOC(g.partA, 2 * CGV_BLOCKS + 2);
-  DALLOC(g.partB, 2 * CGV_BLOCKS + 2);
-  DALLOC(g.sc, 8);
-  DALLOC(g.ic, 8);
-  g.ctl = &h->misc->ctl;
-  g.fused = 0;
-  g.ngrp = 0;
+  GPDev& d = h->gp;
+  int occ_p = 0, occ_c = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, (const void*)k_gg_point, PCG_THREADS, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, (const void*)k_gg_camera, PCG_THREADS, 0);
+  k_gg_point<<<std::max(1, occ_p) * h->num_sms, PCG_THREADS, 0, cs>>>(d, g);
+  if (d.topo.nt) k_gg_camera<<<std::max(1, occ_c) * h->num_sms, PCG_THREADS, 0, cs>>>(d, g);
+  const char* gv = getenv("SSFM_GVEC");
+  const bool cluster = !(gv && gv[0] == '0');
+  if (cluster) {   // the vector phases as one thread-block cluster kernel
+    k_gg_vec<<<GV_CL, GV_THREADS, 0, cs>>>(d, g, hc);
+  } else {
+    k_gg_q<<<CGV_BLOCKS, 256, 0, cs>>>(d, g);
+    k_gg_update<<<CGV_BLOCKS, 256, 0, cs>>>(d, g, CGV_BLOCKS);
+    k_gg_pupdate<<<CGV_BLOCKS, 256, 0, cs>>>(d, g, CGV_BLOCKS);
+    k_g_scalars<<<1, 32, 0, cs>>>(d, g, CGV_BLOCKS, hc);
+  }
+  h->graph_body_kernels = 2 + (cluster ? 1 : 4);
+}
+
+// GP: the PCG as a CUDA graph (gp_pcg_graph.cuh); single-rank two-pass handles
+static int build_gp_pcg_graph(ssfm_handle* h) {
+  int rc = alloc_gdev(h);
+  if (rc) return rc;
   cudaGraphConditionalHandle hc;
   cudaGraphNodeParams cp = {};
   cudaGraphNode_t cn;
@@ -1359,17 +1400,7 @@ static int build_gp_pcg_graph(ssfm_handle* h) {
   if ((e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking))) return unavailable(e);
   if ((e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed)))
     return unavailable(e);
-  GPDev& d = h->gp;
-  int occ_p = 0, occ_c = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, (const void*)k_gg_point, PCG_THREADS, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, (const void*)k_gg_camera, PCG_THREADS, 0);
-  k_gg_point<<<std::max(1, occ_p) * h->num_sms, PCG_THREADS, 0, cs>>>(d, g);
-  if (d.topo.nt) k_gg_camera<<<std::max(1, occ_c) * h->num_sms, PCG_THREADS, 0, cs>>>(d, g);
-  k_gg_q<<<CGV_BLOCKS, 256, 0, cs>>>(d, g);
-  k_gg_update<<<CGV_BLOCKS, 256, 0, cs>>>(d, g, CGV_BLOCKS);
-  k_gg_pupdate<<<CGV_BLOCKS, 256, 0, cs>>>(d, g, CGV_BLOCKS);
-  k_g_scalars<<<1, 32, 0, cs>>>(d, g, CGV_BLOCKS, hc);
-  h->graph_body_kernels = 6;
+  capture_gp_pcg_body(h, cs, hc);
   if ((e = cudaStreamEndCapture(cs, &body))) return unavailable(e);
   if ((e = cudaGraphInstantiate(&h->pcg_exec, h->pcg_graph, 0))) return unavailable(e);
   cudaStreamDestroy(cs);
@@ -1453,11 +1484,12 @@ static int launch_pcg(ssfm_handle* h, double lam, const ssfm_lm_config* cfg, cud
 
 // damped elimination blocks and the preconditioner at lambda (async)
 static int launch_solve_pre(ssfm_handle* h, double lam, cudaStream_t st) {
-  CU(cudaMemsetAsync(&h->misc->status, 0, sizeof(int), st));
-  CU(cudaMemsetAsync(&h->misc->ctl, 0, sizeof(CGCtl), st));
+  CU(zero_async(&h->misc->status, sizeof(int), st));
+  CU(zero_async(&h->misc->ctl, sizeof(CGCtl), st));
   if (h->kind == 0) {
     BADev& d = h->ba;
     ba_k_ptinv<<<nblk(d.bp.P, 256), 256, 0, st>>>(d, lam);
+    if (d.Kcm) { ba_k_kobs<<<nblk(d.topo.N, 256), 256, 0, st>>>(d); count_launch(h); }
     if (d.topo.nt) ba_k_precond<<<d.topo.nt, SSFM_TILE, 0, st>>>(d);
     const double* cs = nullptr;
     if (sharded(h)) {
@@ -1470,7 +1502,15 @@ static int launch_solve_pre(ssfm_handle* h, double lam, cudaStream_t st) {
     ba_k_camprec<<<nblk(d.bp.C, 64), 64, 0, st>>>(d, lam, cs);
     count_launch(h, 3);
     if (d.bp.focal_mode == 2) {
-      ba_k_shared_focal_prec<<<1, 256, 0, st>>>(d, nblk(d.bp.P, 256));
+      const double* wsum = nullptr;
+      if (sharded(h)) {   // sum_j a_j^T Cinv_j a_j over every rank's points
+        k_sum_partials<<<1, 1024, 0, st>>>(d.fwpart, nblk(d.bp.P, 256), h->ar_tmp + 8);
+        int rc = allreduce(h, h->ar_tmp + 8, 1, AR_SUM, st);
+        if (rc) return rc;
+        wsum = h->ar_tmp + 8;
+        count_launch(h);
+      }
+      ba_k_shared_focal_prec<<<1, 256, 0, st>>>(d, nblk(d.bp.P, 256), wsum);
       count_launch(h);
     }
   } else {
@@ -1550,6 +1590,10 @@ static int launch_post_step(ssfm_handle* h, double* theta, cudaStream_t st) {
 static int read_misc(ssfm_handle* h, cudaStream_t st) {
   CU(cudaMemcpyAsync(h->hmisc, h->misc, sizeof(Misc), cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
+  // a collective that timed out anywhere since the solve began (cost,
+  // linearize, solve) leaves this rank's exchanged values invalid: fail loudly
+  if (sharded(h) && (h->hmisc->status & ST_COMM_TIMEOUT))
+    return set_err(SSFM_COMM_ERROR, "a peer rank did not reach the exchange in time (SSFM_COMM_TIMEOUT_S)");
   return SSFM_OK;
 }
 
@@ -1645,7 +1689,7 @@ extern "C" int ssfm_solve_normal(ssfm_handle* h, double lambda, const ssfm_lm_co
   cudaStream_t st = (cudaStream_t)stream;
   int rc = launch_solve(h, lambda, cfg, st);
   if (rc) return rc;
-  if (delta) CU(cudaMemcpyAsync(delta, h->delta, sizeof(double) * h->total_params, cudaMemcpyDeviceToDevice, st));
+  if (delta) CU(copy_async(delta, h->delta, h->total_params, st));
   if ((rc = sync_status(h, st))) return rc;
   if ((rc = read_misc(h, st))) return rc;
   const Misc& m = *h->hmisc;
@@ -1658,7 +1702,7 @@ extern "C" int ssfm_solve_normal(ssfm_handle* h, double lambda, const ssfm_lm_co
 extern "C" int ssfm_post_step(ssfm_handle* h, double* theta, void* stream) {
   if (!h || !theta) return set_err(SSFM_INVALID_ARGUMENT, "null argument");
   cudaStream_t st = (cudaStream_t)stream;
-  CU(cudaMemsetAsync(&h->misc->status, 0, sizeof(int), st));
+  CU(zero_async(&h->misc->status, sizeof(int), st));
   int rc = launch_post_step(h, theta, st);
   if (rc) return rc;
   if ((rc = read_misc(h, st))) return rc;
@@ -1714,7 +1758,7 @@ static cudaError_t cap_handle(cudaStream_t st, cudaGraphConditionalHandle* hc) {
 }
 
 static bool lm_graph_wanted(const ssfm_handle* h) {
-  if (h->kind != 0 || sharded(h) || h->lm_state < 0) return false;
+  if (sharded(h) || h->lm_state < 0) return false;
   const char* e = getenv("SSFM_LM_GRAPH");
   return !(e && e[0] == '0');
 }
@@ -1744,11 +1788,14 @@ static int build_lm_graph(ssfm_handle* h, const ssfm_lm_config* cfg) {
     int rc = alloc_gdev(h);
     if (rc) return rc;
   }
+  const bool ba = h->kind == 0;
+  double* scal = ba ? h->ba.scal : h->gp.scal;
   cudaStream_t s0 = nullptr, s1 = nullptr, s2 = nullptr;
   auto unavailable = [&](cudaError_t e) {
     cudaGetLastError();
     h->capturing = false;
     h->ba.lamp = nullptr;
+    h->gp.lamp = nullptr;
     for (cudaStream_t x : {s0, s1, s2}) {
       if (!x) continue;
       cudaGraph_t junk = nullptr;
@@ -1784,6 +1831,7 @@ static int build_lm_graph(ssfm_handle* h, const ssfm_lm_config* cfg) {
   const long long n = h->total_params;
   h->capturing = true;
   d.lamp = &S->lam;   // captured kernels read lambda from the loop state
+  h->gp.lamp = &S->lam;
   const long long k0 = h->prof.kernel_launches;
   int rc = SSFM_OK;
   if ((e = cudaStreamBeginCaptureToGraph(s0, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed)))
@@ -1796,7 +1844,7 @@ static int build_lm_graph(ssfm_handle* h, const ssfm_lm_config* cfg) {
     return unavailable(e);
   const long long k1 = h->prof.kernel_launches;
   if ((rc = launch_linearize(h, h->theta, nullptr, nullptr, s1))) { unavailable(cudaErrorUnknown); return rc; }
-  k_lm_gradcheck<<<1, 1, 0, s1>>>(S, d.scal + SC_GMAX);
+  k_lm_gradcheck<<<1, 1, 0, s1>>>(S, scal + SC_GMAX);
   h->lm_k_lin = h->prof.kernel_launches - k1 + 1;
   if ((e = cudaStreamEndCapture(s1, &blin))) return unavailable(e);
   if ((e = cap_handle(s0, &hsolve))) return unavailable(e);
@@ -1812,23 +1860,31 @@ static int build_lm_graph(ssfm_handle* h, const ssfm_lm_config* cfg) {
   const double tol = cfg->cg_tol;
   if (gpcg) {
     k_g_setparams_lm<<<1, 1, 0, s1>>>(g, S, tol, max_it);
-    k_g_init<<<CGV_BLOCKS, 256, 0, s1>>>(d, g);
-    if (d.Gpm) { k_cam_wvec<<<h->cam_blocks, 256, 0, s1>>>(d, g.p, d.Wc); count_launch(h); }
-    k_g_init2<<<1, 32, 0, s1>>>(d, g, CGV_BLOCKS);
+    if (ba) {
+      k_g_init<<<CGV_BLOCKS, 256, 0, s1>>>(d, g);
+      if (d.Gpm) { k_cam_wvec<<<h->cam_blocks, 256, 0, s1>>>(d, g.p, d.Wc); count_launch(h); }
+      k_g_init2<<<1, 32, 0, s1>>>(d, g, CGV_BLOCKS);
+    } else {
+      k_gg_init<<<CGV_BLOCKS, 256, 0, s1>>>(h->gp, g);
+      k_g_init2<<<1, 32, 0, s1>>>(h->gp, g, CGV_BLOCKS);
+    }
     if ((e = cap_handle(s1, &hpcg))) return unavailable(e);
     k_g_cond_init<<<1, 1, 0, s1>>>(g, hpcg);
     count_launch(h, 5);
     if ((e = cap_cond(s1, hpcg, cudaGraphCondTypeWhile, &bpcg))) return unavailable(e);
-    if (!g.fused) set_l2_window(h, s2, d.yv, sizeof(double) * 4 * (size_t)d.bp.P);
+    if (ba && !g.fused) set_l2_window(h, s2, d.yv, sizeof(double) * 4 * (size_t)d.bp.P);
     if ((e = cudaStreamBeginCaptureToGraph(s2, bpcg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed)))
       return unavailable(e);
-    capture_ba_pcg_body(h, s2, hpcg);
+    if (ba) capture_ba_pcg_body(h, s2, hpcg);
+    else capture_gp_pcg_body(h, s2, hpcg);
     if ((e = cudaStreamEndCapture(s2, &bpcg))) return unavailable(e);
   } else {
-    double lam = 0.0;   // read from d.lamp by the kernel
+    double lam = 0.0;   // read from the device lambda by the kernel
     CGCtl* ctl = &h->misc->ctl;
     void* a[13];
-    a[0] = &d; a[1] = &h->fz; a[2] = &h->cm; a[3] = &lam; a[4] = (void*)&max_it; a[5] = (void*)&tol;
+    if (ba) a[0] = &d;
+    else a[0] = &h->gp;
+    a[1] = &h->fz; a[2] = &h->cm; a[3] = &lam; a[4] = (void*)&max_it; a[5] = (void*)&tol;
     a[6] = &h->x; a[7] = &h->r; a[8] = &h->z; a[9] = &h->p; a[10] = &h->q;
     a[11] = &h->part; a[12] = &ctl;
     if ((e = cudaLaunchCooperativeKernel(h->pcg_fn, dim3(h->pcg_grid), dim3(h->pcg_threads), a, h->pcg_smem, s1)))
@@ -1840,7 +1896,7 @@ static int build_lm_graph(ssfm_handle* h, const ssfm_lm_config* cfg) {
   k_axpy_theta<<<nblk(n, 256), 256, 0, s1>>>(h->theta, h->delta, h->cand, n);
   if ((rc = launch_post_step(h, h->cand, s1))) { unavailable(cudaErrorUnknown); return rc; }
   if ((rc = launch_cost(h, h->cand, s1))) { unavailable(cudaErrorUnknown); return rc; }
-  k_lm_decide<CGCtl><<<1, 1, 0, s1>>>(S, &h->misc->status, &h->misc->ctl, d.scal + SC_COST, h->lrecs);
+  k_lm_decide<CGCtl><<<1, 1, 0, s1>>>(S, &h->misc->status, &h->misc->ctl, scal + SC_COST, h->lrecs);
   k_lm_accept<<<std::min(nblk(n, 256), 4 * h->num_sms), 256, 0, s1>>>(S, h->cand, h->theta, n);
   h->lm_k_solve = h->prof.kernel_launches - k2 + 5;   // + marks, axpy, decide, accept
   if ((e = cudaStreamEndCapture(s1, &bsolve))) return unavailable(e);
@@ -1849,6 +1905,7 @@ static int build_lm_graph(ssfm_handle* h, const ssfm_lm_config* cfg) {
   if ((e = cudaStreamEndCapture(s0, &body))) return unavailable(e);
   h->capturing = false;
   d.lamp = nullptr;
+  h->gp.lamp = nullptr;
   h->prof.kernel_launches = k0;   // capture is not execution
   if ((e = cudaGraphInstantiate(&h->lm_exec, h->lm_graph, 0))) return unavailable(e);
   for (cudaStream_t x : {s0, s1, s2}) cudaStreamDestroy(x);
@@ -1883,7 +1940,7 @@ static int lm_solve_graph(ssfm_handle* h, double* theta_io, const ssfm_lm_config
   H.max_it = cfg->max_iterations;
   H.cap = h->lrec_cap;
   CU(cudaMemcpyAsync(h->lms, h->hlms, sizeof(LMState), cudaMemcpyHostToDevice, st));
-  CU(cudaMemcpyAsync(h->theta, theta_io, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  CU(copy_async(h->theta, theta_io, n, st));
   h->prof.pcg_ms = h->prof.lin_ms = h->prof.all_ms = 0;
   h->prof.pcg_launches = h->prof.lin_launches = h->prof.all_launches = 0;
   h->prof.cg_iters = 0;
@@ -1891,12 +1948,12 @@ static int lm_solve_graph(ssfm_handle* h, double* theta_io, const ssfm_lm_config
   for (int k = 0; k < 5; ++k) h->prof.phase_ms[k] = 0;
   int rc = launch_cost(h, h->theta, st);
   if (rc) return rc;
-  k_lm_init<<<1, 1, 0, st>>>(h->lms, h->ba.scal + SC_COST);
+  k_lm_init<<<1, 1, 0, st>>>(h->lms, (h->kind == 0 ? h->ba.scal : h->gp.scal) + SC_COST);
   count_launch(h);
   if (cfg->max_iterations >= 1) CU(cudaGraphLaunch(h->lm_exec, st));
   CU(cudaMemcpyAsync(h->hlms, h->lms, sizeof(LMState), cudaMemcpyDeviceToHost, st));
   CU(cudaMemcpyAsync(h->hlrecs, h->lrecs, sizeof(LMRecDev) * h->lrec_cap, cudaMemcpyDeviceToHost, st));
-  CU(cudaMemcpyAsync(theta_io, h->theta, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  CU(copy_async(theta_io, h->theta, n, st));
   CU(cudaStreamSynchronize(st));
   CU(cudaGetLastError());
   const LMState R = *h->hlms;
@@ -1946,6 +2003,7 @@ extern "C" int ssfm_lm_solve(ssfm_handle* h, double* theta_io, const ssfm_lm_con
   cudaStream_t st = (cudaStream_t)stream;
   using clk = std::chrono::steady_clock;
   int rc;
+  CU(zero_async(&h->misc->status, sizeof(int), st));
   if (lm_graph_wanted(h)) {
     rc = lm_solve_graph(h, theta_io, cfg, recs, cap, n_recs, termination, st);
     if (rc != -1) return rc;   // -1: no graph on this runtime, run the host loop
@@ -1953,7 +2011,7 @@ extern "C" int ssfm_lm_solve(ssfm_handle* h, double* theta_io, const ssfm_lm_con
   if (n_recs) *n_recs = 0;
   int term = SSFM_TERM_MAX_ITER;
   const long long n = h->total_params;
-  CU(cudaMemcpyAsync(h->theta, theta_io, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  CU(copy_async(h->theta, theta_io, n, st));
   if ((rc = launch_cost(h, h->theta, st))) return rc;
   if ((rc = read_misc(h, st))) return rc;
   double cost = h->hmisc->scal[SC_COST];
@@ -2003,7 +2061,7 @@ extern "C" int ssfm_lm_solve(ssfm_handle* h, double* theta_io, const ssfm_lm_con
     }
     const int code = status_to_code(m.status);
     if (code == SSFM_COMM_ERROR) {   // a peer did not answer: the exchanged values are not valid
-      CU(cudaMemcpyAsync(theta_io, h->theta, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+      CU(copy_async(theta_io, h->theta, n, st));
       CU(cudaStreamSynchronize(st));
       if (n_recs) *n_recs = std::min(nrec, (int)cap);
       return set_err(SSFM_COMM_ERROR, status_msg(m.status, m));
@@ -2049,7 +2107,7 @@ extern "C" int ssfm_lm_solve(ssfm_handle* h, double* theta_io, const ssfm_lm_con
       lam = std::min(lam * cfg->lambda_up, cfg->lambda_max);
     }
   }
-  CU(cudaMemcpyAsync(theta_io, h->theta, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  CU(copy_async(theta_io, h->theta, n, st));
   CU(cudaStreamSynchronize(st));
   if (n_recs) *n_recs = std::min(nrec, (int)cap);
   if (termination) *termination = term;
@@ -2091,8 +2149,6 @@ extern "C" int ssfm_profile_get(const ssfm_handle* h, int32_t kind, double* ms, 
 extern "C" int ssfm_comm_init(ssfm_handle* h, int32_t rank, int32_t nranks, void* ipc_handle_out,
                               void** region_out) {
   if (!h) return set_err(SSFM_INVALID_ARGUMENT, "null argument");
-  if (h->kind == 0 && h->ba.bp.focal_mode == 2)
-    return set_err(SSFM_INVALID_ARGUMENT, "point sharding: shared focal not supported");
   if (nranks < 1 || nranks > SSFM_MAX_RANKS || rank < 0 || rank >= nranks)
     return set_err(SSFM_INVALID_ARGUMENT, "bad rank / nranks");
   if (h->region) return set_err(SSFM_INVALID_ARGUMENT, "exchange region already initialised");
@@ -2152,6 +2208,23 @@ extern "C" int ssfm_comm_connect(ssfm_handle* h, const void* ipc_handles, void* 
     cm.buf[r] = reinterpret_cast<double*>(static_cast<char*>(ptr) + 256);
   }
   cm.nranks = R;
+  // build the graph PCG now, from the connecting thread: building it inside
+  // the first solve would allocate device memory while a peer shard's kernel
+  // may already wait in an exchange. With several shards on one device, a
+  // device allocation (like a NULL-stream command) serialises the streams
+  // around it, so the peer would wait for this shard's kernels forever.
+  if (h->kind == 0 && h->graph_state == 1 && !h->graph_sharded) {
+    cudaGraphExecDestroy(h->pcg_exec);
+    cudaGraphDestroy(h->pcg_graph);
+    h->pcg_exec = nullptr;
+    h->pcg_graph = nullptr;
+    h->graph_state = 0;
+  }
+  if (h->kind == 0 && h->graph_state == 0) {
+    int rc = build_pcg_graph(h);
+    if (rc) return rc;
+    h->graph_sharded = true;
+  }
   return SSFM_OK;
 }
 

@@ -130,8 +130,6 @@ class ShardedBAProblem(_Sharded, BAProblem):
                  rank: int | None = None, world: int | None = None, group=None, comm: str = "torch"):
         arr = as_arrays(scene)
         rank, world = self._init_shard(rank, world, group, comm)
-        if shared_focal and optimize_focal:
-            raise ValueError("shared_focal is not supported by the sharded solver")
         local, (p0, p1), obs = shard_arrays(arr, rank, world)
         if local.num_observations == 0:
             raise ValueError(f"rank {rank} owns no observations (world {world} too large for this scene)")

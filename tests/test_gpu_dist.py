@@ -38,12 +38,13 @@ def scene(cams=40, pts=3000, k=5, seed=0):
     return synth.perturb_arrays(obs, rot_deg=1.0, center_frac=0.01, focal_frac=0.02, point_frac=0.005, seed=1)
 
 
-def solve_local_shards(gpu, st, world, cfg, fused="1", graph="0"):
+def solve_local_shards(gpu, st, world, cfg, fused="1", graph="0", shared_focal=False):
     os.environ["SSFM_PCG_SMS"] = str(140 // world)
     os.environ["SSFM_FUSED"] = fused
     os.environ["SSFM_PCG_GRAPH"] = graph
     try:
-        probs = [bd.ShardedBAProblem(st, b2.RobustLoss("huber", 1.0), rank=r, world=world, comm="local")
+        probs = [bd.ShardedBAProblem(st, b2.RobustLoss("huber", 1.0), shared_focal=shared_focal, rank=r,
+                                     world=world, comm="local")
                  for r in range(world)]
         bd.connect_local(probs)
     finally:
@@ -52,31 +53,64 @@ def solve_local_shards(gpu, st, world, cfg, fused="1", graph="0"):
         os.environ.pop("SSFM_PCG_GRAPH")
     out = [None] * world
 
-    def work(r):
-        with gpu.cuda.stream(gpu.cuda.Stream()):
+    def work(r, stream):
+        with gpu.cuda.stream(stream):
             p = probs[r]
             out[r] = b2.lm_solve(p, p.encode(), cfg)
 
-    run_shards(work, world, 300)   # raises the first shard error
+    run_shards(work, probs, 300)   # raises the first shard error
     return probs, out
 
 
-def run_shards(work, n, timeout):
-    """One host thread per same-device shard. Unreachable handles of earlier
-    tests are destroyed first and the garbage collector is paused meanwhile: a
-    handle destroyed inside a shard's thread synchronises the device while the
-    peer's PCG kernel waits on that shard (a same-device-only hazard; with one
-    process per GPU it cannot happen). Any shard error -- an exchange timeout
-    included -- fails the test on the first attempt."""
+def shard_streams(probs):
+    """One stream per shard, its caching-allocator pool warmed in THIS thread.
+
+    With several shards on one device, a device memory allocation (or any
+    NULL-stream command) issued by one shard's thread serialises the device's
+    streams around it (CUDA's implicit synchronisation rules): the shard's
+    next kernels then wait for everything enqueued before, including a peer's
+    kernel that spins in an exchange waiting for them -- a stall until the
+    exchange timeout. The solver itself allocates nothing once its handles are
+    connected (ssfm_comm_connect also builds the graph PCG), so the shard
+    threads must not make torch's allocator call cudaMalloc either: the
+    tensors lm_solve / cost / gradient allocate are allocated and freed here
+    once per stream first (one process per GPU has no such hazard)."""
+    import torch
+    streams = []
+    for p in probs:
+        s = torch.cuda.Stream()
+        n, m = p.layout.total_params, p.layout.total_residuals
+        with torch.cuda.stream(s):
+            keep = [torch.zeros(n, dtype=torch.float64, device="cuda") for _ in range(4)]
+            keep += [torch.zeros(m, dtype=torch.float64, device="cuda"), torch.zeros(1, dtype=torch.float64,
+                                                                                  device="cuda")]
+            keep.append(keep[0].clone())
+            bool(torch.isfinite(keep[-1]).all())
+            keep[-1].cpu()
+            del keep
+        s.synchronize()
+        streams.append(s)
+    return streams
+
+
+def run_shards(work, probs, timeout):
+    """One host thread per same-device shard, each on its own warmed stream
+    (shard_streams). Unreachable handles of earlier tests are destroyed first
+    and the garbage collector is paused meanwhile: a handle destroyed inside a
+    shard's thread frees device memory, which serialises the streams around a
+    peer's waiting kernel. Any shard error -- an exchange timeout included --
+    fails the test on the first attempt."""
     errs = []
+    n = len(probs)
+    gc.collect()
+    streams = shard_streams(probs)
 
     def guarded(r):
         try:
-            work(r)
+            work(r, streams[r])
         except Exception as e:   # noqa: BLE001 - reported below
             errs.append(e)
 
-    gc.collect()
     gc.disable()
     try:
         ts = [threading.Thread(target=guarded, args=(r,)) for r in range(n)]
@@ -124,6 +158,32 @@ def test_local_shards_match_single_gpu(gpu, world, fused, graph):
     assert np.abs(full - th1).max() <= 1e-6 * max(1.0, np.abs(th1).max())
 
 
+@pytest.mark.parametrize("world,fused,graph", [(2, "1", "0"), (2, "0", "1"), (3, "0", "0")])
+def test_local_shards_shared_focal(gpu, world, fused, graph):
+    """One focal shared by every camera (ba.py:49, 61): its Schur row couples
+    every camera, and its point part is summed over every rank's points."""
+    st = scene()
+    cfg = b2.LMConfig(max_iterations=12)
+    os.environ["SSFM_FUSED"] = fused
+    try:
+        single = b2.BAProblem(st, b2.RobustLoss("huber", 1.0), shared_focal=True)
+        single._native_handle()
+    finally:
+        os.environ.pop("SSFM_FUSED")
+    th1, rep1 = b2.lm_solve(single, single.encode(), cfg)
+    probs, out = solve_local_shards(gpu, st, world, cfg, fused, graph, shared_focal=True)
+    reps = [o[1] for o in out]
+    for rep in reps[1:]:
+        assert [(i.cost_after, i.cg_iters, i.lam) for i in rep.iterations] == \
+               [(i.cost_after, i.cg_iters, i.lam) for i in reps[0].iterations]
+    assert [i.step_accepted for i in reps[0].iterations] == [i.step_accepted for i in rep1.iterations]
+    dev = max(abs(a.cost_after - b.cost_after) / b.cost_after for a, b in zip(reps[0].iterations, rep1.iterations))
+    assert dev < 1e-7
+    full = probs[0].gather_theta(out[0][0], shards=[(p, o[0]) for p, o in zip(probs, out)])
+    assert full.shape == th1.shape
+    assert np.abs(full - th1).max() <= 1e-6 * max(1.0, np.abs(th1).max())
+
+
 def test_sharded_cost_and_gradient_are_global(gpu):
     st = scene(cams=12, pts=400, k=4, seed=3)
     single = b2.BAProblem(st, b2.RobustLoss("huber", 1.0))
@@ -138,12 +198,12 @@ def test_sharded_cost_and_gradient_are_global(gpu):
         os.environ.pop("SSFM_PCG_SMS")
     res = [None, None]
 
-    def work(r):
-        with gpu.cuda.stream(gpu.cuda.Stream()):
+    def work(r, stream):
+        with gpu.cuda.stream(stream):
             p = probs[r]
             res[r] = (p.cost(p.encode()), p.gradient(p.encode()))
 
-    run_shards(work, 2, 120)
+    run_shards(work, probs, 120)
     assert res[0][0] == res[1][0] == pytest.approx(c1, rel=1e-13)
     C = st.num_cameras
     # camera part of the gradient is the global one on every rank; point parts are local
@@ -193,11 +253,11 @@ def test_local_gp_shards_match_single_gpu(gpu, fused):
         os.environ.pop("SSFM_FUSED")
     out = [None, None]
 
-    def work(r):
-        with gpu.cuda.stream(gpu.cuda.Stream()):
+    def work(r, stream):
+        with gpu.cuda.stream(stream):
             out[r] = b2.lm_solve(probs[r], probs[r].initial_theta(), cfg)
 
-    run_shards(work, 2, 300)
+    run_shards(work, probs, 300)
     ra, rb = out[0][1], out[1][1]
     assert [(i.cost_after, i.cg_iters) for i in ra.iterations] == [(i.cost_after, i.cg_iters) for i in rb.iterations]
     assert [i.step_accepted for i in ra.iterations] == [i.step_accepted for i in rep1.iterations]

@@ -73,6 +73,29 @@ def test_device_loop_matches_host_loop(gpu, name, driver):
     assert all(i.device_ms > 0 for i in rep_d.iterations)
 
 
+GP_DRIVERS = {"persistent": {"SSFM_GP_GRAPH": "0"}, "graph": {"SSFM_GP_GRAPH": "1"},
+              "graph_four_kernels": {"SSFM_GP_GRAPH": "1", "SSFM_GVEC": "0"}}
+
+
+@pytest.mark.parametrize("name", ["gp_small.npz", "gp_depth.npz"])
+@pytest.mark.parametrize("driver", sorted(GP_DRIVERS))
+def test_gp_device_loop_matches_host_loop(gpu, name, driver):
+    from .test_gpu_gp import gp_from_golden
+    z = golden(name)
+    with env(GP_DRIVERS[driver]):   # SSFM_GVEC is read when the graphs are captured (first solve)
+        p = gp_from_golden(z)
+        p._native_handle()
+        th0 = p.initial_theta()
+        cfg = b2.LMConfig(max_iterations=25)
+        with env({"SSFM_LM_GRAPH": "0"}):
+            th_h, rep_h = b2.lm_solve(p, th0, cfg)
+        th_d, rep_d = b2.lm_solve(p, th0, cfg)
+    assert mode(p) == 1, "the LM graph did not build"
+    assert rep_d.termination == rep_h.termination
+    assert trajectory(rep_d) == trajectory(rep_h)
+    assert np.array_equal(th_d, th_h)
+
+
 def test_device_loop_max_iterations_and_grad_termination(gpu):
     p = problem_from_golden(golden("ba_small.npz"))
     th0 = p.encode()
