@@ -217,7 +217,7 @@ def run_pipeline(args):
         b2.run_global_sfm(obs)
     sampler = ClockSampler(0)
     sampler.start()
-    time.sleep(0.3)
+    time.sleep(1.0)   # nvidia-smi starts up before the timed region
     stream = torch.cuda.current_stream()
     times, gp_its, ba_its, rms, lm_ms = [], 0, 0, None, 0.0
     for _ in range(max(1, args.steps // 10)):
@@ -316,7 +316,7 @@ def run_b200(args, ws, rank, local):
     log(f"[rank {rank}] warmup {len(rep_w.iterations)} its {time.time() - t_setup:.1f}s, lambda -> {lam:g}")
     sampler = ClockSampler(local)
     sampler.start()
-    time.sleep(0.3)
+    time.sleep(1.0)   # nvidia-smi starts up before the timed region
     stream = torch.cuda.current_stream()
     # exactly K timed LM iterations: continue the warm-up trajectory; if a
     # solve converges early, the next one restarts from theta0 (same workload)

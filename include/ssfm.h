@@ -200,6 +200,15 @@ int ssfm_lm_solve(ssfm_handle* h, double* theta, const ssfm_lm_config* cfg,
                   ssfm_iter_record* recs, int32_t cap, int32_t* n_recs,
                   int32_t* termination, void* stream);
 
+/* ba.prune (ba.py:223-261) on the device: points seen by fewer than two
+ * cameras and cameras left without observations are dropped to a fixed point.
+ * cam_idx / pt_idx [n] int32, camera_map [C] / point_map [P] int32 (old ->
+ * new, -1 removed), obs_mask [n] uint8: device arrays. *n_cam_out, *n_pt_out,
+ * *n_obs_out: survivors. SSFM_EMPTY_PROBLEM when nothing survives. */
+int ssfm_prune(int64_t n, const int32_t* cam_idx, const int32_t* pt_idx, int32_t C, int32_t P,
+               int32_t* camera_map, int32_t* point_map, uint8_t* obs_mask, int32_t* n_cam_out,
+               int32_t* n_pt_out, int64_t* n_obs_out, void* stream);
+
 /* How lm_solve runs its loop on this handle: 1 = the whole LM loop as one
  * CUDA graph (accept/reject, lambda and termination decided on the device,
  * one read-back per solve; single-rank BA handles, SSFM_LM_GRAPH=0 disables),
@@ -340,10 +349,11 @@ int ssfm_schur_solve(const ssfm_schur_plan* plan, const double* data, const doub
  * point-major copy, after ssfm_linearize. Expected 0. */
 int ssfm_check_jacobian(ssfm_handle* h, int64_t* mismatches, void* stream);
 
-/* Diagnostic (BA): mean time (ms) of one standalone launch of a pass of the
- * two-pass Schur operator over the current linearization, reps launches after
- * warm-up. which: 0 = point pass (Jpm, p gather -> y), 1 = camera pass (Jcm,
- * y gather -> tile sums), 2 = both back to back. Call after ssfm_solve_normal. */
+/* Diagnostic (BA and GP): mean time (ms) of one standalone launch of a pass
+ * of the two-pass Schur operator over the current linearization, reps
+ * launches after warm-up. which: 0 = point pass (point-major records, camera
+ * vector gather -> y), 1 = camera pass (camera-major records, y gather ->
+ * tile sums), 2 = both back to back. Call after ssfm_solve_normal. */
 int ssfm_bench_operator(ssfm_handle* h, int32_t which, int32_t reps, double* ms_out, void* stream);
 
 /* Which Schur operator the PCG kernel of this handle runs (no reference

@@ -28,7 +28,7 @@ EXPORTS = (
     "ssfm_rotation_auc", "ssfm_center_moments", "ssfm_apply_sim3",
     "ssfm_bal_read", "ssfm_bal_take", "ssfm_bal_free", "ssfm_make_rays", "ssfm_schur_solve",
     "ssfm_trim_cache", "ssfm_cache_bytes", "ssfm_arena_create", "ssfm_arena_destroy", "ssfm_arena_info",
-    "ssfm_create_ba_in", "ssfm_create_gp_in", "ssfm_lm_mode",
+    "ssfm_create_ba_in", "ssfm_create_gp_in", "ssfm_lm_mode", "ssfm_prune",
 )
 
 TERMINATIONS = {0: "max_iter", 1: "converged_cost", 2: "converged_grad", 3: "solver_failure"}
@@ -109,6 +109,7 @@ def load(required: bool = True):
     lib.ssfm_version.restype = ct.c_char_p
     lib.ssfm_lm_mode.argtypes = [P]
     lib.ssfm_lm_mode.restype = I32
+    lib.ssfm_prune.argtypes = [I64, P, P, I32, I32, P, P, P, ct.POINTER(I32), ct.POINTER(I32), ct.POINTER(I64), P]
     lib.ssfm_create_ba.argtypes = [ct.POINTER(BADescC), P, ct.POINTER(P)]
     lib.ssfm_create_gp.argtypes = [ct.POINTER(GPDescC), P, ct.POINTER(P)]
     lib.ssfm_destroy.argtypes = [P]

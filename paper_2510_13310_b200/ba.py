@@ -45,6 +45,10 @@ class _DeviceProblem:
     def _create(self, arena=None):  # pragma: no cover - abstract
         raise NotImplementedError
 
+    def _enter_collective(self):
+        """Hook before each native call (sharded problems synchronise their
+        local shards here, dist._Sharded._enter_collective)."""
+
     def _native_handle(self, workspace=None):
         """The device problem, created on first use; with a Workspace (lm_solve,
         run_ba / run_gp) it is created in the workspace's device arena."""
@@ -85,6 +89,7 @@ class _DeviceProblem:
         from .lm import _stream
         t = self._theta_dev(torch, theta)
         out = ct.c_double(0.0)
+        self._enter_collective()
         _native.check(_native.load().ssfm_cost(ct.c_void_p(self._native_handle().ptr),
                                                ct.c_void_p(t.data_ptr()), ct.byref(out),
                                                _stream(torch)))
@@ -99,6 +104,7 @@ class _DeviceProblem:
         J = torch.empty(self.jac_width * self.num_obs if want_J else 1, dtype=torch.float64, device="cuda")
         g = torch.empty(self.layout.total_params, dtype=torch.float64, device="cuda")
         gmax = ct.c_double(0.0)
+        self._enter_collective()
         _native.check(_native.load().ssfm_linearize(
             ct.c_void_p(h.ptr), ct.c_void_p(t.data_ptr()), ct.c_void_p(r.data_ptr()),
             ct.c_void_p(J.data_ptr()) if want_J else None, ct.c_void_p(g.data_ptr()),
@@ -123,6 +129,7 @@ class _DeviceProblem:
         from .lm import _stream
         is_t = isinstance(theta, torch.Tensor)
         t = self._theta_dev(torch, theta).clone()
+        self._enter_collective()
         _native.check(_native.load().ssfm_post_step(ct.c_void_p(self._native_handle().ptr),
                                                     ct.c_void_p(t.data_ptr()), _stream(torch)))
         return t if is_t else t.cpu().numpy()
@@ -293,13 +300,48 @@ class PruneRemap:
     observation_mask: np.ndarray
 
 
+def _prune_device(cam, pt, c, p):
+    """(camera_map, point_map, observation mask) from ssfm_prune (the fixed
+    point of ba.py:234-243 on the device, bit-identical); None without a GPU."""
+    try:
+        import torch
+    except ImportError:   # pragma: no cover
+        return None
+    if not torch.cuda.is_available() or _native.load(required=False) is None:
+        return None
+    from .lm import _stream
+    n = len(cam)
+    cam_d = torch.as_tensor(cam.astype(np.int32)).cuda()
+    pt_d = torch.as_tensor(pt.astype(np.int32)).cuda()
+    cmap = torch.empty(max(c, 1), dtype=torch.int32, device="cuda")
+    pmap = torch.empty(max(p, 1), dtype=torch.int32, device="cuda")
+    mask = torch.empty(max(n, 1), dtype=torch.uint8, device="cuda")
+    nc, npt, no = ct.c_int32(0), ct.c_int32(0), ct.c_int64(0)
+    _native.check(_native.load().ssfm_prune(n, ct.c_void_p(cam_d.data_ptr()), ct.c_void_p(pt_d.data_ptr()), c, p,
+                                            ct.c_void_p(cmap.data_ptr()), ct.c_void_p(pmap.data_ptr()),
+                                            ct.c_void_p(mask.data_ptr()), ct.byref(nc), ct.byref(npt),
+                                            ct.byref(no), _stream(torch)))
+    return (cmap[:c].cpu().numpy().astype(np.int64), pmap[:p].cpu().numpy().astype(np.int64),
+            mask[:n].cpu().numpy().astype(bool))
+
+
 def prune(scene):
     """Drop points seen by < 2 cameras and cameras left without observations,
-    to a fixed point (ba.py:223-261). Host index preprocessing (not per
-    iteration)."""
+    to a fixed point (ba.py:223-261). On the device (ssfm_prune) when a GPU is
+    present; the host restatement below serves CPU-only use."""
     arr = as_arrays(scene)
     c, p = arr.num_cameras, arr.num_points
     cam, pt = arr.cam_idx.astype(np.int64), arr.pt_idx.astype(np.int64)
+    dev = _prune_device(cam, pt, c, p)
+    if dev is not None:
+        cmap, pmap, obs_ok = dev
+        cam_ok, pt_ok = cmap >= 0, pmap >= 0
+    else:
+        cmap, pmap, obs_ok, cam_ok, pt_ok = _prune_host(cam, pt, c, p)
+    return _prune_apply(scene, arr, cmap, pmap, obs_ok, cam_ok, pt_ok)
+
+
+def _prune_host(cam, pt, c, p):
     cam_ok = np.ones(c, dtype=bool)
     pt_ok = np.ones(p, dtype=bool)
     while True:
@@ -316,6 +358,12 @@ def prune(scene):
     cmap[cam_ok] = np.arange(int(cam_ok.sum()))
     pmap = np.full(p, -1, dtype=np.int64)
     pmap[pt_ok] = np.arange(int(pt_ok.sum()))
+    return cmap, pmap, obs_ok, cam_ok, pt_ok
+
+
+def _prune_apply(scene, arr, cmap, pmap, obs_ok, cam_ok, pt_ok):
+    cam, pt = arr.cam_idx.astype(np.int64), arr.pt_idx.astype(np.int64)
+    c, p = arr.num_cameras, arr.num_points
     out = SceneArrays(arr.quats[cam_ok], arr.centers[cam_ok], arr.focals[cam_ok], arr.pps[cam_ok],
                       arr.dists[cam_ok], arr.model_tag, arr.points[pt_ok], cmap[cam[obs_ok]],
                       pmap[pt[obs_ok]], arr.pixels[obs_ok],

@@ -27,7 +27,6 @@ struct BADev {
   double* Xl;             // [4P] points at the linearization (omega-form, padded: 32-byte gathers)
   double* Wc;             // [8C] per-camera omega-form vector of the current p / x (ba_wvec)
   double* Rpm;            // [4N] point-major weighted residual [r0, r1, 0, 0] (ba_k_lin_tile; full sectors)
-  double* Kcm;            // [8N] camera-major [Jp Cinv Jp^T (3), Jp y0 (2), 0 x3] per damped solve (ba_k_kobs)
   double* Jcm;            // [16 * Npad]
   double* Fcm;            // [9 * Npad] factored records (ba_factor) + v = X - t, camera-major (two-pass only)
   BACam* camlin;          // [C] camera cache at the linearization (cams is overwritten by trial costs)
@@ -69,6 +68,75 @@ __device__ __forceinline__ void gpm_store(const BADev& d, long long i, const dou
   for (int k = 0; k < 8; ++k) d.Gpm[k * d.Npad + i] = jp8[k];
 #endif
 }
+// Factored camera-major record Fcm of observation i (ba_factor + v = X - t).
+// FCM_AOS=1: one record per observation, pinhole 64 bytes [s00, e0, e1, phi,
+// v0, v1, v2, 0], bal 96 bytes [s00, e0, e1, phi, s01, s11, v0, v1, v2, 0 x3]
+// (2 / 3 vector loads instead of 7 / 9 scalar ones); 0: SoA rows [9][Npad].
+#ifndef FCM_AOS
+#define FCM_AOS 1
+#endif
+__host__ __device__ __forceinline__ long long fcm_doubles(int model, long long Npad) {
+#if FCM_AOS
+  return (model == 1 ? 12ll : 8ll) * Npad;
+#else
+  (void)model;
+  return 9ll * Npad;
+#endif
+}
+// F[0..5] = s00, e0, e1, phi, s01, s11 (ba_factor), F[6..8] = v
+__device__ __forceinline__ void fcm_store(const BADev& d, long long i, const double* F, unsigned long long pol) {
+#if FCM_AOS
+  (void)pol;
+  if (d.bp.model == 1) {
+    double* r = d.Fcm + 12 * i;
+    *reinterpret_cast<double4*>(r) = make_double4(F[0], F[1], F[2], F[3]);
+    *reinterpret_cast<double4*>(r + 4) = make_double4(F[4], F[5], F[6], F[7]);
+    *reinterpret_cast<double4*>(r + 8) = make_double4(F[8], 0.0, 0.0, 0.0);
+  } else {
+    double* r = d.Fcm + 8 * i;
+    *reinterpret_cast<double4*>(r) = make_double4(F[0], F[1], F[2], F[3]);
+    *reinterpret_cast<double4*>(r + 4) = make_double4(F[6], F[7], F[8], 0.0);
+  }
+#else
+  const long long Np = d.Npad;
+#pragma unroll
+  for (int k = 0; k < 9; ++k)
+    if (d.bp.model == 1 || k < 4 || k > 5) st_hint(d.Fcm + k * Np + i, F[k], pol);
+#endif
+}
+// f[0..5] = s00, e0, e1, phi, s01, s11 (pinhole: s01 = 0, s11 = s00), vv = v
+__device__ __forceinline__ void fcm_load(const BADev& d, long long i, double* f, double* vv, unsigned long long pol) {
+#if FCM_AOS
+  if (d.bp.model == 1) {
+    double a[4], b[4], c[4];
+    ld_v4_ro(d.Fcm + 12 * i, a, pol);
+    ld_v4_ro(d.Fcm + 12 * i + 4, b, pol);
+    ld_v4_ro(d.Fcm + 12 * i + 8, c, pol);
+    f[0] = a[0]; f[1] = a[1]; f[2] = a[2]; f[3] = a[3]; f[4] = b[0]; f[5] = b[1];
+    vv[0] = b[2]; vv[1] = b[3]; vv[2] = c[0];
+  } else {
+    double a[4], b[4];
+    ld_v4_ro(d.Fcm + 8 * i, a, pol);
+    ld_v4_ro(d.Fcm + 8 * i + 4, b, pol);
+    f[0] = a[0]; f[1] = a[1]; f[2] = a[2]; f[3] = a[3]; f[4] = 0.0; f[5] = a[0];
+    vv[0] = b[0]; vv[1] = b[1]; vv[2] = b[2];
+  }
+#else
+  const long long Np = d.Npad;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) f[k] = ldg_stream(d.Fcm + k * Np + i, pol);
+  if (d.bp.model == 1) {
+    f[4] = ldg_stream(d.Fcm + 4 * Np + i, pol);
+    f[5] = ldg_stream(d.Fcm + 5 * Np + i, pol);
+  } else {
+    f[4] = 0.0;
+    f[5] = f[0];
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) vv[k] = ldg_stream(d.Fcm + (6 + k) * Np + i, pol);
+#endif
+}
+
 __device__ __forceinline__ void gpm_load(const BADev& d, long long i, double* G, unsigned long long pol) {
 #if GPM_AOS
   ld_v4_ro(d.Gpm + 8 * i, G, pol);
@@ -322,10 +390,7 @@ __global__ void __launch_bounds__(SSFM_TILE) ba_k_linearize_cm(BADev d, const do
 #pragma unroll
       for (int k = 0; k < BA_JREC; ++k) d.Jcm[k * Np + i] = J[k];
     }
-    if (d.Fcm) {
-#pragma unroll
-      for (int k = 0; k < BA_FREC + 3; ++k) d.Fcm[k * Np + i] = F[k];
-    }
+    if (d.Fcm) fcm_store(d, i, F, pol_evict_first());
     double a[8], b[8];
     ba_jc_row(J, 0, a);
     ba_jc_row(J, 1, b);
@@ -358,6 +423,10 @@ __global__ void __launch_bounds__(SSFM_TILE) ba_k_linearize_cm(BADev d, const do
 //    Jp^T Jf) summed per point in observation order from Gpm / Rpm, as
 //    ba_k_linearize does (the same values: the records are bit-identical).
 // ---------------------------------------------------------------------------
+#ifndef LIN_FRAME
+#define LIN_FRAME 0   // camera-frame accumulation of the tile's J^T J (no full Jacobian per observation)
+#endif
+__device__ __forceinline__ double ba_precond_f_entry(const double* cb, const double* w, int o);
 __global__ void __launch_bounds__(SSFM_TILE) ba_k_lin_tile(BADev d, const double* __restrict__ theta) {
   __shared__ double sm[(SSFM_TILE / 32) * CAM_V];
   const int t = blockIdx.x;
@@ -369,24 +438,49 @@ __global__ void __launch_bounds__(SSFM_TILE) ba_k_lin_tile(BADev d, const double
   for (int k = 0; k < CAM_V; ++k) v[k] = 0.0;
   if (i < o1) {
     const unsigned long long pst = pol_evict_first();
-    const long long Np = d.Npad;
     const int j = d.topo.cm_pt[i];
     const int ip = d.topo.cm_to_pm[i];
+#if LIN_FRAME
+    // residual and factored record only; Jp = S E R, Jf = phi e; the tile's
+    // J^T J / J^T r accumulate the camera-frame rows
+    // a~_r = [D(v)^T (SE)_r ; -(SE)_r ; phi e_r] and are mapped once per tile
+    // through T = diag(Pi, R^T, 1) (as ba_k_precond does)
+    const BACam cc = d.cams[c];
+    BAProj pr;
+    double r[2], sw, ct, F[BA_FREC + 3];
+    ba_residual(d.bp, cc, theta + d.bp.off_pts + 3ll * j, d.pix_cm + 2ll * i, pr, r, sw, ct);
+    ba_factor(d.bp, cc, pr, sw, F);
+    F[6] = pr.v[0]; F[7] = pr.v[1]; F[8] = pr.v[2];
+    fcm_store(d, i, F, pst);
+    const double f4 = d.bp.model == 1 ? F[4] : 0.0, f5 = d.bp.model == 1 ? F[5] : F[0];
+    const double se[2][3] = {{F[0], f4, -(F[0] * F[1] + f4 * F[2])}, {f4, f5, -(f4 * F[1] + f5 * F[2])}};
+    double g8[8];
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        g8[3 * rr + k] = se[rr][0] * cc.R[k] + se[rr][1] * cc.R[3 + k] + se[rr][2] * cc.R[6 + k];
+    g8[6] = F[3] * F[1];
+    g8[7] = F[3] * F[2];
+    gpm_store(d, ip, g8);
+    *reinterpret_cast<double4*>(d.Rpm + 4ll * ip) = make_double4(r[0], r[1], 0.0, 0.0);
+    double a[8], b[8];
+    ba_dqt_mul(cc.qh, pr.v, se[0], a);
+    ba_dqt_mul(cc.qh, pr.v, se[1], b);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) { a[4 + k] = -se[0][k]; b[4 + k] = -se[1][k]; }
+    a[7] = g8[6];
+    b[7] = g8[7];
+#else
     double r[2], J[BA_JREC], ct, F[BA_FREC + 3];
     ba_obs_eval(d.bp, d.cams + c, theta + d.bp.off_pts + 3ll * j, d.pix_cm + 2ll * i, r, J, &ct, F);
-    if (d.bp.model == 1) {
-#pragma unroll
-      for (int k = 0; k < BA_FREC + 3; ++k) st_hint(d.Fcm + k * Np + i, F[k], pst);
-    } else {   // pinhole: rows 4-5 (s01, s11) are implied
-#pragma unroll
-      for (int k = 0; k < BA_FREC + 3; ++k)
-        if (k < 4 || k > 5) st_hint(d.Fcm + k * Np + i, F[k], pst);
-    }
+    fcm_store(d, i, F, pst);   // pinhole: s01, s11 are implied
     gpm_store(d, ip, J + 8);
     *reinterpret_cast<double4*>(d.Rpm + 4ll * ip) = make_double4(r[0], r[1], 0.0, 0.0);
     double a[8], b[8];
     ba_jc_row(J, 0, a);
     ba_jc_row(J, 1, b);
+#endif
     int idx = 0;
 #pragma unroll
     for (int p = 0; p < 8; ++p)
@@ -396,11 +490,25 @@ __global__ void __launch_bounds__(SSFM_TILE) ba_k_lin_tile(BADev d, const double
     for (int p = 0; p < 8; ++p) v[36 + p] = a[p] * r[0] + b[p] * r[1];
   }
   block_reduce<CAM_V>(v, sm);
+#if LIN_FRAME
+  __shared__ double smw[CAM_V];
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < CAM_V; ++k) smw[k] = v[k];
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const double* cb = reinterpret_cast<const double*>(d.camlin + c);
+    double* dst = d.tilebuf + (long long)CAM_V * t;
+    for (int o = threadIdx.x; o < CAM_V; o += 32) dst[o] = ba_precond_f_entry(cb, smw, o);
+  }
+#else
   if (threadIdx.x == 0) {
     double* dst = d.tilebuf + (long long)CAM_V * t;
 #pragma unroll
     for (int k = 0; k < CAM_V; ++k) dst[k] = v[k];
   }
+#endif
 }
 
 __global__ void __launch_bounds__(256) ba_k_lin_points(BADev d, const double* __restrict__ theta,
@@ -647,27 +755,16 @@ __device__ __forceinline__ void ba_precond_f(const BADev& d, int t, double* v) {
   const int o0 = d.topo.tile_obs[t], o1 = d.topo.tile_obs[t + 1];
   const int i = o0 + threadIdx.x;
   if (i >= o1) return;
-  const long long Np = d.Npad;
   const double* cb = reinterpret_cast<const double*>(d.camlin + d.topo.tile_cam[t]);
   double f[6], vv[3];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) f[k] = d.Fcm[k * Np + i];
-  if (d.bp.model == 1) { f[4] = d.Fcm[4 * Np + i]; f[5] = d.Fcm[5 * Np + i]; }
-  else { f[4] = 0.0; f[5] = f[0]; }
-#pragma unroll
-  for (int k = 0; k < 3; ++k) vv[k] = d.Fcm[(6 + k) * Np + i];
+  fcm_load(d, i, f, vv, pol_evict_first());
   double qh[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) qh[k] = cb[9 + k];
   const double se[2][3] = {{f[0], f[4], -(f[0] * f[1] + f[4] * f[2])},
                            {f[4], f[5], -(f[4] * f[1] + f[5] * f[2])}};
   double k00, k01, k11, ty0, ty1;
-  if (d.Kcm) {   // per-observation point terms from ba_k_kobs (coalesced, no per-point gathers)
-    double K[8];
-    ld_v4_ro(d.Kcm + 8ll * i, K, pol_evict_first());
-    ld_v4_ro(d.Kcm + 8ll * i + 4, K + 4, pol_evict_first());
-    k00 = K[0]; k01 = K[1]; k11 = K[2]; ty0 = K[3]; ty1 = K[4];
-  } else {
+  {
     const int j = d.topo.cm_pt[i];
     double ci[6], y[3];
 #pragma unroll
@@ -707,35 +804,6 @@ __device__ __forceinline__ void ba_precond_f(const BADev& d, int t, double* v) {
   for (int p = 0; p < 8; ++p) v[36 + p] = a[p] * ty0 + b[p] * ty1;
 }
 
-// Point terms of the preconditioner per observation (omega-form handles):
-// K_o = Jp_o Cinv_j Jp_o^T and Jp_o y0_j from the point-major record, stored
-// as a whole 64-byte record at the observation's camera-major position, so
-// ba_k_precond streams them instead of gathering Cinv_j and y0_j per
-// observation (the gathers missed L2: 6.3 GB of DRAM per C5 launch).
-__global__ void ba_k_kobs(BADev d) {
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= d.topo.N) return;
-  const unsigned long long pst = pol_evict_first();
-  double G[8];
-  gpm_load(d, i, G, pst);
-  const int j = d.topo.pm_pt[i];
-  double ci[6], y[3];
-#pragma unroll
-  for (int k = 0; k < 6; ++k) ci[k] = __ldg(d.Cinv + 6ll * j + k);
-#pragma unroll
-  for (int k = 0; k < 3; ++k) y[k] = __ldg(d.y0 + 3ll * j + k);
-  double w0[3], w1[3];
-  sym3_matvec(ci, G, w0);
-  sym3_matvec(ci, G + 3, w1);
-  const double k00 = G[0] * w0[0] + G[1] * w0[1] + G[2] * w0[2];
-  const double k01 = G[3] * w0[0] + G[4] * w0[1] + G[5] * w0[2];
-  const double k11 = G[3] * w1[0] + G[4] * w1[1] + G[5] * w1[2];
-  const double ty0 = G[0] * y[0] + G[1] * y[1] + G[2] * y[2];
-  const double ty1 = G[3] * y[0] + G[4] * y[1] + G[5] * y[2];
-  double* dst = d.Kcm + 8ll * d.topo.pm_to_cm[i];
-  *reinterpret_cast<double4*>(dst) = make_double4(k00, k01, k11, ty0);
-  *reinterpret_cast<double4*>(dst + 4) = make_double4(ty1, 0.0, 0.0, 0.0);
-}
 
 // W = T W~ T^T, u = T u~ for the tile's camera, T = diag(Pi, R^T, 1): one
 // output entry per lane of warp 0 (packed upper 36 + 8), from W~ in shared

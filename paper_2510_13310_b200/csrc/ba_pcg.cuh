@@ -65,18 +65,6 @@ __device__ __forceinline__ double cta_partials_sum(const double* part, int n, in
 // rounding. (A factored point pass lost, 0.555 -> 0.832 ms: every observation
 // gathers its camera's R, qh, t through L1, which saturates at 89 %; the
 // point pass keeps the Jacobian record.)
-__device__ __forceinline__ void ba_load_frec(const double* __restrict__ F, long long Np, long long i, int model,
-                                             unsigned long long pol, double* f) {
-#pragma unroll
-  for (int k = 0; k < 4; ++k) f[k] = ldg_stream(F + k * Np + i, pol);
-  if (model == 1) {
-    f[4] = ldg_stream(F + 4 * Np + i, pol);
-    f[5] = ldg_stream(F + 5 * Np + i, pol);
-  } else {
-    f[4] = 0.0;
-    f[5] = f[0];
-  }
-}
 
 #ifndef CAMF_MINB
 #define CAMF_MINB 2      // CTAs per SM of the factored camera pass
@@ -85,43 +73,19 @@ __device__ __forceinline__ void ba_load_frec(const double* __restrict__ F, long 
 #define CAMF_UNROLL 2
 #endif
 constexpr int kCamfUnroll = CAMF_UNROLL;
-#ifndef CAMF_PF
-#define CAMF_PF 0        // L2 bulk prefetch of the next tile's records
-#endif
 #ifndef CAMF_HOIST
 #define CAMF_HOIST 1     // keep the tile camera's R, qh in registers across the loop
 #endif
 template <bool RO>
 __device__ __forceinline__ void ba_camera_pass_f(const BADev& d, const double* y, double* tile8) {
   const unsigned long long pstream = pol_evict_first(), pkeep = pol_evict_last();
-  const long long Np = d.Npad;
-  const int model = d.bp.model;
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-#if CAMF_PF
-  // the next tile's bounds are loaded one tile ahead, and its record rows are
-  // prefetched into L2 (one bulk request per row) while this tile runs
-  int nx0 = 0, nx1 = 0;
-  if (gw + warps < d.topo.nt) { nx0 = __ldg(d.topo.tile_obs + gw + warps); nx1 = __ldg(d.topo.tile_obs + gw + warps + 1); }
-#endif
   for (int t = gw; t < d.topo.nt; t += warps) {
     const int o0 = __ldg(d.topo.tile_obs + t), o1 = __ldg(d.topo.tile_obs + t + 1);
     const int c = __ldg(d.topo.tile_cam + t);
     const double* cb = reinterpret_cast<const double*>(d.camlin + c);
-#if CAMF_PF
-    if (t + warps < d.topo.nt) {
-      const int nrow = model == 1 ? 9 : 7;
-      if (lane < nrow) {
-        const int row = (model == 1 || lane < 4) ? lane : lane + 2;   // pinhole: rows 0-3, 6-8
-        pf_l2_bulk(d.Fcm + row * Np + nx0, 8ll * (nx1 - nx0));
-      } else if (lane == 16) {
-        pf_l2_bulk(d.topo.cm_pt + nx0, 4ll * (nx1 - nx0));
-      }
-      const int tn = t + 2 * warps;
-      if (tn < d.topo.nt) { nx0 = __ldg(d.topo.tile_obs + tn); nx1 = __ldg(d.topo.tile_obs + tn + 1); }
-    }
-#endif
     double o[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) o[k] = 0.0;
@@ -144,9 +108,7 @@ __device__ __forceinline__ void ba_camera_pass_f(const BADev& d, const double* y
       for (int k = 0; k < 4; ++k) qh[k] = __ldg(cb + 9 + k);
 #endif
       double f[6], vv[3];
-      ba_load_frec(d.Fcm, Np, i, model, pstream, f);
-#pragma unroll
-      for (int k = 0; k < 3; ++k) vv[k] = ldg_stream(d.Fcm + (6 + k) * Np + i, pstream);
+      fcm_load(d, i, f, vv, pstream);
       const int j = ldg_stream_i(d.topo.cm_pt + i, pstream);
       double yj[4];
       if constexpr (RO) ld_v4_ro(y + 4ll * j, yj, pkeep);
@@ -289,7 +251,7 @@ __device__ __forceinline__ void ba_point_pass(const BADev& d, const double* v, d
 }
 
 #ifndef PTW_CIEARLY
-#define PTW_CIEARLY 0
+#define PTW_CIEARLY 1   // owners load Cinv at the batch start (C5 point pass 0.46 -> 0.45 ms)
 #endif
 // P1 in the omega form (ba_wobs): W = the per-camera vector of p (ba_wvec).
 // Streams the 64-byte Jp + Jf record and the camera and point indices per

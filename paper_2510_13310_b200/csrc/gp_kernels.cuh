@@ -67,6 +67,33 @@ struct GPDev {
   const double* lamp;     // device-resident lambda (LM loop as a CUDA graph) or nullptr: lam / the argument
 };
 
+// GP observation record {a, g0, g1, g2} in the point- or camera-major array:
+// GP_AOS=1 one 32-byte record per observation (one vector load), 0: SoA rows.
+#ifndef GP_AOS
+#define GP_AOS 1
+#endif
+__device__ __forceinline__ void gp_rec_st(double* base, long long Np, long long i, const double* rec) {
+#if GP_AOS
+  (void)Np;
+  *reinterpret_cast<double4*>(base + 4 * i) = make_double4(rec[0], rec[1], rec[2], rec[3]);
+#else
+#pragma unroll
+  for (int k = 0; k < 4; ++k) base[k * Np + i] = rec[k];
+#endif
+}
+// STREAM: L2 evict_first, no L1 allocation (the PCG passes)
+template <bool STREAM>
+__device__ __forceinline__ void gp_rec_ld(const double* base, long long Np, long long i, double* rec) {
+#if GP_AOS
+  (void)Np;
+  if constexpr (STREAM) ld_v4_ro(base + 4 * i, rec, pol_evict_first());
+  else ld_v4(base + 4 * i, rec);
+#else
+#pragma unroll
+  for (int k = 0; k < 4; ++k) rec[k] = __ldg(base + k * Np + i);
+#endif
+}
+
 __device__ __forceinline__ double gp_at(const GPDev& g, int cam, double a) {
   return (g.gp.gauge_fixed && cam == 0) ? 0.0 : a;
 }
@@ -162,8 +189,7 @@ __global__ void __launch_bounds__(256) gp_k_linearize(GPDev g, const double* __r
         gp_record(g, c, span, blk, d, s, rec, r, bo);
         const double a = rec[0];
         const double at = gp_at(g, c, a);
-#pragma unroll
-        for (int k = 0; k < GP_JREC; ++k) g.Jpm[k * Np + i] = rec[k];
+        gp_rec_st(g.Jpm, Np, i, rec);
         g.bo_pm[i] = bo;
         const int o = g.topo.pm_obs[i];
         if (!g.gp.depth_mode) {
@@ -241,8 +267,7 @@ __global__ void __launch_bounds__(SSFM_TILE) gp_k_linearize_cm(GPDev g, const do
                    g.gp.depth_mode ? g.dep_cm[i] : 0.0, theta, span, blk, d, s);
     double rec[4], r[3], bo;
     gp_record(g, c, span, blk, d, s, rec, r, bo);
-#pragma unroll
-    for (int k = 0; k < GP_JREC; ++k) g.Jcm[k * Np + i] = rec[k];
+    gp_rec_st(g.Jcm, Np, i, rec);
 #pragma unroll
     for (int k = 0; k < 3; ++k) g.rcm[k * Np + i] = r[k];
     g.bo_cm[i] = bo;
@@ -323,8 +348,7 @@ __global__ void __launch_bounds__(256) gp_k_pt_elim(GPDev g, double lam) {
       for (int k = 0; k < 9; ++k) val[k] = 0.0;
       if (i < ob1) {
         double rec[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) rec[k] = g.Jpm[k * Np + i];
+        gp_rec_ld<false>(g.Jpm, Np, i, rec);
         const double inv = gp_inv(lam, rec);
         const double a = rec[0], bo = g.bo_pm[i];
         const double f = inv * a * a;
@@ -399,8 +423,7 @@ __global__ void __launch_bounds__(SSFM_TILE) gp_k_cam_elim(GPDev g, double lam) 
   if (i < o1) {
     const long long Np = g.Npad;
     double rec[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) rec[k] = g.Jcm[k * Np + i];
+    gp_rec_ld<false>(g.Jcm, Np, i, rec);
     const double a = rec[0], at = gp_at(g, c, a);
     const double inv = gp_inv(lam, rec);
     const double* gg = rec + 1;
@@ -524,8 +547,7 @@ __device__ __forceinline__ void gp_point_pass(const GPDev& g, const double* v, d
       double val[3] = {0.0, 0.0, 0.0};
       if (i < ob1) {
         double rec[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) rec[k] = __ldg(g.Jpm + k * Np + i);
+        gp_rec_ld<true>(g.Jpm, Np, i, rec);
         const int c = __ldg(g.topo.pm_cam + i);
         const double at = gp_at(g, c, rec[0]);
         const double inv = gp_inv(lam, rec);
@@ -570,8 +592,7 @@ __device__ __forceinline__ void gp_camera_pass(const GPDev& g, const double* y, 
     double o[3] = {0.0, 0.0, 0.0};
     for (int i = o0 + lane; i < o1; i += 32) {
       double rec[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) rec[k] = __ldg(g.Jcm + k * Np + i);
+      gp_rec_ld<true>(g.Jcm, Np, i, rec);
       const int j = __ldg(g.topo.cm_pt + i);
       const double at = gp_at(g, c, rec[0]);
       const double inv = gp_inv(lam, rec);
@@ -624,8 +645,7 @@ __device__ __forceinline__ void gp_fused_pass(const GPDev& g, const FusedTopo& f
       double val[3] = {0.0, 0.0, 0.0};
       if (i < ob1) {
         c = __ldg(g.topo.pm_cam + i);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) rec[k] = __ldg(g.Jpm + k * Np + i);
+        gp_rec_ld<true>(g.Jpm, Np, i, rec);
         tk = __ldg(fz.tick + i);
         double pc[4];
         ld_v4(v + 4ll * c, pc);
@@ -658,8 +678,7 @@ __device__ __forceinline__ void gp_fused_pass(const GPDev& g, const FusedTopo& f
       if (have) {
         if (rounds > 1) {
           c = __ldg(g.topo.pm_cam + i);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) rec[k] = __ldg(g.Jpm + k * Np + i);
+          gp_rec_ld<true>(g.Jpm, Np, i, rec);
           tk = __ldg(fz.tick + i);
         }
         const int owner = rounds > 1 ? 0 : smown[warp][lane];
@@ -885,8 +904,7 @@ __global__ void __launch_bounds__(256) gp_k_backsub(GPDev g, const double* __res
       double val[3] = {0.0, 0.0, 0.0};
       if (i < ob1) {
         double rec[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) rec[k] = g.Jpm[k * Np + i];
+        gp_rec_ld<false>(g.Jpm, Np, i, rec);
         const int c = g.topo.pm_cam[i];
         const double at = gp_at(g, c, rec[0]);
         const double inv = gp_inv(lam, rec);
@@ -924,8 +942,7 @@ __global__ void __launch_bounds__(256) gp_k_backsub(GPDev g, const double* __res
         const int i = base + lane;
         if (i < ob1) {
           double rec[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) rec[k] = g.Jpm[k * Np + i];
+          gp_rec_ld<false>(g.Jpm, Np, i, rec);
           const int c = g.topo.pm_cam[i], j = g.topo.pm_pt[i];
           const double at = gp_at(g, c, rec[0]);
           const double inv = gp_inv(lam, rec);

@@ -28,6 +28,7 @@
 #include "block_algebra.cuh"
 #include "dense.cuh"
 #include "lm_graph.cuh"
+#include "prune.cuh"
 #include "schur_explicit.cuh"
 #include "metrics.cuh"
 
@@ -595,7 +596,7 @@ static int setup_ba_pcg(ssfm_handle* h, cudaStream_t st) {
   const char* fe = getenv("SSFM_FACTORED");
   if (h->fz.G == 0 && !(fe && fe[0] == '0')) {
     BADev& d = h->ba;
-    DALLOC(d.Fcm, (long long)(BA_FREC + 3) * d.Npad);
+    DALLOC(d.Fcm, fcm_doubles(d.bp.model, d.Npad));
     DALLOC(d.camlin, d.bp.C);
     h->pcg_fn = (void*)ba_k_pcg<0, true>;
     // and the point pass the omega form (ba_wobs: Jp + Jf, 8 doubles per
@@ -609,9 +610,6 @@ static int setup_ba_pcg(ssfm_handle* h, cudaStream_t st) {
       // ba_k_lin_points; SSFM_LIN2=0: the two evaluating passes)
       const char* le = getenv("SSFM_LIN2");
       if (!(le && le[0] == '0')) DALLOC(d.Rpm, 4ll * d.Npad);
-      // preconditioner point terms streamed camera-major (SSFM_KOBS=0: gathered)
-      const char* ke = getenv("SSFM_KOBS");
-      if (!(ke && ke[0] == '0')) DALLOC(d.Kcm, 8ll * d.Npad);
     }
   }
   const char* ge = getenv("SSFM_PCG_GRAPH");
@@ -1489,7 +1487,6 @@ static int launch_solve_pre(ssfm_handle* h, double lam, cudaStream_t st) {
   if (h->kind == 0) {
     BADev& d = h->ba;
     ba_k_ptinv<<<nblk(d.bp.P, 256), 256, 0, st>>>(d, lam);
-    if (d.Kcm) { ba_k_kobs<<<nblk(d.topo.N, 256), 256, 0, st>>>(d); count_launch(h); }
     if (d.topo.nt) ba_k_precond<<<d.topo.nt, SSFM_TILE, 0, st>>>(d);
     const double* cs = nullptr;
     if (sharded(h)) {
@@ -2249,10 +2246,40 @@ extern "C" int ssfm_check_jacobian(ssfm_handle* h, int64_t* mismatches, void* st
   return SSFM_OK;
 }
 
+// GP passes as standalone kernels (per-pass timing / ncu, ssfm_bench_operator)
+__global__ void __launch_bounds__(PCG_THREADS, 4) k_gop_point(GPDev d, const double* v, double* y) {
+  __shared__ double smp[PCG_THREADS / 32][SSFM_BATCH][3];
+  gp_point_pass(d, v, y, smp);
+}
+__global__ void __launch_bounds__(PCG_THREADS, 4) k_gop_camera(GPDev d, const double* y, double* tile4) {
+  __shared__ double smred[(PCG_THREADS / 32) * 8];
+  gp_camera_pass(d, y, tile4, smred);
+}
+
+static int bench_operator_gp(ssfm_handle* h, int32_t which, int32_t reps, double* ms_out, cudaStream_t st) {
+  GPDev& d = h->gp;
+  int occ_p = 0, occ_c = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, (const void*)k_gop_point, PCG_THREADS, 0));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, (const void*)k_gop_camera, PCG_THREADS, 0));
+  auto run = [&]() {
+    if (which != 1) k_gop_point<<<std::max(1, occ_p) * h->num_sms, PCG_THREADS, 0, st>>>(d, h->p, d.yv);
+    if (which != 0 && d.topo.nt) k_gop_camera<<<std::max(1, occ_c) * h->num_sms, PCG_THREADS, 0, st>>>(d, d.yv, d.tilebuf);
+  };
+  for (int w = 0; w < 2; ++w) run();
+  CU(cudaEventRecord(h->ev0, st));
+  for (int k = 0; k < reps; ++k) run();
+  CU(cudaEventRecord(h->ev1, st));
+  CU(cudaEventSynchronize(h->ev1));
+  float ms = 0.f;
+  CU(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  *ms_out = ms / reps;
+  return SSFM_OK;
+}
+
 extern "C" int ssfm_bench_operator(ssfm_handle* h, int32_t which, int32_t reps, double* ms_out, void* stream) {
   if (!h || !ms_out || reps < 1) return set_err(SSFM_INVALID_ARGUMENT, "bad argument");
-  if (h->kind != 0) return set_err(SSFM_INVALID_ARGUMENT, "BA handles only");
   cudaStream_t st = (cudaStream_t)stream;
+  if (h->kind == 1) return bench_operator_gp(h, which, reps, ms_out, st);
   BADev& d = h->ba;
   const bool fac = d.Fcm != nullptr;
   const void* fn = which != 1 ? (const void*)k_op_point
@@ -2636,5 +2663,83 @@ extern "C" int ssfm_make_rays(int64_t n, const int64_t* cam_idx, const double* p
   k_make_rays<<<nblk(n, 256), 256, 0, (cudaStream_t)stream>>>(n, (const long long*)cam_idx, pixels, pps, focals,
                                                               quats, depths, rays, ray_depths);
   CU(cudaGetLastError());
+  return SSFM_OK;
+}
+
+// ba.prune (ba.py:223-261) on the device (csrc/prune.cuh). Inputs and outputs
+// are device arrays; camera_map [C], point_map [P] (int32, -1 = removed),
+// obs_mask [N] (uint8). Returns SSFM_EMPTY_PROBLEM when every observation is
+// removed (errors.EmptyProblem, the reference raises the same).
+extern "C" int ssfm_prune(int64_t n, const int32_t* cam_idx, const int32_t* pt_idx, int32_t C, int32_t P,
+                          int32_t* camera_map, int32_t* point_map, uint8_t* obs_mask, int32_t* n_cam_out,
+                          int32_t* n_pt_out, int64_t* n_obs_out, void* stream) {
+  if (n < 0 || C < 0 || P < 0 || (n > 0 && (!cam_idx || !pt_idx)) || !camera_map || !point_map || !obs_mask)
+    return set_err(SSFM_INVALID_ARGUMENT, "ssfm_prune: bad argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned char *cam_ok = nullptr, *pt_ok = nullptr;
+  int *cnt_cam = nullptr, *cnt_pt = nullptr, *scan = nullptr, *flag = nullptr, *changed = nullptr;
+  unsigned long long* alive = nullptr;
+  int *hchanged = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  const int M = std::max(C, P) + 1;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (int*)nullptr, (int*)nullptr, M, st);
+  auto cleanup = [&]() {
+    cudaFree(cam_ok); cudaFree(pt_ok); cudaFree(cnt_cam); cudaFree(cnt_pt); cudaFree(scan); cudaFree(flag);
+    cudaFree(changed); cudaFree(alive); cudaFree(tmp);
+    if (hchanged) cudaFreeHost(hchanged);
+  };
+  if (cudaMalloc(&cam_ok, C + 1) || cudaMalloc(&pt_ok, P + 1) || cudaMalloc(&cnt_cam, sizeof(int) * (C + 1)) ||
+      cudaMalloc(&cnt_pt, sizeof(int) * (P + 1)) || cudaMalloc(&scan, sizeof(int) * M) ||
+      cudaMalloc(&flag, sizeof(int) * M) || cudaMalloc(&changed, sizeof(int)) ||
+      cudaMalloc(&alive, sizeof(unsigned long long)) || cudaMalloc(&tmp, tmp_bytes + 16) ||
+      cudaMallocHost((void**)&hchanged, sizeof(int))) {
+    cleanup();
+    return set_err(SSFM_CUDA_ERROR, "ssfm_prune: out of memory");
+  }
+  cudaMemsetAsync(cam_ok, 1, C + 1, st);
+  cudaMemsetAsync(pt_ok, 1, P + 1, st);
+  cudaMemsetAsync(cnt_cam, 0, sizeof(int) * (C + 1), st);
+  cudaMemsetAsync(cnt_pt, 0, sizeof(int) * (P + 1), st);
+  const int gb = std::max(1, std::min(nblk(n, 256), 148 * 8));
+  int rounds = 0;
+  while (true) {   // the fixed point of ba.py:234-243
+    cudaMemsetAsync(changed, 0, sizeof(int), st);
+    if (n > 0) k_prune_count<<<gb, 256, 0, st>>>(cam_idx, pt_idx, n, cam_ok, pt_ok, cnt_cam, cnt_pt);
+    if (P > 0) k_prune_drop<<<nblk(P, 256), 256, 0, st>>>(cnt_pt, pt_ok, P, 2, changed);
+    if (C > 0) k_prune_drop<<<nblk(C, 256), 256, 0, st>>>(cnt_cam, cam_ok, C, 1, changed);
+    cudaMemcpyAsync(hchanged, changed, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) { cleanup(); return set_err(SSFM_CUDA_ERROR, "ssfm_prune"); }
+    ++rounds;
+    if (!*hchanged) break;
+  }
+  // maps: exclusive scans of the survivor flags
+  int ncam = 0, npt = 0;
+  auto make_map = [&](const unsigned char* ok, int cnt, int32_t* map, int* total) -> int {
+    if (cnt == 0) { *total = 0; return 0; }
+    k_prune_flags<<<nblk(cnt + 1, 256), 256, 0, st>>>(ok, cnt + 1, flag);
+    cudaMemsetAsync(flag + cnt, 0, sizeof(int), st);
+    size_t tb = tmp_bytes;
+    if (cub::DeviceScan::ExclusiveSum(tmp, tb, flag, scan, cnt + 1, st)) return 1;
+    k_prune_map<<<nblk(cnt, 256), 256, 0, st>>>(ok, scan, cnt, map);
+    if (cudaMemcpyAsync(total, scan + cnt, sizeof(int), cudaMemcpyDeviceToHost, st)) return 1;
+    return cudaStreamSynchronize(st) != cudaSuccess;
+  };
+  if (make_map(cam_ok, C, camera_map, &ncam) || make_map(pt_ok, P, point_map, &npt)) {
+    cleanup();
+    return set_err(SSFM_CUDA_ERROR, "ssfm_prune: map");
+  }
+  unsigned long long nalive = 0;
+  cudaMemsetAsync(alive, 0, sizeof(unsigned long long), st);
+  if (n > 0) k_prune_obs<<<gb, 256, 0, st>>>(cam_idx, pt_idx, n, cam_ok, pt_ok, obs_mask, alive);
+  cudaMemcpyAsync(&nalive, alive, sizeof(nalive), cudaMemcpyDeviceToHost, st);
+  const cudaError_t e = cudaStreamSynchronize(st);
+  cleanup();
+  if (e != cudaSuccess) return set_err(SSFM_CUDA_ERROR, std::string("ssfm_prune: ") + cudaGetErrorString(e));
+  if (n_cam_out) *n_cam_out = ncam;
+  if (n_pt_out) *n_pt_out = npt;
+  if (n_obs_out) *n_obs_out = (int64_t)nalive;
+  (void)rounds;
+  if (nalive == 0) return set_err(SSFM_EMPTY_PROBLEM, "pruning removed every observation");
   return SSFM_OK;
 }

@@ -96,6 +96,21 @@ class _Sharded:
         self._connect_torch(h)
         return h
 
+    def _enter_collective(self):
+        """Before every native call that exchanges with the peers. Several
+        shards on one device (comm="local"): each shard first finishes its
+        torch-side work on its stream, then all shards enter together. The
+        exchanges spin on the device, and a torch allocation, device-to-device
+        copy or memset issued by one shard's thread while a peer's kernel
+        already waits in an exchange is an implicit synchronisation point
+        between the streams: that shard's kernels would queue behind the
+        peer's waiting kernel. (One process per GPU has no such hazard.)"""
+        bar = getattr(self, "_local_barrier", None)
+        if bar is not None:
+            import torch
+            torch.cuda.current_stream().synchronize()
+            bar.wait(timeout=600)
+
     def _native_handle(self, workspace=None):
         h = super()._native_handle(workspace)
         if not self._connected:
@@ -223,7 +238,16 @@ def connect_local(problems) -> None:
     this process on the current device: exchange regions are plain device
     pointers. Their collective calls must then run concurrently (one host
     thread per problem) and their PCG grids must fit the device together
-    (set SSFM_PCG_SMS before the handles are created)."""
+    (set SSFM_PCG_SMS before the handles are created). The process needs
+    CUDA_MODULE_LOADING=EAGER (set before CUDA initialises): a kernel loaded
+    lazily at its first launch waits for the device, i.e. for a peer shard's
+    kernel spinning in an exchange."""
+    import os
+    import warnings
+    if os.environ.get("CUDA_MODULE_LOADING", "LAZY").upper() != "EAGER":
+        warnings.warn("connect_local: set CUDA_MODULE_LOADING=EAGER before CUDA initialises; with lazy "
+                      "module loading the first exchange of same-device shards can stall", RuntimeWarning)
+    import threading
     lib = _native.load()
     world = len(problems)
     regions = (ct.c_void_p * world)()
@@ -238,6 +262,9 @@ def connect_local(problems) -> None:
         h = _DeviceProblem._native_handle(p)
         _native.check(lib.ssfm_comm_connect(ct.c_void_p(h.ptr), None, regions))
         p._connected = True
+    bar = threading.Barrier(world)   # the shards enter each collective call together (_enter_collective)
+    for p in problems:
+        p._local_barrier = bar
 
 
 def run_ba_sharded(scene, loss=None, config=None, optimize_focal: bool = True, group=None):

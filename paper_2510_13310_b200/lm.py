@@ -178,6 +178,7 @@ def lm_solve(problem, theta0, config: LMConfig | None = None,
     nrec = ct.c_int32(0)
     term = ct.c_int32(0)
     cfg = _native.lm_config_c(config)
+    getattr(problem, "_enter_collective", lambda: None)()
     rc = lib.ssfm_lm_solve(ct.c_void_p(h.ptr), ct.c_void_p(theta.data_ptr()), ct.byref(cfg), recs,
                            cap, ct.byref(nrec), ct.byref(term), _stream(torch))
     report = SolveReport(termination=_native.TERMINATIONS.get(term.value, "max_iter"))

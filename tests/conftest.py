@@ -22,6 +22,13 @@ os.environ.setdefault("SSFM_COMM_TIMEOUT_S", "45")
 # waits behind its peer's spinning PCG kernel (false serialisation, observed as
 # 40 s stalls). Read at CUDA context creation, so set before torch touches CUDA.
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+# ... and every kernel must be loaded before the first exchange: with lazy
+# module loading (CUDA 12's default) the first launch of a kernel loads it,
+# and that load waits for the device, including a peer shard's kernel that
+# spins in an exchange waiting for this shard -- the first collective of the
+# first same-device sharded solve then stalls until the exchange timeout.
+# (One process per GPU has no such cross-shard wait.)
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
 
 def pytest_configure(config):
