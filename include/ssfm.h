@@ -209,6 +209,15 @@ int ssfm_prune(int64_t n, const int32_t* cam_idx, const int32_t* pt_idx, int32_t
                int32_t* camera_map, int32_t* point_map, uint8_t* obs_mask, int32_t* n_cam_out,
                int32_t* n_pt_out, int64_t* n_obs_out, void* stream);
 
+/* The CUDA device a handle lives on. */
+int32_t ssfm_handle_device(const ssfm_handle* h);
+
+/* Several devices in one process (dist.connect_local): enable direct access
+ * from `device` to `peer` before their handles' exchange regions are
+ * connected (ssfm_comm_connect with region pointers). SSFM_COMM_ERROR when
+ * the devices cannot access each other. */
+int ssfm_enable_peer_access(int32_t device, int32_t peer);
+
 /* How lm_solve runs its loop on this handle: 1 = the whole LM loop as one
  * CUDA graph (accept/reject, lambda and termination decided on the device,
  * one read-back per solve; single-rank BA handles, SSFM_LM_GRAPH=0 disables),

@@ -28,7 +28,7 @@ EXPORTS = (
     "ssfm_rotation_auc", "ssfm_center_moments", "ssfm_apply_sim3",
     "ssfm_bal_read", "ssfm_bal_take", "ssfm_bal_free", "ssfm_make_rays", "ssfm_schur_solve",
     "ssfm_trim_cache", "ssfm_cache_bytes", "ssfm_arena_create", "ssfm_arena_destroy", "ssfm_arena_info",
-    "ssfm_create_ba_in", "ssfm_create_gp_in", "ssfm_lm_mode", "ssfm_prune",
+    "ssfm_create_ba_in", "ssfm_create_gp_in", "ssfm_lm_mode", "ssfm_prune", "ssfm_handle_device", "ssfm_enable_peer_access",
 )
 
 TERMINATIONS = {0: "max_iter", 1: "converged_cost", 2: "converged_grad", 3: "solver_failure"}
@@ -107,6 +107,9 @@ def load(required: bool = True):
     P, I32, I64, D = ct.c_void_p, ct.c_int32, ct.c_int64, ct.c_double
     lib.ssfm_last_error.restype = ct.c_char_p
     lib.ssfm_version.restype = ct.c_char_p
+    lib.ssfm_handle_device.argtypes = [P]
+    lib.ssfm_handle_device.restype = I32
+    lib.ssfm_enable_peer_access.argtypes = [I32, I32]
     lib.ssfm_lm_mode.argtypes = [P]
     lib.ssfm_lm_mode.restype = I32
     lib.ssfm_prune.argtypes = [I64, P, P, I32, I32, P, P, P, ct.POINTER(I32), ct.POINTER(I32), ct.POINTER(I64), P]

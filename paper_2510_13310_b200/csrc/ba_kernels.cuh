@@ -423,92 +423,61 @@ __global__ void __launch_bounds__(SSFM_TILE) ba_k_linearize_cm(BADev d, const do
 //    Jp^T Jf) summed per point in observation order from Gpm / Rpm, as
 //    ba_k_linearize does (the same values: the records are bit-identical).
 // ---------------------------------------------------------------------------
-#ifndef LIN_FRAME
-#define LIN_FRAME 0   // camera-frame accumulation of the tile's J^T J (no full Jacobian per observation)
-#endif
 __device__ __forceinline__ double ba_precond_f_entry(const double* cb, const double* w, int o);
-__global__ void __launch_bounds__(SSFM_TILE) ba_k_lin_tile(BADev d, const double* __restrict__ theta) {
+#ifndef LIN_MINB
+#define LIN_MINB 1
+#endif
+// one observation of ba_k_lin_tile: records out, its J^T J / J^T r terms added to v
+__device__ __forceinline__ void ba_lin_obs(const BADev& d, const double* __restrict__ theta, int c, long long i,
+                                           double* v) {
+  const unsigned long long pst = pol_evict_first();
+  const int j = d.topo.cm_pt[i];
+  const int ip = d.topo.cm_to_pm[i];
+  double r[2], J[BA_JREC], ct, F[BA_FREC + 3];
+  ba_obs_eval(d.bp, d.cams + c, theta + d.bp.off_pts + 3ll * j, d.pix_cm + 2ll * i, r, J, &ct, F);
+  fcm_store(d, i, F, pst);   // pinhole: s01, s11 are implied
+  gpm_store(d, ip, J + 8);
+  *reinterpret_cast<double4*>(d.Rpm + 4ll * ip) = make_double4(r[0], r[1], 0.0, 0.0);
+  double a[8], b[8];
+  ba_jc_row(J, 0, a);
+  ba_jc_row(J, 1, b);
+  int idx = 0;
+#pragma unroll
+  for (int p = 0; p < 8; ++p)
+#pragma unroll
+    for (int q = p; q < 8; ++q) v[idx++] += a[p] * a[q] + b[p] * b[q];
+#pragma unroll
+  for (int p = 0; p < 8; ++p) v[36 + p] += a[p] * r[0] + b[p] * r[1];
+}
+
+// per tile group (topo.grp_tile: up to SSFM_GRP tiles of one camera; the
+// camera is uniform, so no per-observation camera gather): every observation
+// evaluated once; its records written; the group's J^T J / J^T r reduced
+// once into its first tile's slot (the other tiles' slots zero)
+__global__ void __launch_bounds__(SSFM_TILE, LIN_MINB) ba_k_lin_tile(BADev d, const double* __restrict__ theta) {
   __shared__ double sm[(SSFM_TILE / 32) * CAM_V];
-  const int t = blockIdx.x;
-  const int o0 = d.topo.tile_obs[t], o1 = d.topo.tile_obs[t + 1];
-  const int c = d.topo.tile_cam[t];
-  const int i = o0 + threadIdx.x;
+  __shared__ double smw[CAM_V];
+  const int g = blockIdx.x;
+  const int t0 = d.topo.grp_tile[g], t1 = d.topo.grp_tile[g + 1];
+  const int o0 = d.topo.tile_obs[t0], o1 = d.topo.tile_obs[t1];
+  const int c = d.topo.tile_cam[t0];
   double v[CAM_V];
 #pragma unroll
   for (int k = 0; k < CAM_V; ++k) v[k] = 0.0;
-  if (i < o1) {
-    const unsigned long long pst = pol_evict_first();
-    const int j = d.topo.cm_pt[i];
-    const int ip = d.topo.cm_to_pm[i];
-#if LIN_FRAME
-    // residual and factored record only; Jp = S E R, Jf = phi e; the tile's
-    // J^T J / J^T r accumulate the camera-frame rows
-    // a~_r = [D(v)^T (SE)_r ; -(SE)_r ; phi e_r] and are mapped once per tile
-    // through T = diag(Pi, R^T, 1) (as ba_k_precond does)
-    const BACam cc = d.cams[c];
-    BAProj pr;
-    double r[2], sw, ct, F[BA_FREC + 3];
-    ba_residual(d.bp, cc, theta + d.bp.off_pts + 3ll * j, d.pix_cm + 2ll * i, pr, r, sw, ct);
-    ba_factor(d.bp, cc, pr, sw, F);
-    F[6] = pr.v[0]; F[7] = pr.v[1]; F[8] = pr.v[2];
-    fcm_store(d, i, F, pst);
-    const double f4 = d.bp.model == 1 ? F[4] : 0.0, f5 = d.bp.model == 1 ? F[5] : F[0];
-    const double se[2][3] = {{F[0], f4, -(F[0] * F[1] + f4 * F[2])}, {f4, f5, -(f4 * F[1] + f5 * F[2])}};
-    double g8[8];
-#pragma unroll
-    for (int rr = 0; rr < 2; ++rr)
-#pragma unroll
-      for (int k = 0; k < 3; ++k)
-        g8[3 * rr + k] = se[rr][0] * cc.R[k] + se[rr][1] * cc.R[3 + k] + se[rr][2] * cc.R[6 + k];
-    g8[6] = F[3] * F[1];
-    g8[7] = F[3] * F[2];
-    gpm_store(d, ip, g8);
-    *reinterpret_cast<double4*>(d.Rpm + 4ll * ip) = make_double4(r[0], r[1], 0.0, 0.0);
-    double a[8], b[8];
-    ba_dqt_mul(cc.qh, pr.v, se[0], a);
-    ba_dqt_mul(cc.qh, pr.v, se[1], b);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) { a[4 + k] = -se[0][k]; b[4 + k] = -se[1][k]; }
-    a[7] = g8[6];
-    b[7] = g8[7];
-#else
-    double r[2], J[BA_JREC], ct, F[BA_FREC + 3];
-    ba_obs_eval(d.bp, d.cams + c, theta + d.bp.off_pts + 3ll * j, d.pix_cm + 2ll * i, r, J, &ct, F);
-    fcm_store(d, i, F, pst);   // pinhole: s01, s11 are implied
-    gpm_store(d, ip, J + 8);
-    *reinterpret_cast<double4*>(d.Rpm + 4ll * ip) = make_double4(r[0], r[1], 0.0, 0.0);
-    double a[8], b[8];
-    ba_jc_row(J, 0, a);
-    ba_jc_row(J, 1, b);
-#endif
-    int idx = 0;
-#pragma unroll
-    for (int p = 0; p < 8; ++p)
-#pragma unroll
-      for (int q = p; q < 8; ++q) v[idx++] = a[p] * a[q] + b[p] * b[q];
-#pragma unroll
-    for (int p = 0; p < 8; ++p) v[36 + p] = a[p] * r[0] + b[p] * r[1];
-  }
+  for (int i = o0 + threadIdx.x; i < o1; i += blockDim.x) ba_lin_obs(d, theta, c, i, v);
   block_reduce<CAM_V>(v, sm);
-#if LIN_FRAME
-  __shared__ double smw[CAM_V];
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int k = 0; k < CAM_V; ++k) smw[k] = v[k];
   }
   __syncthreads();
-  if (threadIdx.x < 32) {
-    const double* cb = reinterpret_cast<const double*>(d.camlin + c);
-    double* dst = d.tilebuf + (long long)CAM_V * t;
-    for (int o = threadIdx.x; o < CAM_V; o += 32) dst[o] = ba_precond_f_entry(cb, smw, o);
+  if (threadIdx.x < 64) {
+    double* dst = d.tilebuf + (long long)CAM_V * t0;
+    for (int o = threadIdx.x; o < CAM_V; o += 64) dst[o] = smw[o];
+  } else {
+    for (int k = threadIdx.x - 64; k < CAM_V * (t1 - t0 - 1); k += blockDim.x - 64)
+      d.tilebuf[(long long)CAM_V * (t0 + 1) + k] = 0.0;
   }
-#else
-  if (threadIdx.x == 0) {
-    double* dst = d.tilebuf + (long long)CAM_V * t;
-#pragma unroll
-    for (int k = 0; k < CAM_V; ++k) dst[k] = v[k];
-  }
-#endif
 }
 
 __global__ void __launch_bounds__(256) ba_k_lin_points(BADev d, const double* __restrict__ theta,
@@ -751,11 +720,8 @@ __global__ void ba_k_ptinv(BADev d, double lam) {
 // Factored form (two-pass handles, no Jcm): the rows of Jc in the camera
 // frame, a~_r = [D(v)^T (SE)_r ; -(SE)_r ; phi e_r], are reduced over the
 // tile and mapped once per tile by T = diag(Pi, R^T, 1): W = T W~ T^T.
-__device__ __forceinline__ void ba_precond_f(const BADev& d, int t, double* v) {
-  const int o0 = d.topo.tile_obs[t], o1 = d.topo.tile_obs[t + 1];
-  const int i = o0 + threadIdx.x;
-  if (i >= o1) return;
-  const double* cb = reinterpret_cast<const double*>(d.camlin + d.topo.tile_cam[t]);
+// accumulates observation i's terms into v (the tile's camera cache cb)
+__device__ __forceinline__ void ba_precond_f(const BADev& d, long long i, const double* cb, double* v) {
   double f[6], vv[3];
   fcm_load(d, i, f, vv, pol_evict_first());
   double qh[4];
@@ -799,9 +765,9 @@ __device__ __forceinline__ void ba_precond_f(const BADev& d, int t, double* v) {
 #pragma unroll
   for (int p = 0; p < 8; ++p)
 #pragma unroll
-    for (int q = p; q < 8; ++q) v[idx++] = a[p] * ka[q] + b[p] * kb[q];
+    for (int q = p; q < 8; ++q) v[idx++] += a[p] * ka[q] + b[p] * kb[q];
 #pragma unroll
-  for (int p = 0; p < 8; ++p) v[36 + p] = a[p] * ty0 + b[p] * ty1;
+  for (int p = 0; p < 8; ++p) v[36 + p] += a[p] * ty0 + b[p] * ty1;
 }
 
 
@@ -852,22 +818,7 @@ __global__ void __launch_bounds__(SSFM_TILE) ba_k_precond(BADev d) {
   double v[CAM_V];
 #pragma unroll
   for (int k = 0; k < CAM_V; ++k) v[k] = 0.0;
-  if (!d.Jcm) {
-    __shared__ double smw[CAM_V];
-    ba_precond_f(d, t, v);
-    block_reduce<CAM_V>(v, sm);
-    if (threadIdx.x == 0) {
-#pragma unroll
-      for (int k = 0; k < CAM_V; ++k) smw[k] = v[k];
-    }
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      const double* cb = reinterpret_cast<const double*>(d.camlin + d.topo.tile_cam[t]);
-      double* dst = d.tilebuf + (long long)CAM_V * t;
-      for (int o = threadIdx.x; o < CAM_V; o += 32) dst[o] = ba_precond_f_entry(cb, smw, o);
-    }
-    return;
-  }
+  if (!d.Jcm) return;   // factored records: ba_k_precond_grp
   if (i < o1) {
     const long long Np = d.Npad;
     double J[BA_JREC];
@@ -908,6 +859,41 @@ __global__ void __launch_bounds__(SSFM_TILE) ba_k_precond(BADev d) {
     double* dst = d.tilebuf + (long long)CAM_V * t;
 #pragma unroll
     for (int k = 0; k < CAM_V; ++k) dst[k] = v[k];
+  }
+}
+
+// Factored preconditioner terms per tile GROUP (up to SSFM_GRP consecutive
+// tiles of one camera, topo.grp_tile): each thread accumulates several
+// observations, one block reduction and one mapping through
+// T = diag(Pi, R^T, 1) per group instead of per tile. The group's sums land
+// in its first tile's slot; its other tiles' slots are zero (the per-camera
+// sums over tiles are unchanged).
+#ifndef PRE_MINB
+#define PRE_MINB 1   // CTAs per SM (2: 128 registers with spills)
+#endif
+__global__ void __launch_bounds__(SSFM_TILE, PRE_MINB) ba_k_precond_grp(BADev d) {
+  __shared__ double sm[(SSFM_TILE / 32) * CAM_V];
+  __shared__ double smw[CAM_V];
+  const int g = blockIdx.x;
+  const int t0 = d.topo.grp_tile[g], t1 = d.topo.grp_tile[g + 1];
+  const int o0 = d.topo.tile_obs[t0], o1 = d.topo.tile_obs[t1];
+  const double* cb = reinterpret_cast<const double*>(d.camlin + d.topo.tile_cam[t0]);
+  double v[CAM_V];
+#pragma unroll
+  for (int k = 0; k < CAM_V; ++k) v[k] = 0.0;
+  for (int i = o0 + threadIdx.x; i < o1; i += blockDim.x) ba_precond_f(d, i, cb, v);
+  block_reduce<CAM_V>(v, sm);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < CAM_V; ++k) smw[k] = v[k];
+  }
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    double* dst = d.tilebuf + (long long)CAM_V * t0;
+    for (int o = threadIdx.x; o < CAM_V; o += 64) dst[o] = ba_precond_f_entry(cb, smw, o);
+  } else {
+    for (int k = threadIdx.x - 64; k < CAM_V * (t1 - t0 - 1); k += blockDim.x - 64)
+      d.tilebuf[(long long)CAM_V * (t0 + 1) + k] = 0.0;
   }
 }
 

@@ -49,16 +49,18 @@ struct FusedTopo {
 #define FZ_MAX_TICKET 65535
 
 // Ticket counters live in shared memory; acquire/release at CTA scope on the
-// shared window (generic atomics would go through the generic LSU path).
+// shared window (generic atomics would go through the generic LSU path). As
+// atomics (an OR with 0 to read, an exchange to write) so that racecheck sees
+// the flag protocol as synchronisation, not as racing plain accesses.
 __device__ __forceinline__ int ld_acquire_smem(const int* p) {
   const unsigned a = (unsigned)__cvta_generic_to_shared(p);
   int v;
-  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  asm volatile("atom.acquire.cta.shared::cta.or.b32 %0, [%1], 0;" : "=r"(v) : "r"(a) : "memory");
   return v;
 }
 __device__ __forceinline__ void st_release_smem(int* p, int v) {
   const unsigned a = (unsigned)__cvta_generic_to_shared(p);
-  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+  asm volatile("{ .reg .b32 old; atom.release.cta.shared::cta.exch.b32 old, [%0], %1; }" ::"r"(a), "r"(v) : "memory");
 }
 
 // Camera accumulator layout: SL doubles per camera, its 16-byte chunks XOR-

@@ -422,6 +422,20 @@ static int build_topo(ssfm_handle* h, const int* cam, const int* pt, int C, int 
   DALLOC(T.tile_obs, nt + 1); DALLOC(T.tile_cam, nt + 1);
   if (C) k_tile_write<<<nblk(C, TB), TB, 0, st>>>(T.cam_seg, T.cam_tile, C, T.tile_obs, T.tile_cam);
   k_set_last<<<1, 1, 0, st>>>(T.tile_obs, nt, (int)N);
+  // tile groups (host: C + 1 tile offsets)
+  {
+    std::vector<int> ct(C + 1);
+    CU(cudaMemcpyAsync(ct.data(), T.cam_tile, sizeof(int) * (C + 1), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    std::vector<int> g;
+    for (int c = 0; c < C; ++c)
+      for (int t = ct[c]; t < ct[c + 1]; t += SSFM_GRP) g.push_back(t);
+    g.push_back(nt);
+    T.ng = (int)g.size() - 1;
+    DALLOC(T.grp_tile, g.size());
+    CU(cudaMemcpyAsync(T.grp_tile, g.data(), sizeof(int) * g.size(), cudaMemcpyHostToDevice, st));
+    CU(cudaStreamSynchronize(st));
+  }
   CU(cudaGetLastError());
   return SSFM_OK;
 }
@@ -1113,7 +1127,7 @@ static int launch_linearize(ssfm_handle* h, const double* theta, double* r_out, 
     if (d.camlin) CU(copy_async(reinterpret_cast<double*>(d.camlin), reinterpret_cast<const double*>(d.cams),
                                 (long long)(sizeof(BACam) / 8) * d.bp.C, st));
     if (d.Rpm && !r_out && !J_out) {   // each observation evaluated once (camera tiles), then point sums
-      if (d.topo.nt) ba_k_lin_tile<<<d.topo.nt, SSFM_TILE, 0, st>>>(d, theta);
+      if (d.topo.nt) ba_k_lin_tile<<<d.topo.ng, SSFM_TILE, 0, st>>>(d, theta);   // tile groups
       ba_k_lin_points<<<h->lin_blocks, 256, 0, st>>>(d, theta, h->red);
     } else {
       ba_k_linearize<<<h->lin_blocks, 256, 0, st>>>(d, theta, r_out, J_out, h->red);
@@ -1487,7 +1501,10 @@ static int launch_solve_pre(ssfm_handle* h, double lam, cudaStream_t st) {
   if (h->kind == 0) {
     BADev& d = h->ba;
     ba_k_ptinv<<<nblk(d.bp.P, 256), 256, 0, st>>>(d, lam);
-    if (d.topo.nt) ba_k_precond<<<d.topo.nt, SSFM_TILE, 0, st>>>(d);
+    if (d.topo.nt) {
+      if (d.Jcm) ba_k_precond<<<d.topo.nt, SSFM_TILE, 0, st>>>(d);
+      else ba_k_precond_grp<<<d.topo.ng, SSFM_TILE, 0, st>>>(d);   // factored records: tile groups
+    }
     const double* cs = nullptr;
     if (sharded(h)) {
       k_cam_tilesum<<<h->cam_blocks, 256, 0, st>>>(d.topo, d.tilebuf, CAM_V, h->camsum);
@@ -2222,6 +2239,27 @@ extern "C" int ssfm_comm_connect(ssfm_handle* h, const void* ipc_handles, void* 
     if (rc) return rc;
     h->graph_sharded = true;
   }
+  return SSFM_OK;
+}
+
+extern "C" int32_t ssfm_handle_device(const ssfm_handle* h) { return h ? h->device : -1; }
+
+// Peer access from `device` to `peer` (several devices driven by one process,
+// dist.connect_local): the exchange regions of the other devices' handles are
+// then read and written directly over NVLink.
+extern "C" int ssfm_enable_peer_access(int32_t device, int32_t peer) {
+  if (device == peer) return SSFM_OK;
+  int can = 0;
+  CU(cudaDeviceCanAccessPeer(&can, device, peer));
+  if (!can) return set_err(SSFM_COMM_ERROR, "device " + std::to_string(device) + " cannot access device " +
+                                                std::to_string(peer) + " (no peer access)");
+  int cur = 0;
+  CU(cudaGetDevice(&cur));
+  CU(cudaSetDevice(device));
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) { cudaGetLastError(); e = cudaSuccess; }
+  cudaSetDevice(cur);
+  if (e != cudaSuccess) return set_err(SSFM_COMM_ERROR, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
   return SSFM_OK;
 }
 

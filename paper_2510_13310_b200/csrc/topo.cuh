@@ -43,6 +43,10 @@ struct Topo {
   int* tile_cam = nullptr;  // [nt]
   int* cam_tile = nullptr;  // [C+1]
   int nt = 0;
+  // tile groups: up to SSFM_GRP consecutive tiles of one camera (one CTA of
+  // the per-camera reductions: linearize, preconditioner)
+  int* grp_tile = nullptr;  // [ng+1] first tile of each group
+  int ng = 0;
 };
 
 __global__ void k_check_index(const int* __restrict__ cam, const int* __restrict__ pt,
@@ -145,3 +149,7 @@ __global__ void k_tile_write(const int* __restrict__ cam_seg, const int* __restr
 }
 
 __global__ void k_set_last(int* a, int idx, int v) { a[idx] = v; }
+
+#ifndef SSFM_GRP
+#define SSFM_GRP 4
+#endif

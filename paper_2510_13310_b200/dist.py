@@ -235,8 +235,8 @@ class ShardedGPProblem(_Sharded, GPProblem):
 
 def connect_local(problems) -> None:
     """Connect several sharded problems (ranks 0..R-1 of one problem) living in
-    this process on the current device: exchange regions are plain device
-    pointers. Their collective calls must then run concurrently (one host
+    this process -- on one device, or on several (peer access is enabled
+    between them): exchange regions are plain device pointers. Their collective calls must then run concurrently (one host
     thread per problem) and their PCG grids must fit the device together
     (set SSFM_PCG_SMS before the handles are created). The process needs
     CUDA_MODULE_LOADING=EAGER (set before CUDA initialises): a kernel loaded
@@ -254,6 +254,13 @@ def connect_local(problems) -> None:
     for p in problems:
         if p.world != world or p.comm != "local":
             raise ValueError("connect_local needs comm='local' problems of one world")
+    # shards on several devices of this process: direct peer access both ways
+    devs = sorted({int(lib.ssfm_handle_device(ct.c_void_p(_DeviceProblem._native_handle(p).ptr))) for p in problems})
+    for a in devs:
+        for b in devs:
+            if a != b:
+                _native.check(lib.ssfm_enable_peer_access(a, b))
+    for p in problems:
         h = _DeviceProblem._native_handle(p)
         reg = ct.c_void_p(0)
         _native.check(lib.ssfm_comm_init(ct.c_void_p(h.ptr), p.rank, world, None, ct.byref(reg)))

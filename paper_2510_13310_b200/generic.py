@@ -530,7 +530,8 @@ def lm_solve_generic(problem, theta0, config, workspace=None):
     from .sparse_block import apply_damping, jtj, jtr
     ws = workspace or Workspace()
     layout = problem.layout
-    theta = np.array(theta0, dtype=np.float64, copy=True)
+    was_tensor = hasattr(theta0, "detach") and hasattr(theta0, "device")   # a torch tensor: returned as one
+    theta = np.array(theta0.detach().cpu().numpy() if was_tensor else theta0, dtype=np.float64, copy=True)
     if theta.shape != (layout.total_params,):
         from .errors import DimensionMismatch
         raise DimensionMismatch("theta0 length does not match the problem layout")
@@ -578,4 +579,7 @@ def lm_solve_generic(problem, theta0, config, workspace=None):
                 break
         else:
             lam = min(lam * config.lambda_up, config.lambda_max)
+    if was_tensor:
+        import torch
+        return torch.as_tensor(theta).to(theta0.device), report
     return theta, report

@@ -37,12 +37,18 @@ for rep in range(2):
             ms = ct.c_double()
             _native.check(lib.ssfm_bench_operator(ct.c_void_p(h.ptr), which, 20, ct.byref(ms), st))
             out.append(ms.value)
+        lib.ssfm_profile_enable(ct.c_void_p(h.ptr), 1)
         _, r = b2.lm_solve(p, th, b2.LMConfig(max_iterations=4))
+        pms, pl, cgit = ct.c_double(0), ct.c_int64(0), ct.c_double(0)
+        lib.ssfm_profile_get(ct.c_void_p(h.ptr), 0, ct.byref(pms), ct.byref(pl), ct.byref(cgit))
+        lib.ssfm_profile_enable(ct.c_void_p(h.ptr), 0)
         dm = [round(i.device_ms, 2) for i in r.iterations]
         cg = [i.cg_iters for i in r.iterations]
         per_cg = sum(i.device_ms for i in r.iterations[1:]) / max(1, sum(cg[1:]))
+        non_pcg = (sum(i.device_ms for i in r.iterations) - pms.value) / max(1, len(r.iterations))
         print(f"{os.path.basename(lib_path) + ' ' + envs:40s} point {out[0]:.4f} camera {out[1]:.4f} pair {out[2]:.4f} ms | "
-              f"lm ms {dm} cg {cg} ({per_cg:.4f} ms/cg incl. step overhead)", flush=True)
+              f"lm ms {dm} cg {cg} ({per_cg:.4f} ms/cg incl. step overhead; non-PCG {non_pcg:.2f} ms/it, "
+              f"PCG {pms.value / max(1, cgit.value):.4f} ms/cg)", flush=True)
         p.release(trim=True)
         for kv in filter(None, envs.split(",")):
             os.environ.pop(kv.split("=")[0], None)

@@ -96,6 +96,10 @@ def test_lm_solve_dense_solver_and_foreign_provider(gpu):
     assert rep.termination == "converged_cost"
     assert rep.iterations[-1].cost_after == pytest.approx(float(z["records"][-1, 2]), rel=1e-8)
     assert all(i.cg_iters == 0 for i in rep.iterations)
+    # tensor in, tensor out (as on the native path)
+    tht, rept = b2.lm_solve(p, gpu.as_tensor(z["theta0"]).cuda(), b2.LMConfig(solver="dense", max_iterations=30))
+    assert isinstance(tht, gpu.Tensor) and tht.is_cuda
+    assert np.array_equal(tht.cpu().numpy(), th) and rept.termination == rep.termination
 
     class Line:                     # a duck-typed provider (lm.py:730-739): fit y = a x + b
         def __init__(self):
