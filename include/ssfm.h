@@ -69,7 +69,7 @@ typedef enum {
 } ssfm_termination;
 
 enum { SSFM_PINHOLE = 0, SSFM_BAL_RADIAL = 1 };   /* scene.py:19-20 */
-enum { SSFM_LOSS_TRIVIAL = 0, SSFM_LOSS_HUBER = 1 }; /* scene.py:233-242 */
+enum { SSFM_LOSS_TRIVIAL = 0, SSFM_LOSS_HUBER = 1, SSFM_LOSS_CAUCHY = 2 }; /* scene.py:233-242; Cauchy: an extension */
 
 /* LMConfig (lm.py:36-58). solver: 0 = schur_pcg (the only device solver). */
 typedef struct {

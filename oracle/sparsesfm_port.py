@@ -85,8 +85,13 @@ def drotate_dq(q, v):
 
 
 def huber(kind, delta, s):
-    """(cost, weight) per block (scene.py:398-408)."""
+    """(cost, weight) per block (scene.py:398-408). kind "cauchy" is an
+    extension with no reference counterpart (parity unpinned): cost =
+    delta^2 log1p(s / delta^2), weight = 1 / (1 + s / delta^2)."""
     s = np.asarray(s, dtype=np.float64)
+    if kind == "cauchy":
+        d2 = delta * delta
+        return d2 * np.log1p(s / d2), 1.0 / (1.0 + s / d2)
     if kind != "huber":
         return s.copy(), np.ones_like(s)
     d2 = delta * delta

@@ -35,7 +35,7 @@ struct BAParams {
   long long N;
   int model;          // 0 pinhole, 1 bal
   int focal_mode;     // 0 none (fixed focals), 1 per camera, 2 shared
-  int loss_kind;      // 0 trivial, 1 huber
+  int loss_kind;      // 0 trivial, 1 huber, 2 cauchy
   double delta;
   long long off_pts;  // 7C
   long long off_foc;  // 7C + 3P
@@ -104,6 +104,13 @@ __device__ __forceinline__ void ba_project(const BACam& c, const double* X, int 
 
 // robust_weight_many (scene.py:398-408): cost term and IRLS weight.
 __device__ __forceinline__ void robust(int kind, double delta, double s, double& cost, double& w) {
+  if (kind == 2) {   // Cauchy (an extension: scene.cauchy_cost_weight)
+    const double d2 = MUL(delta, delta);
+    const double r = DIV(s, d2);
+    cost = MUL(d2, log1p(r));
+    w = DIV(1.0, ADD(1.0, r));
+    return;
+  }
   if (kind == 1) {
     const double d2 = MUL(delta, delta);
     if (s > d2) {

@@ -763,6 +763,10 @@ static int create_ba(const ssfm_ba_desc* desc, ssfm_arena* arena, void* stream, 
   d.bp.C = C; d.bp.P = P; d.bp.N = N;
   d.bp.model = desc->model;
   d.bp.focal_mode = desc->optimize_focal ? (desc->shared_focal ? 2 : 1) : 0;
+  if (desc->loss_kind < 0 || desc->loss_kind > 2) {
+    free_handle(h);
+    return set_err(SSFM_INVALID_ARGUMENT, "unknown loss kind");
+  }
   d.bp.loss_kind = desc->loss_kind;
   d.bp.delta = desc->loss_delta;
   d.bp.off_pts = 7ll * C;
@@ -884,6 +888,10 @@ static int create_gp(const ssfm_gp_desc* desc, ssfm_arena* arena, void* stream, 
   g.gp.C = C; g.gp.P = P; g.gp.N = N;
   g.gp.depth_mode = desc->depth_mode;
   g.gp.gauge_fixed = desc->gauge_fixed;
+  if (desc->loss_kind < 0 || desc->loss_kind > 2) {
+    free_handle(h);
+    return set_err(SSFM_INVALID_ARGUMENT, "unknown loss kind");
+  }
   g.gp.loss_kind = desc->loss_kind;
   g.gp.delta = desc->loss_delta;
   g.gp.off_pts = 3ll * C;
