@@ -427,20 +427,24 @@ __device__ __forceinline__ double ba_precond_f_entry(const double* cb, const dou
 #ifndef LIN_MINB
 #define LIN_MINB 1
 #endif
-// one observation of ba_k_lin_tile: records out, its J^T J / J^T r terms added to v
-__device__ __forceinline__ void ba_lin_obs(const BADev& d, const double* __restrict__ theta, int c, long long i,
-                                           double* v) {
+// one observation of ba_k_lin_tile: records out, its rows a, b of Jc and
+// residual r (j = its point, ip = its point-major position)
+__device__ __forceinline__ void ba_lin_obs_rows(const BADev& d, const double* __restrict__ theta, int c, long long i,
+                                                int j, int ip, double* a, double* b, double* r) {
   const unsigned long long pst = pol_evict_first();
-  const int j = d.topo.cm_pt[i];
-  const int ip = d.topo.cm_to_pm[i];
-  double r[2], J[BA_JREC], ct, F[BA_FREC + 3];
+  double J[BA_JREC], ct, F[BA_FREC + 3];
   ba_obs_eval(d.bp, d.cams + c, theta + d.bp.off_pts + 3ll * j, d.pix_cm + 2ll * i, r, J, &ct, F);
   fcm_store(d, i, F, pst);   // pinhole: s01, s11 are implied
   gpm_store(d, ip, J + 8);
   *reinterpret_cast<double4*>(d.Rpm + 4ll * ip) = make_double4(r[0], r[1], 0.0, 0.0);
-  double a[8], b[8];
   ba_jc_row(J, 0, a);
   ba_jc_row(J, 1, b);
+}
+// ... and its J^T J / J^T r terms added to v
+__device__ __forceinline__ void ba_lin_obs(const BADev& d, const double* __restrict__ theta, int c, long long i,
+                                           double* v) {
+  double a[8], b[8], r[2];
+  ba_lin_obs_rows(d, theta, c, i, d.topo.cm_pt[i], d.topo.cm_to_pm[i], a, b, r);
   int idx = 0;
 #pragma unroll
   for (int p = 0; p < 8; ++p)
@@ -471,6 +475,107 @@ __global__ void __launch_bounds__(SSFM_TILE, LIN_MINB) ba_k_lin_tile(BADev d, co
     for (int k = 0; k < CAM_V; ++k) smw[k] = v[k];
   }
   __syncthreads();
+  if (threadIdx.x < 64) {
+    double* dst = d.tilebuf + (long long)CAM_V * t0;
+    for (int o = threadIdx.x; o < CAM_V; o += 64) dst[o] = smw[o];
+  } else {
+    for (int k = threadIdx.x - 64; k < CAM_V * (t1 - t0 - 1); k += blockDim.x - 64)
+      d.tilebuf[(long long)CAM_V * (t0 + 1) + k] = 0.0;
+  }
+}
+
+// ba_k_lin_tile with the group's Jc^T Jc on the fp64 tensor cores (DMMA
+// m8n8k4: two observations' rows a, b per C += U^T U step, the rows staged
+// per warp in shared memory; see ba_k_precond_mma): a lane keeps 2
+// accumulators of the 8x8 block instead of 36, so 12 warps per SM instead of
+// 8, and the point indices are requested one round ahead. Deterministic (fixed
+// assignment and order); equal to the scalar sums to rounding.
+#ifndef LIN_MMA
+#define LIN_MMA 1
+#endif
+#define LIN_MMA_THREADS 128
+#ifndef LIN_MMA_MINB
+#define LIN_MMA_MINB 3   // 4: 128 registers, spills
+#endif
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+// C fragments (8x8, two per lane) and u (warp-summed 8-vector) of every warp
+// -> packed 44 in shared memory, summed over warps in warp order into smw
+template <int NW>
+__device__ __forceinline__ void mma_group_sum(double c0, double c1, double (&u)[8], double (*sred)[CAM_V],
+                                              double* smw) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int p = lane >> 2, tig = lane & 3;
+  warp_allreduce<8>(u);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int q = 2 * tig + h;
+    if (p <= q) sred[wid][p * 8 - p * (p - 1) / 2 + (q - p)] = h ? c1 : c0;
+  }
+  if (lane < 8) {
+    double x = u[0];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) x = lane == k ? u[k] : x;
+    sred[wid][36 + lane] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < CAM_V) {
+    double x = sred[0][threadIdx.x];
+    for (int w = 1; w < NW; ++w) x += sred[w][threadIdx.x];
+    smw[threadIdx.x] = x;
+  }
+  __syncthreads();
+}
+__global__ void __launch_bounds__(LIN_MMA_THREADS, LIN_MMA_MINB) ba_k_lin_tile_mma(BADev d, const double* __restrict__ theta) {
+  constexpr int NW = LIN_MMA_THREADS / 32;
+  __shared__ double sU[NW][64][8];   // rows a, b of the warp's 32 observations
+  __shared__ double sred[NW][CAM_V];
+  __shared__ double smw[CAM_V];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int g = blockIdx.x;
+  const int t0 = d.topo.grp_tile[g], t1 = d.topo.grp_tile[g + 1];
+  const int o0 = d.topo.tile_obs[t0], o1 = d.topo.tile_obs[t1];
+  const int c = d.topo.tile_cam[t0];
+  const unsigned long long pst = pol_evict_first();
+  double c0 = 0.0, c1 = 0.0, u[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) u[k] = 0.0;
+  int i = o0 + wid * 32 + lane;
+  int jn = 0, ipn = 0;
+  if (i < o1) { jn = ldg_stream_i(d.topo.cm_pt + i, pst); ipn = ldg_stream_i(d.topo.cm_to_pm + i, pst); }
+  for (int base = o0 + wid * 32; base < o1; base += LIN_MMA_THREADS) {
+    i = base + lane;
+    const int j = jn, ip = ipn;
+    if (i + LIN_MMA_THREADS < o1) {
+      jn = ldg_stream_i(d.topo.cm_pt + i + LIN_MMA_THREADS, pst);
+      ipn = ldg_stream_i(d.topo.cm_to_pm + i + LIN_MMA_THREADS, pst);
+    }
+    double a[8], b[8], r[2] = {0.0, 0.0};
+    if (i < o1) {
+      ba_lin_obs_rows(d, theta, c, i, j, ip, a, b, r);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) { a[k] = 0.0; b[k] = 0.0; }
+    }
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      sU[wid][2 * lane][p] = a[p];
+      sU[wid][2 * lane + 1][p] = b[p];
+      u[p] += a[p] * r[0] + b[p] * r[1];
+    }
+    __syncwarp();
+#pragma unroll 4
+    for (int s = 0; s < 16; ++s) {
+      const double x = sU[wid][4 * s + tig][gid];
+      dmma884(c0, c1, x, x);
+    }
+    __syncwarp();
+  }
+  mma_group_sum<NW>(c0, c1, u, sred, smw);
   if (threadIdx.x < 64) {
     double* dst = d.tilebuf + (long long)CAM_V * t0;
     for (int o = threadIdx.x; o < CAM_V; o += 64) dst[o] = smw[o];
@@ -721,7 +826,11 @@ __global__ void ba_k_ptinv(BADev d, double lam) {
 // frame, a~_r = [D(v)^T (SE)_r ; -(SE)_r ; phi e_r], are reduced over the
 // tile and mapped once per tile by T = diag(Pi, R^T, 1): W = T W~ T^T.
 // accumulates observation i's terms into v (the tile's camera cache cb)
-__device__ __forceinline__ void ba_precond_f(const BADev& d, long long i, const double* cb, double* v) {
+// observation i's camera-frame rows a, b of Jc, K = Jp Cinv_j Jp^T (k00, k01,
+// k11) and Jp y0_j (ty0, ty1); j = the observation's point
+__device__ __forceinline__ void ba_precond_rows(const BADev& d, long long i, int j, const double* cb, double* a,
+                                                double* b, double& k00, double& k01, double& k11, double& ty0,
+                                                double& ty1) {
   double f[6], vv[3];
   fcm_load(d, i, f, vv, pol_evict_first());
   double qh[4];
@@ -729,9 +838,7 @@ __device__ __forceinline__ void ba_precond_f(const BADev& d, long long i, const 
   for (int k = 0; k < 4; ++k) qh[k] = cb[9 + k];
   const double se[2][3] = {{f[0], f[4], -(f[0] * f[1] + f[4] * f[2])},
                            {f[4], f[5], -(f[4] * f[1] + f[5] * f[2])}};
-  double k00, k01, k11, ty0, ty1;
   {
-    const int j = d.topo.cm_pt[i];
     double ci[6], y[3];
 #pragma unroll
     for (int k = 0; k < 6; ++k) ci[k] = d.Cinv[6ll * j + k];
@@ -751,13 +858,16 @@ __device__ __forceinline__ void ba_precond_f(const BADev& d, long long i, const 
     ty0 = jp[0][0] * y[0] + jp[0][1] * y[1] + jp[0][2] * y[2];
     ty1 = jp[1][0] * y[0] + jp[1][1] * y[1] + jp[1][2] * y[2];
   }
-  double a[8], b[8];
   ba_dqt_mul(qh, vv, se[0], a);
   ba_dqt_mul(qh, vv, se[1], b);
 #pragma unroll
   for (int k = 0; k < 3; ++k) { a[4 + k] = -se[0][k]; b[4 + k] = -se[1][k]; }
   a[7] = f[3] * f[1];
   b[7] = f[3] * f[2];
+}
+__device__ __forceinline__ void ba_precond_f(const BADev& d, long long i, const double* cb, double* v) {
+  double a[8], b[8], k00, k01, k11, ty0, ty1;
+  ba_precond_rows(d, i, d.topo.cm_pt[i], cb, a, b, k00, k01, k11, ty0, ty1);
   double ka[8], kb[8];
 #pragma unroll
   for (int p = 0; p < 8; ++p) { ka[p] = k00 * a[p] + k01 * b[p]; kb[p] = k01 * a[p] + k11 * b[p]; }
@@ -888,6 +998,72 @@ __global__ void __launch_bounds__(SSFM_TILE, PRE_MINB) ba_k_precond_grp(BADev d)
     for (int k = 0; k < CAM_V; ++k) smw[k] = v[k];
   }
   __syncthreads();
+  if (threadIdx.x < 64) {
+    double* dst = d.tilebuf + (long long)CAM_V * t0;
+    for (int o = threadIdx.x; o < CAM_V; o += 64) dst[o] = ba_precond_f_entry(cb, smw, o);
+  } else {
+    for (int k = threadIdx.x - 64; k < CAM_V * (t1 - t0 - 1); k += blockDim.x - 64)
+      d.tilebuf[(long long)CAM_V * (t0 + 1) + k] = 0.0;
+  }
+}
+
+// The same group sums on the fp64 tensor cores (DMMA m8n8k4). Per group of
+// two observations the 8x8 term  sum_r a_r ka_r^T  (rows a, b of both
+// observations, ka / kb = K-weighted rows) is one  C += A B  with
+// A = [a1 b1 a2 b2]^T (8x4) and B = [ka1 kb1 ka2 kb2] (4x8): each warp stages
+// its 32 observations' rows in shared memory and issues 16 DMMAs, so a lane
+// keeps 2 accumulators of W~ instead of 36 (and 8 of u~): 16 warps per SM
+// instead of 8, and the gathers of Cinv_j / y0_j are requested one round
+// ahead. Fixed observation -> warp / lane / k-slot assignment and a fixed
+// reduction order: deterministic. The entries differ from the scalar sums by
+// rounding only (a different summation order).
+#ifndef PRE_MMA
+#define PRE_MMA 1
+#endif
+#define PRE_MMA_THREADS 128   // 32 KB of staged rows per CTA
+__global__ void __launch_bounds__(PRE_MMA_THREADS, 4) ba_k_precond_mma(BADev d) {
+  constexpr int NW = PRE_MMA_THREADS / 32;
+  __shared__ double sU[NW][64][8];   // rows a, b of the warp's 32 observations
+  __shared__ double sV[NW][64][8];   // K-weighted rows ka, kb
+  __shared__ double sred[NW][CAM_V];
+  __shared__ double smw[CAM_V];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int g = blockIdx.x;
+  const int t0 = d.topo.grp_tile[g], t1 = d.topo.grp_tile[g + 1];
+  const int o0 = d.topo.tile_obs[t0], o1 = d.topo.tile_obs[t1];
+  const double* cb = reinterpret_cast<const double*>(d.camlin + d.topo.tile_cam[t0]);
+  double c0 = 0.0, c1 = 0.0, u[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) u[k] = 0.0;
+  int i = o0 + wid * 32 + lane;
+  int jn = i < o1 ? ldg_stream_i(d.topo.cm_pt + i, pol_evict_first()) : 0;
+  for (int base = o0 + wid * 32; base < o1; base += PRE_MMA_THREADS) {
+    i = base + lane;
+    const int j = jn;
+    if (i + PRE_MMA_THREADS < o1) jn = ldg_stream_i(d.topo.cm_pt + i + PRE_MMA_THREADS, pol_evict_first());
+    double a[8], b[8];
+    double k00 = 0.0, k01 = 0.0, k11 = 0.0, ty0 = 0.0, ty1 = 0.0;
+    if (i < o1) {
+      ba_precond_rows(d, i, j, cb, a, b, k00, k01, k11, ty0, ty1);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) { a[k] = 0.0; b[k] = 0.0; }
+    }
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      sU[wid][2 * lane][p] = a[p];
+      sU[wid][2 * lane + 1][p] = b[p];
+      sV[wid][2 * lane][p] = k00 * a[p] + k01 * b[p];
+      sV[wid][2 * lane + 1][p] = k01 * a[p] + k11 * b[p];
+      u[p] += a[p] * ty0 + b[p] * ty1;
+    }
+    __syncwarp();
+#pragma unroll 4
+    for (int s = 0; s < 16; ++s) dmma884(c0, c1, sU[wid][4 * s + tig][gid], sV[wid][4 * s + tig][gid]);
+    __syncwarp();
+  }
+  mma_group_sum<NW>(c0, c1, u, sred, smw);
   if (threadIdx.x < 64) {
     double* dst = d.tilebuf + (long long)CAM_V * t0;
     for (int o = threadIdx.x; o < CAM_V; o += 64) dst[o] = ba_precond_f_entry(cb, smw, o);
@@ -1088,6 +1264,16 @@ __global__ void k_cam_wvec(BADev d, const double* __restrict__ v, double* W) {
 // One observation's Jp^T (Jc p_c) in the omega form (point-major index i):
 // the AoS record Gpm[8i..8i+7] = [Jp row 0, Jp row 1, Jf], the camera's W
 // (of p) and the observation's point X at the linearization.
+__device__ __forceinline__ void ba_wobs_math(const double* G, const double* w, const double* X, double* val) {
+  const double u0 = (w[1] * X[2] - w[2] * X[1]) - w[3];
+  const double u1 = (w[2] * X[0] - w[0] * X[2]) - w[4];
+  const double u2 = (w[0] * X[1] - w[1] * X[0]) - w[5];
+  const double t0 = G[0] * u0 + G[1] * u1 + G[2] * u2 + G[6] * w[6];
+  const double t1 = G[3] * u0 + G[4] * u1 + G[5] * u2 + G[7] * w[6];
+  val[0] = G[0] * t0 + G[3] * t1;
+  val[1] = G[1] * t0 + G[4] * t1;
+  val[2] = G[2] * t0 + G[5] * t1;
+}
 template <bool RO>
 __device__ __forceinline__ void ba_wobs(const BADev& d, long long i, int c, const double* __restrict__ W,
                                         const double* X, double* val) {

@@ -76,6 +76,9 @@ constexpr int kCamfUnroll = CAMF_UNROLL;
 #ifndef CAMF_HOIST
 #define CAMF_HOIST 1     // keep the tile camera's R, qh in registers across the loop
 #endif
+#ifndef CAMF_PF
+#define CAMF_PF 1        // point index one round ahead (ba_camera_pass_f)
+#endif
 template <bool RO>
 __device__ __forceinline__ void ba_camera_pass_f(const BADev& d, const double* y, double* tile8) {
   const unsigned long long pstream = pol_evict_first(), pkeep = pol_evict_last();
@@ -96,6 +99,13 @@ __device__ __forceinline__ void ba_camera_pass_f(const BADev& d, const double* y
 #pragma unroll
     for (int k = 0; k < 4; ++k) qh[k] = __ldg(cb + 9 + k);
 #endif
+#if CAMF_PF
+    // the point index one round ahead: a round's y gather is issued together
+    // with its record stream instead of behind the index's DRAM latency
+    // (two rounds ahead: the loop is unrolled by two)
+    int jn = o0 + lane < o1 ? ldg_stream_i(d.topo.cm_pt + o0 + lane, pstream) : 0;
+    int jn2 = o0 + lane + 32 < o1 ? ldg_stream_i(d.topo.cm_pt + o0 + lane + 32, pstream) : 0;
+#endif
 #pragma unroll kCamfUnroll
     for (int i = o0 + lane; i < o1; i += 32) {
 #if !CAMF_HOIST
@@ -108,11 +118,21 @@ __device__ __forceinline__ void ba_camera_pass_f(const BADev& d, const double* y
       for (int k = 0; k < 4; ++k) qh[k] = __ldg(cb + 9 + k);
 #endif
       double f[6], vv[3];
+#if CAMF_PF
+      const int j = jn;
+      double yj[4];
+      if constexpr (RO) ld_v4_ro(y + 4ll * j, yj, pkeep);
+      else ld_v4_hint(y + 4ll * j, yj, pkeep);
+      fcm_load(d, i, f, vv, pstream);
+      jn = jn2;
+      if (i + 64 < o1) jn2 = ldg_stream_i(d.topo.cm_pt + i + 64, pstream);
+#else
       fcm_load(d, i, f, vv, pstream);
       const int j = ldg_stream_i(d.topo.cm_pt + i, pstream);
       double yj[4];
       if constexpr (RO) ld_v4_ro(y + 4ll * j, yj, pkeep);
       else ld_v4_hint(y + 4ll * j, yj, pkeep);
+#endif
       double ry[3];
 #pragma unroll
       for (int r = 0; r < 3; ++r) ry[r] = R[3 * r] * yj[0] + R[3 * r + 1] * yj[1] + R[3 * r + 2] * yj[2];
@@ -250,9 +270,111 @@ __device__ __forceinline__ void ba_point_pass(const BADev& d, const double* v, d
   }
 }
 
-#ifndef PTW_CIEARLY
-#define PTW_CIEARLY 1   // owners load Cinv at the batch start (C5 point pass 0.46 -> 0.45 ms)
+#ifndef PTW_PIPE
+#define PTW_PIPE 1      // index prefetch one round ahead, contiguous batch ranges per warp
 #endif
+#ifndef PTW_CIEARLY
+// owners load Cinv at the batch start (C5 point pass 0.46 -> 0.45 ms without
+// PTW_PIPE; with it the 12 registers spill)
+#define PTW_CIEARLY (!PTW_PIPE)
+#endif
+#if PTW_PIPE
+// P1 in the omega form (ba_wobs): W = the per-camera vector of p (ba_wvec).
+// Streams the 64-byte Jp + Jf record and the camera and point indices per
+// observation, gathers W_c (64 bytes, L2-resident) and X_j (32 bytes).
+//
+// Latency structure. The loads are issued in program order (volatile asm), so
+// a gather whose address comes from an index loaded in the same round puts
+// the index's DRAM latency in front of everything after it. Here each warp
+// owns a contiguous range of batches, so the next round's observation range
+// is known without a load, and its camera / point indices are requested one
+// round ahead. A round then issues the record stream and both gathers at once
+// (their addresses are already in registers): one DRAM latency per round
+// instead of index -> record -> gather. Same per-point summation order and
+// arithmetic as before: the output is bit-identical.
+template <bool RO = false>
+__device__ __forceinline__ void ba_point_pass_w(const BADev& d, const double* W, double* y,
+                                                double (*sm)[SSFM_BATCH][3]) {
+  const unsigned long long pstream = pol_evict_first(), pkeep = pol_evict_last();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nb = d.topo.nb;
+  const int b0 = (int)((long long)nb * gw / warps), b1 = (int)((long long)nb * (gw + 1) / warps);
+  if (b0 >= b1) return;   // warp-uniform
+  int ob0 = d.topo.bat_obs[b0], ob1 = d.topo.bat_obs[b0 + 1], pb0 = d.topo.bat_pt[b0];
+  int cn = 0, jn = 0;
+  if (ob0 + lane < ob1) {
+    cn = ldg_stream_i(d.topo.pm_cam + ob0 + lane, pstream);
+    jn = ldg_stream_i(d.topo.pm_pt + ob0 + lane, pstream);
+  }
+  for (int b = b0; b < b1; ++b) {
+    const int pb1 = d.topo.bat_pt[b + 1];
+    const int nob1 = b + 1 < b1 ? d.topo.bat_obs[b + 2] : ob1;   // end of the next batch
+    const int my_pt = pb0 + lane;
+    const bool own = my_pt < pb1;
+    int ps = 0, pe = 0;
+#if PTW_CIEARLY
+    double ci[6];
+#endif
+    if (own) {
+      ps = d.topo.pt_seg[my_pt]; pe = d.topo.pt_seg[my_pt + 1];
+#if PTW_CIEARLY
+#pragma unroll
+      for (int k = 0; k < 6; ++k) ci[k] = __ldg(d.Cinv + 6ll * my_pt + k);
+#endif
+    }
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int base = ob0; base < ob1; base += SSFM_BATCH) {
+      const int i = base + lane;
+      const int c = cn, j = jn;
+      const bool act = i < ob1;
+      double G[8], w[8], X[4];
+      if (act) gpm_load(d, i, G, pstream);
+      // the next round's indices: this batch's next round or the next batch's first
+      const bool more = base + SSFM_BATCH < ob1;
+      const int ni = more ? i + SSFM_BATCH : ob1 + lane, nend = more ? ob1 : nob1;
+      if (ni < nend) {
+        cn = ldg_stream_i(d.topo.pm_cam + ni, pstream);
+        jn = ldg_stream_i(d.topo.pm_pt + ni, pstream);
+      }
+      double val[3] = {0.0, 0.0, 0.0};
+      if (act) {
+        if constexpr (RO) {
+          ld_v4_ro(W + 8ll * c, w, pkeep);
+          ld_v4_ro(W + 8ll * c + 4, w + 4, pkeep);
+        } else {
+          ld_v4(W + 8ll * c, w);
+          ld_v4(W + 8ll * c + 4, w + 4);
+        }
+        ld_v4_ro(d.Xl + 4ll * j, X, pkeep);
+        ba_wobs_math(G, w, X, val);
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) sm[wib][lane][k] = val[k];
+      __syncwarp();
+      const int a = max(ps, base), e = min(pe, base + SSFM_BATCH);
+      for (int o = a; o < e; ++o) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) acc[k] += sm[wib][o - base][k];
+      }
+      __syncwarp();
+    }
+    if (own) {
+      double w3[3];
+#if !PTW_CIEARLY
+      double ci[6];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) ci[k] = __ldg(d.Cinv + 6ll * my_pt + k);
+#endif
+      sym3_matvec(ci, acc, w3);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) st_hint(y + 4ll * my_pt + k, w3[k], pkeep);
+    }
+    ob0 = ob1; ob1 = nob1; pb0 = pb1;
+  }
+}
+#else
 // P1 in the omega form (ba_wobs): W = the per-camera vector of p (ba_wvec).
 // Streams the 64-byte Jp + Jf record and the camera and point indices per
 // observation (the 16-double record and one index before), gathers W_c (64
@@ -314,6 +436,7 @@ __device__ __forceinline__ void ba_point_pass_w(const BADev& d, const double* W,
     }
   }
 }
+#endif
 
 // P1, software-pipelined: while a warp works on batch b, the Jacobian rows
 // and camera ids of its next batch are already in flight into a second

@@ -528,6 +528,108 @@ __device__ __forceinline__ double grp4_get(double v, int k) {
   return __shfl_sync(SSFM_FULL, v, base + k);
 }
 
+#ifndef GP_PIPE
+#define GP_PIPE 1   // index prefetch one round ahead (as ba_point_pass_w / ba_camera_pass_f)
+#endif
+#if GP_PIPE
+// Each warp owns a contiguous range of point batches, so the next round's
+// observation range is known without a load and its camera indices are
+// requested one round ahead: a round issues its record stream and its camera
+// gather together (one DRAM latency per round instead of index -> gather).
+// Same arithmetic and per-point order as before: bit-identical output.
+__device__ __forceinline__ void gp_point_pass(const GPDev& g, const double* v, double* y,
+                                              double (*sm)[SSFM_BATCH][3]) {
+  const unsigned long long pstream = pol_evict_first();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long Np = g.Npad;
+  const double lam = g.lam;
+  const int nb = g.topo.nb;
+  const int b0 = (int)((long long)nb * gw / warps), b1 = (int)((long long)nb * (gw + 1) / warps);
+  if (b0 >= b1) return;   // warp-uniform
+  int ob0 = g.topo.bat_obs[b0], ob1 = g.topo.bat_obs[b0 + 1], pb0 = g.topo.bat_pt[b0];
+  int cn = ob0 + lane < ob1 ? ldg_stream_i(g.topo.pm_cam + ob0 + lane, pstream) : 0;
+  for (int b = b0; b < b1; ++b) {
+    const int pb1 = g.topo.bat_pt[b + 1];
+    const int nob1 = b + 1 < b1 ? g.topo.bat_obs[b + 2] : ob1;   // end of the next batch
+    const int my_pt = pb0 + lane;
+    int ps = 0, pe = 0;
+    if (my_pt < pb1) { ps = g.topo.pt_seg[my_pt]; pe = g.topo.pt_seg[my_pt + 1]; }
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int base = ob0; base < ob1; base += SSFM_BATCH) {
+      const int i = base + lane;
+      const int c = cn;
+      const bool act = i < ob1;
+      double rec[4], pc[4];
+      if (act) {
+        gp_rec_ld<true>(g.Jpm, Np, i, rec);
+        ld_v4(v + 4ll * c, pc);   // 4 slots per camera: one 32-byte gather
+      }
+      const bool more = base + SSFM_BATCH < ob1;
+      const int ni = more ? i + SSFM_BATCH : ob1 + lane, nend = more ? ob1 : nob1;
+      if (ni < nend) cn = ldg_stream_i(g.topo.pm_cam + ni, pstream);
+      double val[3] = {0.0, 0.0, 0.0};
+      if (act) {
+        const double at = gp_at(g, c, rec[0]);
+        const double inv = gp_inv(lam, rec);
+        gp_u_mul(at, rec[0], inv, rec + 1, pc, val);
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) sm[wib][lane][k] = val[k];
+      __syncwarp();
+      const int a0 = max(ps, base), e = min(pe, base + SSFM_BATCH);
+      for (int o = a0; o < e; ++o) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) acc[k] += sm[wib][o - base][k];
+      }
+      __syncwarp();
+    }
+    if (my_pt < pb1) {
+      double M[6], w[3];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) M[k] = __ldg(g.Minv_pt + 6ll * my_pt + k);
+      sym3_matvec(M, acc, w);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) y[4ll * my_pt + k] = w[k];   // padded: one 32-byte gather
+    }
+    ob0 = ob1; ob1 = nob1; pb0 = pb1;
+  }
+}
+
+__device__ __forceinline__ void gp_camera_pass(const GPDev& g, const double* y, double* tile4,
+                                               double* smred) {
+  // one warp per camera tile, register accumulation, one butterfly; the point
+  // index is requested one round ahead so the y gather leaves with the record
+  (void)smred;
+  const unsigned long long pstream = pol_evict_first();
+  const long long Np = g.Npad;
+  const double lam = g.lam;
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  for (int t = gw; t < g.topo.nt; t += warps) {
+    const int o0 = __ldg(g.topo.tile_obs + t), o1 = __ldg(g.topo.tile_obs + t + 1);
+    const int c = __ldg(g.topo.tile_cam + t);
+    double o[3] = {0.0, 0.0, 0.0};
+    int jn = o0 + lane < o1 ? ldg_stream_i(g.topo.cm_pt + o0 + lane, pstream) : 0;
+    for (int i = o0 + lane; i < o1; i += 32) {
+      const int j = jn;
+      double rec[4], yj[4], u[3];
+      gp_rec_ld<true>(g.Jcm, Np, i, rec);
+      ld_v4(y + 4ll * j, yj);
+      if (i + 32 < o1) jn = ldg_stream_i(g.topo.cm_pt + i + 32, pstream);
+      const double at = gp_at(g, c, rec[0]);
+      const double inv = gp_inv(lam, rec);
+      gp_u_mul(at, rec[0], inv, rec + 1, yj, u);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) o[k] += u[k];
+    }
+    warp_allreduce<3>(o);
+    if (lane < 3) tile4[4ll * t + lane] = lane == 0 ? o[0] : (lane == 1 ? o[1] : o[2]);
+  }
+}
+#else
 __device__ __forceinline__ void gp_point_pass(const GPDev& g, const double* v, double* y,
                                               double (*sm)[SSFM_BATCH][3]) {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -606,6 +708,8 @@ __device__ __forceinline__ void gp_camera_pass(const GPDev& g, const double* y, 
     if (lane < 3) tile4[4ll * t + lane] = lane == 0 ? o[0] : (lane == 1 ? o[1] : o[2]);
   }
 }
+
+#endif
 
 // Fused single pass for GP (the BA version is ba_fused_pass, fused.cuh): y_j
 // for every point of the warp's batch, then each observation's camera term
