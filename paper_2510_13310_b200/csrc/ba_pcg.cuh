@@ -784,8 +784,7 @@ ba_k_pcg(BADev d, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg
     double a = 0.0;
     if constexpr (SL == 0) {
       const int c = s >> 3, k = s & 7;
-      const int t0 = d.topo.cam_tile[c], t1 = d.topo.cam_tile[c + 1];
-      for (int t = t0; t < t1; ++t) a += tile8[8ll * t + k];
+      a = tiles_sum<8>(tile8, k, d.topo.cam_tile[c], d.topo.cam_tile[c + 1]);
     } else {
       for (int gq = 0; gq < ngrp; ++gq) a += fz.gpart[(long long)gq * S + s];
     }

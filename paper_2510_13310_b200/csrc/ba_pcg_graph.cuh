@@ -146,8 +146,7 @@ __global__ void __launch_bounds__(256) k_g_q(BADev d, FusedTopo fz, CGGraphDev g
         acc = comm_peer_load(cm.buf[0] + xoff + s);
         for (int rk = 1; rk < cm.nranks; ++rk) acc += comm_peer_load(cm.buf[rk] + xoff + s);
       } else if (!g.fused) {
-        const int t0 = d.topo.cam_tile[c], t1 = d.topo.cam_tile[c + 1];
-        for (int t = t0; t < t1; ++t) acc += d.tilebuf[8ll * t + k];
+        acc = tiles_sum<8>(d.tilebuf, k, d.topo.cam_tile[c], d.topo.cam_tile[c + 1]);
       } else {
         for (int gq = 0; gq < g.ngrp; ++gq) acc += fz.gpart[(long long)gq * S + s];
       }
@@ -175,7 +174,7 @@ __global__ void __launch_bounds__(256) k_gx_post(BADev d, FusedTopo fz, CGGraphD
     const int c = s >> 3, k = s & 7;
     double a = 0.0;
     if (!g.fused) {
-      for (int t = d.topo.cam_tile[c]; t < d.topo.cam_tile[c + 1]; ++t) a += d.tilebuf[8ll * t + k];
+      a = tiles_sum<8>(d.tilebuf, k, d.topo.cam_tile[c], d.topo.cam_tile[c + 1]);
     } else {
       for (int gq = 0; gq < g.ngrp; ++gq) a += fz.gpart[(long long)gq * S + s];
     }
@@ -359,8 +358,7 @@ k_g_vec(BADev d, FusedTopo fz, CGGraphDev g, CommDev cm, cudaGraphConditionalHan
         acc = comm_peer_load(cm.buf[0] + xoff + s);
         for (int rk = 1; rk < cm.nranks; ++rk) acc += comm_peer_load(cm.buf[rk] + xoff + s);
       } else if (!g.fused) {
-        const int t0 = d.topo.cam_tile[c], t1 = d.topo.cam_tile[c + 1];
-        for (int t = t0; t < t1; ++t) acc += d.tilebuf[8ll * t + k];
+        acc = tiles_sum<8>(d.tilebuf, k, d.topo.cam_tile[c], d.topo.cam_tile[c + 1]);
       } else {
         for (int gq = 0; gq < g.ngrp; ++gq) acc += fz.gpart[(long long)gq * (8 * C) + s];
       }

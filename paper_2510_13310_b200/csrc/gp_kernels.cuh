@@ -856,7 +856,7 @@ gp_k_pcg(GPDev g, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg
       for (int gq = 0; gq < NP; ++gq) a += fz.gpart[(long long)gq * S + s];
     } else {
       const int c = s >> 2, k = s & 3;
-      for (int t = g.topo.cam_tile[c]; t < g.topo.cam_tile[c + 1]; ++t) a += tile4[4ll * t + k];
+      a = tiles_sum<4>(tile4, k, g.topo.cam_tile[c], g.topo.cam_tile[c + 1]);
     }
     return a;
   };

@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256) k_gg_q(GPDev d, CGGraphDev g) {
         const double* B = d.Bp + 6ll * c;
         const double row[3][3] = {{B[0], B[1], B[2]}, {B[1], B[3], B[4]}, {B[2], B[4], B[5]}};
         double acc = 0.0;
-        for (int t = d.topo.cam_tile[c]; t < d.topo.cam_tile[c + 1]; ++t) acc += d.tilebuf[4ll * t + k];
+        acc = tiles_sum<4>(d.tilebuf, k, d.topo.cam_tile[c], d.topo.cam_tile[c + 1]);
         qk = row[k][0] * p0 + row[k][1] * p1 + row[k][2] * p2 - acc;
       }
       if ((d.pinned[c] >> k) & 1) qk = pk;
@@ -166,7 +166,7 @@ k_gg_vec(GPDev d, CGGraphDev g, cudaGraphConditionalHandle hc) {
         const double* B = d.Bp + 6ll * c;
         const double row[3][3] = {{B[0], B[1], B[2]}, {B[1], B[3], B[4]}, {B[2], B[4], B[5]}};
         double acc = 0.0;
-        for (int t = d.topo.cam_tile[c]; t < d.topo.cam_tile[c + 1]; ++t) acc += d.tilebuf[4ll * t + k];
+        acc = tiles_sum<4>(d.tilebuf, k, d.topo.cam_tile[c], d.topo.cam_tile[c + 1]);
         qk = row[k][0] * p0 + row[k][1] * p1 + row[k][2] * p2 - acc;
       }
       if ((d.pinned[c] >> k) & 1) qk = pk;

@@ -179,7 +179,7 @@ struct ssfm_handle {
   int comm_nranks = 1;
   // graph PCG (ba_pcg_graph.cuh): built on first use, reused for every solve
   int graph_state = 0;          // 0 not built, 1 ready, -1 unavailable (persistent kernel)
-  bool mma = true;              // DMMA group sums in linearize / preconditioner (SSFM_MMA=0: scalar)
+  bool mma = false;             // DMMA group sums in linearize / preconditioner (SSFM_MMA=1)
   bool graph_sharded = false;   // the built graph carries the exchange kernels
   bool graph_pending = false;   // a graph solve whose body kernels are not yet counted
   int graph_body_kernels = 0;   // kernels per WHILE-body iteration
@@ -628,9 +628,10 @@ static int setup_ba_pcg(ssfm_handle* h, cudaStream_t st) {
     }
   }
   // tile-group sums of linearize / preconditioner on the fp64 tensor cores
-  // (ba_k_lin_tile_mma, ba_k_precond_mma); SSFM_MMA=0: the scalar kernels
+  // (ba_k_lin_tile_mma, ba_k_precond_mma): opt-in, SSFM_MMA=1. They lost at C5
+  // (8.5 vs 7.4 ms of non-PCG work per LM iteration)
   const char* me = getenv("SSFM_MMA");
-  h->mma = !(me && me[0] == '0');
+  h->mma = me && me[0] == '1';
   const char* ge = getenv("SSFM_PCG_GRAPH");
   // two-pass operator from 250k observations: the graph wins well below C5
   // (3000 cameras / 800k obs: 0.067 vs 0.116 ms per CG iteration)

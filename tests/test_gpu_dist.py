@@ -28,7 +28,18 @@ import paper_2510_13310_b200 as b2
 from paper_2510_13310_b200 import dist as bd
 from paper_2510_13310_b200 import synth
 
-pytestmark = pytest.mark.gpu
+# Opt-in (SSFM_SAME_DEVICE_SHARDS=1): these tests run the shards of one scene
+# as separate kernel launches on ONE GPU whose kernels spin on each other's
+# exchange flags. Nothing guarantees such launches run at the same time: on
+# this driver (580.159, sm_100a) same-GPU ranks that wait on one another have
+# raised Xid 109 (context-switch timeout), and in round 2 a 3-shard
+# fused/graph case stalled here and left the next case hung. The default suite
+# covers the multi-rank path on the CPU (tests/test_dist_cpu.py, gloo world 2)
+# and the single-rank device path; with one GPU per gpurun call the device
+# exchange cannot be exercised safely.
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(os.environ.get("SSFM_SAME_DEVICE_SHARDS") != "1",
+                                 reason="same-GPU ranks that spin on each other (opt-in: SSFM_SAME_DEVICE_SHARDS=1)")]
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
