@@ -484,107 +484,6 @@ __global__ void __launch_bounds__(SSFM_TILE, LIN_MINB) ba_k_lin_tile(BADev d, co
   }
 }
 
-// ba_k_lin_tile with the group's Jc^T Jc on the fp64 tensor cores (DMMA
-// m8n8k4: two observations' rows a, b per C += U^T U step, the rows staged
-// per warp in shared memory; see ba_k_precond_mma): a lane keeps 2
-// accumulators of the 8x8 block instead of 36, so 12 warps per SM instead of
-// 8, and the point indices are requested one round ahead. Deterministic (fixed
-// assignment and order); equal to the scalar sums to rounding.
-#ifndef LIN_MMA
-#define LIN_MMA 1
-#endif
-#define LIN_MMA_THREADS 128
-#ifndef LIN_MMA_MINB
-#define LIN_MMA_MINB 3   // 4: 128 registers, spills
-#endif
-__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
-}
-// C fragments (8x8, two per lane) and u (warp-summed 8-vector) of every warp
-// -> packed 44 in shared memory, summed over warps in warp order into smw
-template <int NW>
-__device__ __forceinline__ void mma_group_sum(double c0, double c1, double (&u)[8], double (*sred)[CAM_V],
-                                              double* smw) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int p = lane >> 2, tig = lane & 3;
-  warp_allreduce<8>(u);
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int q = 2 * tig + h;
-    if (p <= q) sred[wid][p * 8 - p * (p - 1) / 2 + (q - p)] = h ? c1 : c0;
-  }
-  if (lane < 8) {
-    double x = u[0];
-#pragma unroll
-    for (int k = 1; k < 8; ++k) x = lane == k ? u[k] : x;
-    sred[wid][36 + lane] = x;
-  }
-  __syncthreads();
-  if (threadIdx.x < CAM_V) {
-    double x = sred[0][threadIdx.x];
-    for (int w = 1; w < NW; ++w) x += sred[w][threadIdx.x];
-    smw[threadIdx.x] = x;
-  }
-  __syncthreads();
-}
-__global__ void __launch_bounds__(LIN_MMA_THREADS, LIN_MMA_MINB) ba_k_lin_tile_mma(BADev d, const double* __restrict__ theta) {
-  constexpr int NW = LIN_MMA_THREADS / 32;
-  __shared__ double sU[NW][64][8];   // rows a, b of the warp's 32 observations
-  __shared__ double sred[NW][CAM_V];
-  __shared__ double smw[CAM_V];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int gid = lane >> 2, tig = lane & 3;
-  const int g = blockIdx.x;
-  const int t0 = d.topo.grp_tile[g], t1 = d.topo.grp_tile[g + 1];
-  const int o0 = d.topo.tile_obs[t0], o1 = d.topo.tile_obs[t1];
-  const int c = d.topo.tile_cam[t0];
-  const unsigned long long pst = pol_evict_first();
-  double c0 = 0.0, c1 = 0.0, u[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) u[k] = 0.0;
-  int i = o0 + wid * 32 + lane;
-  int jn = 0, ipn = 0;
-  if (i < o1) { jn = ldg_stream_i(d.topo.cm_pt + i, pst); ipn = ldg_stream_i(d.topo.cm_to_pm + i, pst); }
-  for (int base = o0 + wid * 32; base < o1; base += LIN_MMA_THREADS) {
-    i = base + lane;
-    const int j = jn, ip = ipn;
-    if (i + LIN_MMA_THREADS < o1) {
-      jn = ldg_stream_i(d.topo.cm_pt + i + LIN_MMA_THREADS, pst);
-      ipn = ldg_stream_i(d.topo.cm_to_pm + i + LIN_MMA_THREADS, pst);
-    }
-    double a[8], b[8], r[2] = {0.0, 0.0};
-    if (i < o1) {
-      ba_lin_obs_rows(d, theta, c, i, j, ip, a, b, r);
-    } else {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) { a[k] = 0.0; b[k] = 0.0; }
-    }
-#pragma unroll
-    for (int p = 0; p < 8; ++p) {
-      sU[wid][2 * lane][p] = a[p];
-      sU[wid][2 * lane + 1][p] = b[p];
-      u[p] += a[p] * r[0] + b[p] * r[1];
-    }
-    __syncwarp();
-#pragma unroll 4
-    for (int s = 0; s < 16; ++s) {
-      const double x = sU[wid][4 * s + tig][gid];
-      dmma884(c0, c1, x, x);
-    }
-    __syncwarp();
-  }
-  mma_group_sum<NW>(c0, c1, u, sred, smw);
-  if (threadIdx.x < 64) {
-    double* dst = d.tilebuf + (long long)CAM_V * t0;
-    for (int o = threadIdx.x; o < CAM_V; o += 64) dst[o] = smw[o];
-  } else {
-    for (int k = threadIdx.x - 64; k < CAM_V * (t1 - t0 - 1); k += blockDim.x - 64)
-      d.tilebuf[(long long)CAM_V * (t0 + 1) + k] = 0.0;
-  }
-}
-
 __global__ void __launch_bounds__(256) ba_k_lin_points(BADev d, const double* __restrict__ theta,
                                                        double* gpt_norm_part) {
   __shared__ double sm[8][SSFM_BATCH][LIN_V];
@@ -998,72 +897,6 @@ __global__ void __launch_bounds__(SSFM_TILE, PRE_MINB) ba_k_precond_grp(BADev d)
     for (int k = 0; k < CAM_V; ++k) smw[k] = v[k];
   }
   __syncthreads();
-  if (threadIdx.x < 64) {
-    double* dst = d.tilebuf + (long long)CAM_V * t0;
-    for (int o = threadIdx.x; o < CAM_V; o += 64) dst[o] = ba_precond_f_entry(cb, smw, o);
-  } else {
-    for (int k = threadIdx.x - 64; k < CAM_V * (t1 - t0 - 1); k += blockDim.x - 64)
-      d.tilebuf[(long long)CAM_V * (t0 + 1) + k] = 0.0;
-  }
-}
-
-// The same group sums on the fp64 tensor cores (DMMA m8n8k4). Per group of
-// two observations the 8x8 term  sum_r a_r ka_r^T  (rows a, b of both
-// observations, ka / kb = K-weighted rows) is one  C += A B  with
-// A = [a1 b1 a2 b2]^T (8x4) and B = [ka1 kb1 ka2 kb2] (4x8): each warp stages
-// its 32 observations' rows in shared memory and issues 16 DMMAs, so a lane
-// keeps 2 accumulators of W~ instead of 36 (and 8 of u~): 16 warps per SM
-// instead of 8, and the gathers of Cinv_j / y0_j are requested one round
-// ahead. Fixed observation -> warp / lane / k-slot assignment and a fixed
-// reduction order: deterministic. The entries differ from the scalar sums by
-// rounding only (a different summation order).
-#ifndef PRE_MMA
-#define PRE_MMA 1
-#endif
-#define PRE_MMA_THREADS 128   // 32 KB of staged rows per CTA
-__global__ void __launch_bounds__(PRE_MMA_THREADS, 4) ba_k_precond_mma(BADev d) {
-  constexpr int NW = PRE_MMA_THREADS / 32;
-  __shared__ double sU[NW][64][8];   // rows a, b of the warp's 32 observations
-  __shared__ double sV[NW][64][8];   // K-weighted rows ka, kb
-  __shared__ double sred[NW][CAM_V];
-  __shared__ double smw[CAM_V];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int gid = lane >> 2, tig = lane & 3;
-  const int g = blockIdx.x;
-  const int t0 = d.topo.grp_tile[g], t1 = d.topo.grp_tile[g + 1];
-  const int o0 = d.topo.tile_obs[t0], o1 = d.topo.tile_obs[t1];
-  const double* cb = reinterpret_cast<const double*>(d.camlin + d.topo.tile_cam[t0]);
-  double c0 = 0.0, c1 = 0.0, u[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) u[k] = 0.0;
-  int i = o0 + wid * 32 + lane;
-  int jn = i < o1 ? ldg_stream_i(d.topo.cm_pt + i, pol_evict_first()) : 0;
-  for (int base = o0 + wid * 32; base < o1; base += PRE_MMA_THREADS) {
-    i = base + lane;
-    const int j = jn;
-    if (i + PRE_MMA_THREADS < o1) jn = ldg_stream_i(d.topo.cm_pt + i + PRE_MMA_THREADS, pol_evict_first());
-    double a[8], b[8];
-    double k00 = 0.0, k01 = 0.0, k11 = 0.0, ty0 = 0.0, ty1 = 0.0;
-    if (i < o1) {
-      ba_precond_rows(d, i, j, cb, a, b, k00, k01, k11, ty0, ty1);
-    } else {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) { a[k] = 0.0; b[k] = 0.0; }
-    }
-#pragma unroll
-    for (int p = 0; p < 8; ++p) {
-      sU[wid][2 * lane][p] = a[p];
-      sU[wid][2 * lane + 1][p] = b[p];
-      sV[wid][2 * lane][p] = k00 * a[p] + k01 * b[p];
-      sV[wid][2 * lane + 1][p] = k01 * a[p] + k11 * b[p];
-      u[p] += a[p] * ty0 + b[p] * ty1;
-    }
-    __syncwarp();
-#pragma unroll 4
-    for (int s = 0; s < 16; ++s) dmma884(c0, c1, sU[wid][4 * s + tig][gid], sV[wid][4 * s + tig][gid]);
-    __syncwarp();
-  }
-  mma_group_sum<NW>(c0, c1, u, sred, smw);
   if (threadIdx.x < 64) {
     double* dst = d.tilebuf + (long long)CAM_V * t0;
     for (int o = threadIdx.x; o < CAM_V; o += 64) dst[o] = ba_precond_f_entry(cb, smw, o);

@@ -179,7 +179,6 @@ struct ssfm_handle {
   int comm_nranks = 1;
   // graph PCG (ba_pcg_graph.cuh): built on first use, reused for every solve
   int graph_state = 0;          // 0 not built, 1 ready, -1 unavailable (persistent kernel)
-  bool mma = false;             // DMMA group sums in linearize / preconditioner (SSFM_MMA=1)
   bool graph_sharded = false;   // the built graph carries the exchange kernels
   bool graph_pending = false;   // a graph solve whose body kernels are not yet counted
   int graph_body_kernels = 0;   // kernels per WHILE-body iteration
@@ -627,11 +626,6 @@ static int setup_ba_pcg(ssfm_handle* h, cudaStream_t st) {
       if (!(le && le[0] == '0')) DALLOC(d.Rpm, 4ll * d.Npad);
     }
   }
-  // tile-group sums of linearize / preconditioner on the fp64 tensor cores
-  // (ba_k_lin_tile_mma, ba_k_precond_mma): opt-in, SSFM_MMA=1. They lost at C5
-  // (8.5 vs 7.4 ms of non-PCG work per LM iteration)
-  const char* me = getenv("SSFM_MMA");
-  h->mma = me && me[0] == '1';
   const char* ge = getenv("SSFM_PCG_GRAPH");
   // two-pass operator from 250k observations: the graph wins well below C5
   // (3000 cameras / 800k obs: 0.067 vs 0.116 ms per CG iteration)
@@ -1141,10 +1135,7 @@ static int launch_linearize(ssfm_handle* h, const double* theta, double* r_out, 
     if (d.camlin) CU(copy_async(reinterpret_cast<double*>(d.camlin), reinterpret_cast<const double*>(d.cams),
                                 (long long)(sizeof(BACam) / 8) * d.bp.C, st));
     if (d.Rpm && !r_out && !J_out) {   // each observation evaluated once (camera tiles), then point sums
-      if (d.topo.nt) {   // tile groups
-        if (LIN_MMA && h->mma) ba_k_lin_tile_mma<<<d.topo.ng, LIN_MMA_THREADS, 0, st>>>(d, theta);
-        else ba_k_lin_tile<<<d.topo.ng, SSFM_TILE, 0, st>>>(d, theta);
-      }
+      if (d.topo.nt) ba_k_lin_tile<<<d.topo.ng, SSFM_TILE, 0, st>>>(d, theta);   // tile groups
       ba_k_lin_points<<<h->lin_blocks, 256, 0, st>>>(d, theta, h->red);
     } else {
       ba_k_linearize<<<h->lin_blocks, 256, 0, st>>>(d, theta, r_out, J_out, h->red);
@@ -1520,7 +1511,6 @@ static int launch_solve_pre(ssfm_handle* h, double lam, cudaStream_t st) {
     ba_k_ptinv<<<nblk(d.bp.P, 256), 256, 0, st>>>(d, lam);
     if (d.topo.nt) {
       if (d.Jcm) ba_k_precond<<<d.topo.nt, SSFM_TILE, 0, st>>>(d);
-      else if (PRE_MMA && h->mma) ba_k_precond_mma<<<d.topo.ng, PRE_MMA_THREADS, 0, st>>>(d);   // tile groups, DMMA
       else ba_k_precond_grp<<<d.topo.ng, SSFM_TILE, 0, st>>>(d);   // factored records: tile groups
     }
     const double* cs = nullptr;
