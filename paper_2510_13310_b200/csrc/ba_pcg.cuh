@@ -177,18 +177,10 @@ __device__ __forceinline__ void ba_camera_pass_f(const BADev& d, const double* y
 #ifndef PTP_PIPE
 #define PTP_PIPE 0       // software-pipelined point pass (ba_point_pass_pipe)
 #endif
-#ifndef PTW_ASYNC
-#define PTW_ASYNC 0      // omega-form point pass with cp.async staging (ba_point_pass_async)
-#endif
 #if PTP_PIPE
 #define PTP_THREADS 128
 #ifndef PTP_MINB
 #define PTP_MINB 6
-#endif
-#elif PTW_ASYNC
-#define PTP_THREADS 128
-#ifndef PTP_MINB
-#define PTP_MINB 4
 #endif
 #else
 #ifndef PTP_THREADS
@@ -281,6 +273,9 @@ __device__ __forceinline__ void ba_point_pass(const BADev& d, const double* v, d
 #ifndef PTW_PIPE
 #define PTW_PIPE 1      // index prefetch one round ahead, contiguous batch ranges per warp
 #endif
+#ifndef PTW_SHFL
+#define PTW_SHFL 0      // warp-shuffle segmented scan instead of the owners' serial shared-memory sums
+#endif
 #ifndef PTW_CIEARLY
 // owners load Cinv at the batch start (C5 point pass 0.46 -> 0.45 ms without
 // PTW_PIPE; with it the 12 registers spill)
@@ -358,15 +353,42 @@ __device__ __forceinline__ void ba_point_pass_w(const BADev& d, const double* W,
         ld_v4_ro(d.Xl + 4ll * j, X, pkeep);
         ba_wobs_math(G, w, X, val);
       }
+      const int a = max(ps, base), e = min(pe, base + SSFM_BATCH);
+#if PTW_SHFL
+      // segmented inclusive scan over the round's lanes (segments = runs of
+      // one point; the idle tail lanes form their own run), then each owner
+      // takes its run's last lane: no shared memory, all lanes busy
+      {
+        const int jj = act ? j : -1;
+        const int jprev = __shfl_up_sync(SSFM_FULL, jj, 1);
+        const unsigned heads = __ballot_sync(SSFM_FULL, lane == 0 || jj != jprev);
+        const unsigned upto = lane == 31 ? SSFM_FULL : ((2u << lane) - 1u);
+        const int s0 = 31 - __clz(heads & upto);
+#pragma unroll
+        for (int dl = 1; dl < 32; dl <<= 1) {
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const double t = __shfl_up_sync(SSFM_FULL, val[k], dl);
+            if (lane - dl >= s0) val[k] += t;
+          }
+        }
+        const int src = a < e ? e - 1 - base : 0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const double t = __shfl_sync(SSFM_FULL, val[k], src);
+          if (a < e) acc[k] += t;
+        }
+      }
+#else
 #pragma unroll
       for (int k = 0; k < 3; ++k) sm[wib][lane][k] = val[k];
       __syncwarp();
-      const int a = max(ps, base), e = min(pe, base + SSFM_BATCH);
       for (int o = a; o < e; ++o) {
 #pragma unroll
         for (int k = 0; k < 3; ++k) acc[k] += sm[wib][o - base][k];
       }
       __syncwarp();
+#endif
     }
     if (own) {
       double w3[3];
@@ -443,148 +465,6 @@ __device__ __forceinline__ void ba_point_pass_w(const BADev& d, const double* W,
       for (int k = 0; k < 3; ++k) st_hint(y + 4ll * my_pt + k, w[k], pkeep);
     }
   }
-}
-#endif
-
-#if PTW_ASYNC
-// P1 in the omega form with every operand of a round staged in shared memory
-// by cp.async one round ahead: while a warp reduces round r, the Gpm records,
-// W_c and X_j of round r + 1 are in flight (no registers held), and the
-// camera / point indices of round r + 2 are loading into registers. The
-// per-round critical path is then the shared-memory reads, the arithmetic and
-// the segmented reduction; the DRAM and L2 latencies overlap the previous
-// round. Each lane stages and reads only its own operands (no cross-lane
-// hazard); 22 doubles per lane per stage (176 bytes: conflict-free 16-byte
-// reads), 2 stages, 4 warps per CTA. Same arithmetic and per-point order as
-// ba_point_pass_w: bit-identical output.
-#define PTA_LS 22
-struct PtaPos {
-  int base, end, b;
-};
-__device__ __forceinline__ void cp_async16(void* s, const void* g, unsigned long long pol) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(sa), "l"(g), "l"(pol) : "memory");
-}
-template <bool RO>
-__device__ __forceinline__ void ba_point_pass_async(const BADev& d, const double* W, double* y,
-                                                    double (*stg)[2][32][PTA_LS], double (*sm)[SSFM_BATCH][3]) {
-  const unsigned long long pstream = pol_evict_first(), pkeep = pol_evict_last();
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nb = d.topo.nb;
-  const int b0 = (int)((long long)nb * gw / warps), b1 = (int)((long long)nb * (gw + 1) / warps);
-  if (b0 >= b1) return;   // warp-uniform
-  const int* bo = d.topo.bat_obs;
-  const int* bpt = d.topo.bat_pt;
-  // producer: the round whose indices load next, and the end of its next batch
-  PtaPos pp{bo[b0], bo[b0 + 1], b0};
-  int pfe = b0 + 1 < b1 ? bo[b0 + 2] : 0;
-  auto padv = [&]() {
-    if (pp.b >= b1) return;
-    if (pp.base + SSFM_BATCH < pp.end) { pp.base += SSFM_BATCH; return; }
-    ++pp.b;
-    pp.base = pp.end;
-    pp.end = pfe;
-    if (pp.b + 1 < b1) pfe = bo[pp.b + 2];
-  };
-  auto ld_idx = [&](int& c, int& j) {
-    const int i = pp.base + lane;
-    if (pp.b < b1 && i < pp.end) {
-      c = ldg_stream_i(d.topo.pm_cam + i, pstream);
-      j = ldg_stream_i(d.topo.pm_pt + i, pstream);
-    }
-  };
-  auto issue = [&](const PtaPos& q, int c, int j, int sidx) {
-    const int i = q.base + lane;
-    if (q.b < b1 && i < q.end) {
-      double* dst = &stg[wib][sidx][lane][0];
-      const double* g = d.Gpm + 8ll * i;
-      const double* w = W + 8ll * c;
-      const double* x = d.Xl + 4ll * j;
-#pragma unroll
-      for (int k = 0; k < 8; k += 2) cp_async16(dst + k, g + k, pstream);
-#pragma unroll
-      for (int k = 0; k < 8; k += 2) cp_async16(dst + 8 + k, w + k, pkeep);
-      cp_async16(dst + 16, x, pkeep);
-      cp_async16(dst + 18, x + 2, pkeep);
-    }
-    cp_commit();
-  };
-  int c = 0, j = 0;
-  ld_idx(c, j);
-  PtaPos cur = pp;
-  issue(cur, c, j, 0);
-  padv();
-  PtaPos nx = pp;
-  ld_idx(c, j);
-  int par = 0;
-  // consumer: the current batch's owners (one lane per point) and the next
-  // batch's point range end
-  int cb = b0, pb0 = bpt[b0], pb1 = bpt[b0 + 1];
-  int npb1 = b0 + 1 < b1 ? bpt[b0 + 2] : 0;
-  int my_pt = pb0 + lane;
-  bool own = my_pt < pb1;
-  int ps = 0, pe = 0;
-  double ci[6];
-  if (own) {
-    ps = d.topo.pt_seg[my_pt]; pe = d.topo.pt_seg[my_pt + 1];
-#pragma unroll
-    for (int k = 0; k < 6; ++k) ci[k] = __ldg(d.Cinv + 6ll * my_pt + k);
-  }
-  double acc[3] = {0.0, 0.0, 0.0};
-  while (cur.b < b1) {
-    issue(nx, c, j, par ^ 1);   // the next round's operands (its indices loaded a round ago)
-    padv();
-    const PtaPos nn = pp;
-    ld_idx(c, j);               // the round after it
-    cp_wait<1>();               // this lane's operands of the current round
-    double val[3] = {0.0, 0.0, 0.0};
-    if (cur.base + lane < cur.end) {
-      const double* sv = &stg[wib][par][lane][0];
-      double G[8], w[8], X[4];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) { G[k] = sv[k]; w[k] = sv[8 + k]; }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) X[k] = sv[16 + k];
-      ba_wobs_math(G, w, X, val);
-    }
-#pragma unroll
-    for (int k = 0; k < 3; ++k) sm[wib][lane][k] = val[k];
-    __syncwarp();
-    const int a = max(ps, cur.base), e = min(pe, cur.base + SSFM_BATCH);
-    for (int o = a; o < e; ++o) {
-#pragma unroll
-      for (int k = 0; k < 3; ++k) acc[k] += sm[wib][o - cur.base][k];
-    }
-    __syncwarp();
-    if (cur.base + SSFM_BATCH >= cur.end) {   // the batch's last round
-      if (own) {
-        double w3[3];
-        sym3_matvec(ci, acc, w3);
-#pragma unroll
-        for (int k = 0; k < 3; ++k) st_hint(y + 4ll * my_pt + k, w3[k], pkeep);
-      }
-      if (++cb < b1) {
-        pb0 = pb1;
-        pb1 = npb1;
-        if (cb + 1 < b1) npb1 = bpt[cb + 2];
-        my_pt = pb0 + lane;
-        own = my_pt < pb1;
-        if (own) {
-          ps = d.topo.pt_seg[my_pt]; pe = d.topo.pt_seg[my_pt + 1];
-#pragma unroll
-          for (int k = 0; k < 6; ++k) ci[k] = __ldg(d.Cinv + 6ll * my_pt + k);
-        }
-#pragma unroll
-        for (int k = 0; k < 3; ++k) acc[k] = 0.0;
-      }
-    }
-    cur = nx;
-    nx = nn;
-    par ^= 1;
-  }
-  cp_wait<0>();
 }
 #endif
 
@@ -1176,10 +1056,6 @@ ba_k_pcg(BADev d, FusedTopo fz, CommDev cm, double lam, int max_iters, double cg
 // kernels (per-pass timing and roofline, ssfm_bench_operator).
 __global__ void __launch_bounds__(PTP_THREADS, PTP_MINB) k_op_point(BADev d, const double* v, double* y) {
   __shared__ double smp[PTP_THREADS / 32][SSFM_BATCH][3];
-#if PTW_ASYNC
-  __shared__ double stg[PTP_THREADS / 32][2][32][PTA_LS];
-  if (d.Gpm) { ba_point_pass_async<true>(d, d.Wc, y, stg, smp); return; }
-#endif
   if (d.Gpm) { ba_point_pass_w<true>(d, d.Wc, y, smp); return; }   // W of v: k_cam_wvec first
 #if PTP_PIPE
   __shared__ PtpStage stg[PTP_THREADS / 32][2];

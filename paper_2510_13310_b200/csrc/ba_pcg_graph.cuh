@@ -87,10 +87,6 @@ __global__ void k_g_init2(Dev d, CGGraphDev g, int nblk) {
 __global__ void __launch_bounds__(PTP_THREADS, PTP_MINB) k_g_point(BADev d, CGGraphDev g) {
   if (*(volatile int*)(g.ic + 3)) return;
   __shared__ double smp[PTP_THREADS / 32][SSFM_BATCH][3];
-#if PTW_ASYNC
-  __shared__ double stg[PTP_THREADS / 32][2][32][PTA_LS];
-  if (d.Gpm) { ba_point_pass_async<true>(d, d.Wc, d.yv, stg, smp); return; }
-#endif
   if (d.Gpm) { ba_point_pass_w<true>(d, d.Wc, d.yv, smp); return; }   // W (of p) is constant here
 #if PTP_PIPE
   __shared__ PtpStage stg[PTP_THREADS / 32][2];
