@@ -273,9 +273,6 @@ __device__ __forceinline__ void ba_point_pass(const BADev& d, const double* v, d
 #ifndef PTW_PIPE
 #define PTW_PIPE 1      // index prefetch one round ahead, contiguous batch ranges per warp
 #endif
-#ifndef PTW_SHFL
-#define PTW_SHFL 0      // warp-shuffle segmented scan instead of the owners' serial shared-memory sums
-#endif
 #ifndef PTW_CIEARLY
 // owners load Cinv at the batch start (C5 point pass 0.46 -> 0.45 ms without
 // PTW_PIPE; with it the 12 registers spill)
@@ -354,32 +351,6 @@ __device__ __forceinline__ void ba_point_pass_w(const BADev& d, const double* W,
         ba_wobs_math(G, w, X, val);
       }
       const int a = max(ps, base), e = min(pe, base + SSFM_BATCH);
-#if PTW_SHFL
-      // segmented inclusive scan over the round's lanes (segments = runs of
-      // one point; the idle tail lanes form their own run), then each owner
-      // takes its run's last lane: no shared memory, all lanes busy
-      {
-        const int jj = act ? j : -1;
-        const int jprev = __shfl_up_sync(SSFM_FULL, jj, 1);
-        const unsigned heads = __ballot_sync(SSFM_FULL, lane == 0 || jj != jprev);
-        const unsigned upto = lane == 31 ? SSFM_FULL : ((2u << lane) - 1u);
-        const int s0 = 31 - __clz(heads & upto);
-#pragma unroll
-        for (int dl = 1; dl < 32; dl <<= 1) {
-#pragma unroll
-          for (int k = 0; k < 3; ++k) {
-            const double t = __shfl_up_sync(SSFM_FULL, val[k], dl);
-            if (lane - dl >= s0) val[k] += t;
-          }
-        }
-        const int src = a < e ? e - 1 - base : 0;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          const double t = __shfl_sync(SSFM_FULL, val[k], src);
-          if (a < e) acc[k] += t;
-        }
-      }
-#else
 #pragma unroll
       for (int k = 0; k < 3; ++k) sm[wib][lane][k] = val[k];
       __syncwarp();
@@ -388,7 +359,6 @@ __device__ __forceinline__ void ba_point_pass_w(const BADev& d, const double* W,
         for (int k = 0; k < 3; ++k) acc[k] += sm[wib][o - base][k];
       }
       __syncwarp();
-#endif
     }
     if (own) {
       double w3[3];
