@@ -427,6 +427,9 @@ __device__ __forceinline__ double ba_precond_f_entry(const double* cb, const dou
 #ifndef LIN_MINB
 #define LIN_MINB 1
 #endif
+#ifndef LIN_PF
+#define LIN_PF 1   // ba_k_lin_tile / ba_k_precond_grp: point indices one step ahead
+#endif
 // one observation of ba_k_lin_tile: records out, its rows a, b of Jc and
 // residual r (j = its point, ip = its point-major position)
 __device__ __forceinline__ void ba_lin_obs_rows(const BADev& d, const double* __restrict__ theta, int c, long long i,
@@ -442,9 +445,9 @@ __device__ __forceinline__ void ba_lin_obs_rows(const BADev& d, const double* __
 }
 // ... and its J^T J / J^T r terms added to v
 __device__ __forceinline__ void ba_lin_obs(const BADev& d, const double* __restrict__ theta, int c, long long i,
-                                           double* v) {
+                                           int j, int ip, double* v) {
   double a[8], b[8], r[2];
-  ba_lin_obs_rows(d, theta, c, i, d.topo.cm_pt[i], d.topo.cm_to_pm[i], a, b, r);
+  ba_lin_obs_rows(d, theta, c, i, j, ip, a, b, r);
   int idx = 0;
 #pragma unroll
   for (int p = 0; p < 8; ++p)
@@ -468,7 +471,24 @@ __global__ void __launch_bounds__(SSFM_TILE, LIN_MINB) ba_k_lin_tile(BADev d, co
   double v[CAM_V];
 #pragma unroll
   for (int k = 0; k < CAM_V; ++k) v[k] = 0.0;
-  for (int i = o0 + threadIdx.x; i < o1; i += blockDim.x) ba_lin_obs(d, theta, c, i, v);
+#if LIN_PF   // the next observation's point index and point-major position one step ahead
+  const unsigned long long pst = pol_evict_first();
+  int jn = 0, ipn = 0;
+  if (o0 + (int)threadIdx.x < o1) {
+    jn = ldg_stream_i(d.topo.cm_pt + o0 + threadIdx.x, pst);
+    ipn = ldg_stream_i(d.topo.cm_to_pm + o0 + threadIdx.x, pst);
+  }
+  for (int i = o0 + threadIdx.x; i < o1; i += blockDim.x) {
+    const int j = jn, ip = ipn;
+    if (i + (int)blockDim.x < o1) {
+      jn = ldg_stream_i(d.topo.cm_pt + i + blockDim.x, pst);
+      ipn = ldg_stream_i(d.topo.cm_to_pm + i + blockDim.x, pst);
+    }
+    ba_lin_obs(d, theta, c, i, j, ip, v);
+  }
+#else
+  for (int i = o0 + threadIdx.x; i < o1; i += blockDim.x) ba_lin_obs(d, theta, c, i, d.topo.cm_pt[i], d.topo.cm_to_pm[i], v);
+#endif
   block_reduce<CAM_V>(v, sm);
   if (threadIdx.x == 0) {
 #pragma unroll
@@ -764,9 +784,9 @@ __device__ __forceinline__ void ba_precond_rows(const BADev& d, long long i, int
   a[7] = f[3] * f[1];
   b[7] = f[3] * f[2];
 }
-__device__ __forceinline__ void ba_precond_f(const BADev& d, long long i, const double* cb, double* v) {
+__device__ __forceinline__ void ba_precond_f(const BADev& d, long long i, int j, const double* cb, double* v) {
   double a[8], b[8], k00, k01, k11, ty0, ty1;
-  ba_precond_rows(d, i, d.topo.cm_pt[i], cb, a, b, k00, k01, k11, ty0, ty1);
+  ba_precond_rows(d, i, j, cb, a, b, k00, k01, k11, ty0, ty1);
   double ka[8], kb[8];
 #pragma unroll
   for (int p = 0; p < 8; ++p) { ka[p] = k00 * a[p] + k01 * b[p]; kb[p] = k01 * a[p] + k11 * b[p]; }
@@ -890,7 +910,17 @@ __global__ void __launch_bounds__(SSFM_TILE, PRE_MINB) ba_k_precond_grp(BADev d)
   double v[CAM_V];
 #pragma unroll
   for (int k = 0; k < CAM_V; ++k) v[k] = 0.0;
-  for (int i = o0 + threadIdx.x; i < o1; i += blockDim.x) ba_precond_f(d, i, cb, v);
+#if LIN_PF
+  const unsigned long long pst = pol_evict_first();
+  int jn = o0 + (int)threadIdx.x < o1 ? ldg_stream_i(d.topo.cm_pt + o0 + threadIdx.x, pst) : 0;
+  for (int i = o0 + threadIdx.x; i < o1; i += blockDim.x) {
+    const int j = jn;
+    if (i + (int)blockDim.x < o1) jn = ldg_stream_i(d.topo.cm_pt + i + blockDim.x, pst);
+    ba_precond_f(d, i, j, cb, v);
+  }
+#else
+  for (int i = o0 + threadIdx.x; i < o1; i += blockDim.x) ba_precond_f(d, i, d.topo.cm_pt[i], cb, v);
+#endif
   block_reduce<CAM_V>(v, sm);
   if (threadIdx.x == 0) {
 #pragma unroll

@@ -77,7 +77,10 @@ constexpr int kCamfUnroll = CAMF_UNROLL;
 #define CAMF_HOIST 1     // keep the tile camera's R, qh in registers across the loop
 #endif
 #ifndef CAMF_PF
-#define CAMF_PF 1        // point index one round ahead (ba_camera_pass_f)
+#define CAMF_PF 1        // point indices CAMF_PFD rounds ahead (ba_camera_pass_f)
+#endif
+#ifndef CAMF_PFD
+#define CAMF_PFD 2
 #endif
 template <bool RO>
 __device__ __forceinline__ void ba_camera_pass_f(const BADev& d, const double* y, double* tile8) {
@@ -102,9 +105,10 @@ __device__ __forceinline__ void ba_camera_pass_f(const BADev& d, const double* y
 #if CAMF_PF
     // the point index one round ahead: a round's y gather is issued together
     // with its record stream instead of behind the index's DRAM latency
-    // (two rounds ahead: the loop is unrolled by two)
-    int jn = o0 + lane < o1 ? ldg_stream_i(d.topo.cm_pt + o0 + lane, pstream) : 0;
-    int jn2 = o0 + lane + 32 < o1 ? ldg_stream_i(d.topo.cm_pt + o0 + lane + 32, pstream) : 0;
+    // (CAMF_PFD rounds ahead: the loop is unrolled by two)
+    int jq[CAMF_PFD];
+#pragma unroll
+    for (int q = 0; q < CAMF_PFD; ++q) jq[q] = o0 + lane + 32 * q < o1 ? ldg_stream_i(d.topo.cm_pt + o0 + lane + 32 * q, pstream) : 0;
 #endif
 #pragma unroll kCamfUnroll
     for (int i = o0 + lane; i < o1; i += 32) {
@@ -119,13 +123,14 @@ __device__ __forceinline__ void ba_camera_pass_f(const BADev& d, const double* y
 #endif
       double f[6], vv[3];
 #if CAMF_PF
-      const int j = jn;
+      const int j = jq[0];
       double yj[4];
       if constexpr (RO) ld_v4_ro(y + 4ll * j, yj, pkeep);
       else ld_v4_hint(y + 4ll * j, yj, pkeep);
       fcm_load(d, i, f, vv, pstream);
-      jn = jn2;
-      if (i + 64 < o1) jn2 = ldg_stream_i(d.topo.cm_pt + i + 64, pstream);
+#pragma unroll
+      for (int q = 0; q + 1 < CAMF_PFD; ++q) jq[q] = jq[q + 1];
+      if (i + 32 * CAMF_PFD < o1) jq[CAMF_PFD - 1] = ldg_stream_i(d.topo.cm_pt + i + 32 * CAMF_PFD, pstream);
 #else
       fcm_load(d, i, f, vv, pstream);
       const int j = ldg_stream_i(d.topo.cm_pt + i, pstream);

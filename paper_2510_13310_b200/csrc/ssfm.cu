@@ -1309,6 +1309,7 @@ static void capture_ba_pcg_body(ssfm_handle* h, cudaStream_t cs, cudaGraphCondit
   const char* gv = getenv("SSFM_GVEC");
   const bool cluster = !(gv && gv[0] == '0');
   if (cluster) {
+    if (GV_CL > 8) cudaFuncSetAttribute((const void*)k_g_vec, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     k_g_vec<<<GV_CL, GV_THREADS, 0, cs>>>(d, h->fz, g, h->cm, hc);
   } else {
     k_g_q<<<CGV_BLOCKS, 256, 0, cs>>>(d, h->fz, g, h->cm);
@@ -1382,6 +1383,7 @@ static void capture_gp_pcg_body(ssfm_handle* h, cudaStream_t cs, cudaGraphCondit
   const char* gv = getenv("SSFM_GVEC");
   const bool cluster = !(gv && gv[0] == '0');
   if (cluster) {   // the vector phases as one thread-block cluster kernel
+    if (GV_CL > 8) cudaFuncSetAttribute((const void*)k_gg_vec, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     k_gg_vec<<<GV_CL, GV_THREADS, 0, cs>>>(d, g, hc);
   } else {
     k_gg_q<<<CGV_BLOCKS, 256, 0, cs>>>(d, g);
