@@ -80,7 +80,7 @@ constexpr int kCamfUnroll = CAMF_UNROLL;
 #define CAMF_PF 1        // point indices CAMF_PFD rounds ahead (ba_camera_pass_f)
 #endif
 #ifndef CAMF_PFD
-#define CAMF_PFD 2
+#define CAMF_PFD 4        // C5 camera pass 0.259 -> 0.252 ms (2 and 3 equal)
 #endif
 template <bool RO>
 __device__ __forceinline__ void ba_camera_pass_f(const BADev& d, const double* y, double* tile8) {
