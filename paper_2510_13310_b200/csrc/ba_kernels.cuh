@@ -457,17 +457,121 @@ __device__ __forceinline__ void ba_lin_obs(const BADev& d, const double* __restr
   for (int p = 0; p < 8; ++p) v[36 + p] += a[p] * r[0] + b[p] * r[1];
 }
 
+// ---------------------------------------------------------------------------
+// Warp transpose-reduction of the 44 per-observation terms of a camera tile
+// group (36 upper entries of an 8x8 block + an 8-vector), for the tile-group
+// kernels of linearize and the preconditioner (LIN_TR). Each lane evaluates
+// its observation's terms on demand (prod(k)); a halving butterfly leaves lane
+// l with the warp sum of term l (terms 0..31) and lanes 2m, 2m+1 with the sum
+// of term 32 + m: 47 shuffles per 32 observations, and 2 accumulators per lane
+// across the loop instead of 44 (the scalar kernels hold 44 and run at 232 /
+// 196 registers, 8 warps per SM). Fixed order: deterministic.
+// ---------------------------------------------------------------------------
+#ifndef LIN_TR
+#define LIN_TR 0
+#endif
+__device__ __forceinline__ void warp_tr44_add(const double (&t)[CAM_V], double& acc1, double& acc2) {
+  const int lane = threadIdx.x & 31;
+  {   // terms 0..31
+    double x[16];
+    const bool h4 = lane & 16;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      const double lo = t[m], hi = t[m + 16];
+      x[m] = (h4 ? hi : lo) + __shfl_xor_sync(SSFM_FULL, h4 ? lo : hi, 16);
+    }
+#pragma unroll
+    for (int w = 8, o = 8; w >= 1; w >>= 1, o >>= 1) {
+      const bool hb = lane & o;
+#pragma unroll
+      for (int m = 0; m < w; ++m) {
+        const double lo = x[m], hi = x[m + w];
+        x[m] = (hb ? hi : lo) + __shfl_xor_sync(SSFM_FULL, hb ? lo : hi, o);
+      }
+    }
+    acc1 += x[0];
+  }
+  {   // terms 32..43 (padded to 16)
+    double x[8];
+    const bool h4 = lane & 16;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const double lo = t[32 + m], hi = 40 + m < CAM_V ? t[40 + m] : 0.0;
+      x[m] = (h4 ? hi : lo) + __shfl_xor_sync(SSFM_FULL, h4 ? lo : hi, 16);
+    }
+#pragma unroll
+    for (int w = 4, o = 8; w >= 1; w >>= 1, o >>= 1) {
+      const bool hb = lane & o;
+#pragma unroll
+      for (int m = 0; m < w; ++m) {
+        const double lo = x[m], hi = x[m + w];
+        x[m] = (hb ? hi : lo) + __shfl_xor_sync(SSFM_FULL, hb ? lo : hi, o);
+      }
+    }
+    acc2 += x[0] + __shfl_xor_sync(SSFM_FULL, x[0], 1);
+  }
+}
+// per-lane accumulators of every warp -> the 44 group sums (warp order) in smw
+__device__ __forceinline__ void tr44_block_sum(double acc1, double acc2, double (*sred)[48], double* smw) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  sred[wid][lane] = acc1;
+  if (!(lane & 1)) sred[wid][32 + (lane >> 1)] = acc2;
+  __syncthreads();
+  if (threadIdx.x < CAM_V) {
+    double x = sred[0][threadIdx.x];
+    for (int w = 1; w < nw; ++w) x += sred[w][threadIdx.x];
+    smw[threadIdx.x] = x;
+  }
+  __syncthreads();
+}
+
 // per tile group (topo.grp_tile: up to SSFM_GRP tiles of one camera; the
 // camera is uniform, so no per-observation camera gather): every observation
 // evaluated once; its records written; the group's J^T J / J^T r reduced
 // once into its first tile's slot (the other tiles' slots zero)
 __global__ void __launch_bounds__(SSFM_TILE, LIN_MINB) ba_k_lin_tile(BADev d, const double* __restrict__ theta) {
-  __shared__ double sm[(SSFM_TILE / 32) * CAM_V];
   __shared__ double smw[CAM_V];
   const int g = blockIdx.x;
   const int t0 = d.topo.grp_tile[g], t1 = d.topo.grp_tile[g + 1];
   const int o0 = d.topo.tile_obs[t0], o1 = d.topo.tile_obs[t1];
   const int c = d.topo.tile_cam[t0];
+#if LIN_TR
+  __shared__ double sred[SSFM_TILE / 32][48];
+  const unsigned long long pst = pol_evict_first();
+  const int lane = threadIdx.x & 31, wbase = o0 + (int)(threadIdx.x & ~31u);
+  double acc1 = 0.0, acc2 = 0.0;
+  int jn = 0, ipn = 0;
+  if (wbase + lane < o1) {
+    jn = ldg_stream_i(d.topo.cm_pt + wbase + lane, pst);
+    ipn = ldg_stream_i(d.topo.cm_to_pm + wbase + lane, pst);
+  }
+  for (int base = wbase; base < o1; base += blockDim.x) {   // warp-uniform
+    const int i = base + lane;
+    const int j = jn, ip = ipn;
+    if (i + (int)blockDim.x < o1) {
+      jn = ldg_stream_i(d.topo.cm_pt + i + blockDim.x, pst);
+      ipn = ldg_stream_i(d.topo.cm_to_pm + i + blockDim.x, pst);
+    }
+    double a[8], b[8], r[2] = {0.0, 0.0};
+    if (i < o1) {
+      ba_lin_obs_rows(d, theta, c, i, j, ip, a, b, r);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) { a[k] = 0.0; b[k] = 0.0; }
+    }
+    double t[CAM_V];
+    int idx = 0;
+#pragma unroll
+    for (int p = 0; p < 8; ++p)
+#pragma unroll
+      for (int q = p; q < 8; ++q) t[idx++] = a[p] * a[q] + b[p] * b[q];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) t[36 + p] = a[p] * r[0] + b[p] * r[1];
+    warp_tr44_add(t, acc1, acc2);
+  }
+  tr44_block_sum(acc1, acc2, sred, smw);
+#else
+  __shared__ double sm[(SSFM_TILE / 32) * CAM_V];
   double v[CAM_V];
 #pragma unroll
   for (int k = 0; k < CAM_V; ++k) v[k] = 0.0;
@@ -495,6 +599,7 @@ __global__ void __launch_bounds__(SSFM_TILE, LIN_MINB) ba_k_lin_tile(BADev d, co
     for (int k = 0; k < CAM_V; ++k) smw[k] = v[k];
   }
   __syncthreads();
+#endif
   if (threadIdx.x < 64) {
     double* dst = d.tilebuf + (long long)CAM_V * t0;
     for (int o = threadIdx.x; o < CAM_V; o += 64) dst[o] = smw[o];
@@ -901,12 +1006,43 @@ __global__ void __launch_bounds__(SSFM_TILE) ba_k_precond(BADev d) {
 #define PRE_MINB 1   // CTAs per SM (2: 128 registers with spills)
 #endif
 __global__ void __launch_bounds__(SSFM_TILE, PRE_MINB) ba_k_precond_grp(BADev d) {
-  __shared__ double sm[(SSFM_TILE / 32) * CAM_V];
   __shared__ double smw[CAM_V];
   const int g = blockIdx.x;
   const int t0 = d.topo.grp_tile[g], t1 = d.topo.grp_tile[g + 1];
   const int o0 = d.topo.tile_obs[t0], o1 = d.topo.tile_obs[t1];
   const double* cb = reinterpret_cast<const double*>(d.camlin + d.topo.tile_cam[t0]);
+#if LIN_TR
+  __shared__ double sred[SSFM_TILE / 32][48];
+  const unsigned long long pst = pol_evict_first();
+  const int lane = threadIdx.x & 31, wbase = o0 + (int)(threadIdx.x & ~31u);
+  double acc1 = 0.0, acc2 = 0.0;
+  int jn = wbase + lane < o1 ? ldg_stream_i(d.topo.cm_pt + wbase + lane, pst) : 0;
+  for (int base = wbase; base < o1; base += blockDim.x) {   // warp-uniform
+    const int i = base + lane;
+    const int j = jn;
+    if (i + (int)blockDim.x < o1) jn = ldg_stream_i(d.topo.cm_pt + i + blockDim.x, pst);
+    double a[8], b[8], k00 = 0.0, k01 = 0.0, k11 = 0.0, ty0 = 0.0, ty1 = 0.0;
+    if (i < o1) {
+      ba_precond_rows(d, i, j, cb, a, b, k00, k01, k11, ty0, ty1);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) { a[k] = 0.0; b[k] = 0.0; }
+    }
+    double ka[8], kb[8], t[CAM_V];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) { ka[p] = k00 * a[p] + k01 * b[p]; kb[p] = k01 * a[p] + k11 * b[p]; }
+    int idx = 0;
+#pragma unroll
+    for (int p = 0; p < 8; ++p)
+#pragma unroll
+      for (int q = p; q < 8; ++q) t[idx++] = a[p] * ka[q] + b[p] * kb[q];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) t[36 + p] = a[p] * ty0 + b[p] * ty1;
+    warp_tr44_add(t, acc1, acc2);
+  }
+  tr44_block_sum(acc1, acc2, sred, smw);
+#else
+  __shared__ double sm[(SSFM_TILE / 32) * CAM_V];
   double v[CAM_V];
 #pragma unroll
   for (int k = 0; k < CAM_V; ++k) v[k] = 0.0;
@@ -927,6 +1063,7 @@ __global__ void __launch_bounds__(SSFM_TILE, PRE_MINB) ba_k_precond_grp(BADev d)
     for (int k = 0; k < CAM_V; ++k) smw[k] = v[k];
   }
   __syncthreads();
+#endif
   if (threadIdx.x < 64) {
     double* dst = d.tilebuf + (long long)CAM_V * t0;
     for (int o = threadIdx.x; o < CAM_V; o += 64) dst[o] = ba_precond_f_entry(cb, smw, o);
