@@ -424,8 +424,11 @@ __global__ void __launch_bounds__(SSFM_TILE) ba_k_linearize_cm(BADev d, const do
 //    ba_k_linearize does (the same values: the records are bit-identical).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ double ba_precond_f_entry(const double* cb, const double* w, int o);
+#ifndef LIN_TR
+#define LIN_TR 1   // warp transpose-reduction of the tile-group sums (C5 non-PCG 7.2 -> 5.9 ms per LM iteration)
+#endif
 #ifndef LIN_MINB
-#define LIN_MINB 1
+#define LIN_MINB (LIN_TR ? 2 : 1)   // CTAs per SM of ba_k_lin_tile (TR: 128 registers, no spills)
 #endif
 #ifndef LIN_PF
 #define LIN_PF 1   // ba_k_lin_tile / ba_k_precond_grp: point indices one step ahead
@@ -467,9 +470,6 @@ __device__ __forceinline__ void ba_lin_obs(const BADev& d, const double* __restr
 // across the loop instead of 44 (the scalar kernels hold 44 and run at 232 /
 // 196 registers, 8 warps per SM). Fixed order: deterministic.
 // ---------------------------------------------------------------------------
-#ifndef LIN_TR
-#define LIN_TR 0
-#endif
 __device__ __forceinline__ void warp_tr44_add(const double (&t)[CAM_V], double& acc1, double& acc2) {
   const int lane = threadIdx.x & 31;
   {   // terms 0..31
@@ -611,7 +611,8 @@ __global__ void __launch_bounds__(SSFM_TILE, LIN_MINB) ba_k_lin_tile(BADev d, co
 
 __global__ void __launch_bounds__(256) ba_k_lin_points(BADev d, const double* __restrict__ theta,
                                                        double* gpt_norm_part) {
-  __shared__ double sm[8][SSFM_BATCH][LIN_V];
+  __shared__ __align__(16) double sm[8][SSFM_BATCH][LIN_V];
+  const int nv2 = d.fpt ? LIN_V / 2 : 5;   // Jp^T jf only for the shared focal: 9 of the 12 values
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -649,13 +650,24 @@ __global__ void __launch_bounds__(256) ba_k_lin_points(BADev d, const double* __
         val[10] = jp[1] * G[6] + jp[4] * G[7];
         val[11] = jp[2] * G[6] + jp[5] * G[7];
       }
+      // 16-byte shared-memory accesses (half the L1 wavefronts of 8-byte
+      // ones: this kernel is L1/TEX bound); same order of additions
+      double2* row = reinterpret_cast<double2*>(&sm[wib][lane][0]);
 #pragma unroll
-      for (int k = 0; k < LIN_V; ++k) sm[wib][lane][k] = val[k];
+      for (int k = 0; k < LIN_V / 2; ++k)
+        if (k < nv2) row[k] = make_double2(val[2 * k], val[2 * k + 1]);
       __syncwarp();
       const int a = max(ps, base), e = min(pe, base + SSFM_BATCH);
       for (int o = a; o < e; ++o) {
+        const double2* src = reinterpret_cast<const double2*>(&sm[wib][o - base][0]);
 #pragma unroll
-        for (int k = 0; k < LIN_V; ++k) acc[k] += sm[wib][o - base][k];
+        for (int k = 0; k < LIN_V / 2; ++k) {
+          if (k < nv2) {
+            const double2 x = src[k];
+            acc[2 * k] += x.x;
+            acc[2 * k + 1] += x.y;
+          }
+        }
       }
       __syncwarp();
     }
@@ -1003,7 +1015,7 @@ __global__ void __launch_bounds__(SSFM_TILE) ba_k_precond(BADev d) {
 // in its first tile's slot; its other tiles' slots are zero (the per-camera
 // sums over tiles are unchanged).
 #ifndef PRE_MINB
-#define PRE_MINB 1   // CTAs per SM (2: 128 registers with spills)
+#define PRE_MINB (LIN_TR ? 2 : 1)   // CTAs per SM (scalar sums at 2: spills)
 #endif
 __global__ void __launch_bounds__(SSFM_TILE, PRE_MINB) ba_k_precond_grp(BADev d) {
   __shared__ double smw[CAM_V];
