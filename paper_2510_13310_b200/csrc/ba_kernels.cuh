@@ -249,6 +249,9 @@ __device__ __forceinline__ void ba_obs_eval(const BAParams& bp, const BACam* __r
 // optional reference-layout exports (r_out [2N], J_out [22N] in observation order).
 // ---------------------------------------------------------------------------
 #define LIN_V 12   // Jp^T Jp (6), Jp^T r (3), Jp^T jf (3, shared focal only)
+#ifndef LP_V2
+#define LP_V2 1
+#endif
 __global__ void __launch_bounds__(256) ba_k_linearize(BADev d, const double* __restrict__ theta,
                                                       double* r_out, double* J_out, double* gpt_norm_part) {
   __shared__ double sm[8][SSFM_BATCH][LIN_V];
@@ -650,8 +653,7 @@ __global__ void __launch_bounds__(256) ba_k_lin_points(BADev d, const double* __
         val[10] = jp[1] * G[6] + jp[4] * G[7];
         val[11] = jp[2] * G[6] + jp[5] * G[7];
       }
-      // 16-byte shared-memory accesses (half the L1 wavefronts of 8-byte
-      // ones: this kernel is L1/TEX bound); same order of additions
+#if LP_V2   // 16-byte shared-memory accesses (half the L1 wavefronts of 8-byte ones: L1/TEX bound)
       double2* row = reinterpret_cast<double2*>(&sm[wib][lane][0]);
 #pragma unroll
       for (int k = 0; k < LIN_V / 2; ++k)
@@ -669,6 +671,16 @@ __global__ void __launch_bounds__(256) ba_k_lin_points(BADev d, const double* __
           }
         }
       }
+#else
+#pragma unroll
+      for (int k = 0; k < LIN_V; ++k) sm[wib][lane][k] = val[k];
+      __syncwarp();
+      const int a = max(ps, base), e = min(pe, base + SSFM_BATCH);
+      for (int o = a; o < e; ++o) {
+#pragma unroll
+        for (int k = 0; k < LIN_V; ++k) acc[k] += sm[wib][o - base][k];
+      }
+#endif
       __syncwarp();
     }
     if (my_pt < pb1) {
