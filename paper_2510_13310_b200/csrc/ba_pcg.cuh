@@ -297,7 +297,10 @@ __device__ __forceinline__ void ba_point_pass(const BADev& d, const double* v, d
 // (their addresses are already in registers): one DRAM latency per round
 // instead of index -> record -> gather. Same per-point summation order and
 // arithmetic as before: the output is bit-identical.
-template <bool RO = false>
+// BS: back-substitution (lm.py:674-690) instead of y: delta_j = y0_j - Cinv_j
+// sum_o Jp^T (Jc x_c), W = the per-camera vector of x, written at
+// y + off_pts + 3j
+template <bool RO = false, bool BS = false>
 __device__ __forceinline__ void ba_point_pass_w(const BADev& d, const double* W, double* y,
                                                 double (*sm)[SSFM_BATCH][3]) {
   const unsigned long long pstream = pol_evict_first(), pkeep = pol_evict_last();
@@ -373,8 +376,14 @@ __device__ __forceinline__ void ba_point_pass_w(const BADev& d, const double* W,
       for (int k = 0; k < 6; ++k) ci[k] = __ldg(d.Cinv + 6ll * my_pt + k);
 #endif
       sym3_matvec(ci, acc, w3);
+      if constexpr (BS) {
+        double* dst = y + d.bp.off_pts + 3ll * my_pt;
 #pragma unroll
-      for (int k = 0; k < 3; ++k) st_hint(y + 4ll * my_pt + k, w3[k], pkeep);
+        for (int k = 0; k < 3; ++k) dst[k] = d.y0[3ll * my_pt + k] - w3[k];
+      } else {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) st_hint(y + 4ll * my_pt + k, w3[k], pkeep);
+      }
     }
     ob0 = ob1; ob1 = nob1; pb0 = pb1;
   }
@@ -384,7 +393,10 @@ __device__ __forceinline__ void ba_point_pass_w(const BADev& d, const double* W,
 // Streams the 64-byte Jp + Jf record and the camera and point indices per
 // observation (the 16-double record and one index before), gathers W_c (64
 // bytes, L2-resident) and X_j (32 bytes).
-template <bool RO = false>
+// BS: back-substitution (lm.py:674-690) instead of y: delta_j = y0_j - Cinv_j
+// sum_o Jp^T (Jc x_c), W = the per-camera vector of x, written at
+// y + off_pts + 3j
+template <bool RO = false, bool BS = false>
 __device__ __forceinline__ void ba_point_pass_w(const BADev& d, const double* W, double* y,
                                                 double (*sm)[SSFM_BATCH][3]) {
   const unsigned long long pstream = pol_evict_first(), pkeep = pol_evict_last();
@@ -436,8 +448,14 @@ __device__ __forceinline__ void ba_point_pass_w(const BADev& d, const double* W,
       for (int k = 0; k < 6; ++k) ci[k] = __ldg(d.Cinv + 6ll * my_pt + k);
 #endif
       sym3_matvec(ci, acc, w);
+      if constexpr (BS) {
+        double* dst = y + d.bp.off_pts + 3ll * my_pt;
 #pragma unroll
-      for (int k = 0; k < 3; ++k) st_hint(y + 4ll * my_pt + k, w[k], pkeep);
+        for (int k = 0; k < 3; ++k) dst[k] = d.y0[3ll * my_pt + k] - w[k];
+      } else {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) st_hint(y + 4ll * my_pt + k, w[k], pkeep);
+      }
     }
   }
 }
@@ -1044,4 +1062,11 @@ __global__ void __launch_bounds__(PCG_THREADS, FAC ? CAMF_MINB : 4) k_op_camera(
   __shared__ double smred[(PCG_THREADS / 32) * 8];
   if constexpr (FAC) ba_camera_pass_f<true>(d, y, tile8);
   else ba_camera_pass<true>(d, y, tile8, smred);
+}
+
+// back-substitution of omega-form handles: the point pass with the W of x
+// (k_cam_wvec first) and the delta_j = y0_j - Cinv_j (.) finaliser
+__global__ void __launch_bounds__(PTP_THREADS, PTP_MINB) ba_k_backsub_w(BADev d, double* delta) {
+  __shared__ double smp[PTP_THREADS / 32][SSFM_BATCH][3];
+  ba_point_pass_w<true, true>(d, d.Wc, delta, smp);
 }

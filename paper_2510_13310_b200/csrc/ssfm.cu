@@ -1563,8 +1563,15 @@ static int launch_solve_pre(ssfm_handle* h, double lam, cudaStream_t st) {
 static int launch_solve_post(ssfm_handle* h, cudaStream_t st) {
   if (h->kind == 0) {
     BADev& d = h->ba;
-    if (d.Gpm) { k_cam_wvec<<<h->cam_blocks, 256, 0, st>>>(d, h->x, d.Wc); count_launch(h); }
-    ba_k_backsub<<<h->lin_blocks, 256, 0, st>>>(d, h->x, h->delta);
+    if (d.Gpm) {   // omega form: the pipelined point pass with the W of x (ba_k_backsub_w)
+      k_cam_wvec<<<h->cam_blocks, 256, 0, st>>>(d, h->x, d.Wc);
+      count_launch(h);
+      int occ = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)ba_k_backsub_w, PTP_THREADS, 0);
+      ba_k_backsub_w<<<std::max(1, occ) * h->num_sms, PTP_THREADS, 0, st>>>(d, h->delta);
+    } else {
+      ba_k_backsub<<<h->lin_blocks, 256, 0, st>>>(d, h->x, h->delta);
+    }
     ba_k_camdelta<<<h->cam_blocks, 256, 0, st>>>(d, h->x, h->delta);
     count_launch(h, 2);
   } else {
