@@ -91,7 +91,41 @@ class ClockSampler:
         self.lines = []
         self.thread = None
 
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:   # the CUDA device this rank uses (CUDA_VISIBLE_DEVICES may remap indices)
+            import torch
+            uuid = str(torch.cuda.get_device_properties(self.gpu).uuid)
+            return pynvml, pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+        except Exception:   # noqa: BLE001 - fall back to the index
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+
+    def _poll(self):
+        # NVML in-process every 200 ms: no nvidia-smi process whose queries can
+        # stall this process's CUDA calls (short timed regions caught 10-140 ms
+        # host stalls with the subprocess sampler)
+        nv, h = self.nv, self.h
+        smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self.halt.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((sm, smax, r))
+            except Exception:   # noqa: BLE001
+                pass
+            self.halt.wait(0.2)
+
     def start(self):
+        self.samples, self.nv = [], None
+        try:
+            self.nv, self.h = self._nvml_handle()
+            self.halt = threading.Event()
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return
+        except Exception:   # noqa: BLE001 - nvidia-smi below
+            self.nv = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
@@ -108,6 +142,19 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def stop(self):
+        if self.nv is not None:
+            self.halt.set()
+            self.thread.join(timeout=2)
+            nv = self.nv
+            bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+            sm = [x[0] for x in self.samples]
+            reasons = sorted({k for _, _, r in self.samples for k, b in bits.items() if r & b})
+            return {"sm_mhz": statistics.median(sm) if sm else None,
+                    "sm_max_mhz": self.samples[0][1] if self.samples else None,
+                    "reasons": reasons, "samples": len(sm), "sampler": "nvml 200 ms"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
