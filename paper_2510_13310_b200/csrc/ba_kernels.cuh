@@ -433,6 +433,9 @@ __device__ __forceinline__ double ba_precond_f_entry(const double* cb, const dou
 #ifndef LIN_MINB
 #define LIN_MINB (LIN_TR ? 2 : 1)   // CTAs per SM of ba_k_lin_tile (TR: 128 registers, no spills)
 #endif
+#ifndef LIN_STPOL
+#define LIN_STPOL 1   // C5 non-PCG 5.62 -> 5.50 ms per LM iteration (profiles/r2b/ab_linearize_store_policy_c5.log)
+#endif
 #ifndef LIN_PF
 #define LIN_PF 1   // ba_k_lin_tile / ba_k_precond_grp: point indices one step ahead
 #endif
@@ -444,8 +447,14 @@ __device__ __forceinline__ void ba_lin_obs_rows(const BADev& d, const double* __
   double J[BA_JREC], ct, F[BA_FREC + 3];
   ba_obs_eval(d.bp, d.cams + c, theta + d.bp.off_pts + 3ll * j, d.pix_cm + 2ll * i, r, J, &ct, F);
   fcm_store(d, i, F, pst);   // pinhole: s01, s11 are implied
+#if LIN_STPOL && GPM_AOS   // the scattered point-major records leave L2 first (the X gathers stay)
+  st_v4_hint(d.Gpm + 8ll * ip, J[8], J[9], J[10], J[11], pst);
+  st_v4_hint(d.Gpm + 8ll * ip + 4, J[12], J[13], J[14], J[15], pst);
+  st_v4_hint(d.Rpm + 4ll * ip, r[0], r[1], 0.0, 0.0, pst);
+#else
   gpm_store(d, ip, J + 8);
   *reinterpret_cast<double4*>(d.Rpm + 4ll * ip) = make_double4(r[0], r[1], 0.0, 0.0);
+#endif
   ba_jc_row(J, 0, a);
   ba_jc_row(J, 1, b);
 }

@@ -200,6 +200,13 @@ __device__ __forceinline__ double tiles_sum(const double* buf, int k, int t0, in
   return s;
 }
 
+// 32-byte store with an L2 eviction policy (a whole sector)
+__device__ __forceinline__ void st_v4_hint(double* a, double x0, double x1, double x2, double x3,
+                                           unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1,%2,%3,%4}, %5;" ::"l"(a), "d"(x0), "d"(x1), "d"(x2),
+               "d"(x3), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void st_hint(double* a, double v, unsigned long long pol) {
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
 }
