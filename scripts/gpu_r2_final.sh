@@ -8,8 +8,8 @@ timeout 2400 python -m pytest tests -m gpu -q -rA --timeout 300 --durations=15 -
 tail -n 6 gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -n 2 gpurun_out/smoke.log
 timeout 900 python bench.py > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
-timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 for c in c4ba c4gp c4 c1 c2gp c3; do timeout 400 python bench.py --config $c --no-cpu-baseline > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; done
+timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 cut -c1-250 gpurun_out/bench_*.json
 timeout 900 ncu --graph-profiling graph --metrics dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/traffic_r2c_c5.csv python scripts/dev_pcg_traffic.py c5 > gpurun_out/traffic_r2c_c5.log 2>&1
 tail -n 2 gpurun_out/traffic_r2c_c5.log
