@@ -270,3 +270,26 @@ def test_gp_graph_pcg_matches_persistent_kernel(gpu):
     b, rb = b2.lm_solve(gra, th, b2.LMConfig(max_iterations=10))
     assert [i.step_accepted for i in ra.iterations] == [i.step_accepted for i in rb.iterations]
     assert np.abs(a - b).max() < 1e-8
+
+
+@pytest.mark.parametrize("div", ["4", "37"])
+def test_point_pass_partition_independent(gpu, div):
+    """The graph PCG's point pass gives each warp a contiguous range of point
+    batches and prefetches the next round's indices across batch boundaries
+    (ba_point_pass_w). Every point is still summed by one owner lane in
+    observation order, so a smaller grid (another batch partition,
+    SSFM_PTP_GRID_DIV) must give bit-identical damped steps on the wide scene
+    (multi-round batches, points seen by up to 60 cameras)."""
+    st = wide_scene()
+    loss = b2.RobustLoss("huber", 1.0)
+    cfg = b2.LMConfig(cg_tol=1e-12, cg_max_iters=5000)
+    ref = with_env({"SSFM_FUSED": "0", "SSFM_PCG_GRAPH": "1"}, lambda: b2.BAProblem(st, loss))
+    alt = with_env({"SSFM_FUSED": "0", "SSFM_PCG_GRAPH": "1", "SSFM_PTP_GRID_DIV": div},
+                   lambda: b2.BAProblem(st, loss))
+    th = ref.encode()
+    ref.gradient(th)
+    alt.gradient(th)
+    for lam in (1e-4, 1e-1):
+        d0, it0 = solve_normal_native(gpu, ref, lam, cfg)
+        d1, it1 = solve_normal_native(gpu, alt, lam, cfg)
+        assert np.array_equal(d0, d1) and it0 == it1
