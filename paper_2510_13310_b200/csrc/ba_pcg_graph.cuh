@@ -301,6 +301,9 @@ __global__ void __launch_bounds__(256) k_g_pupdate(BADev d, CGGraphDev g, int nb
 #ifndef GV_CL
 #define GV_CL 8
 #endif
+// 16 (a non-portable cluster) was measured at the end of round 2: BA -1 % at C5,
+// but the GP vector phase then ends its CG loops at once (wrong steps)
+static_assert(GV_CL >= 1 && GV_CL <= 8, "GV_CL > 8 breaks the GP vector phase (k_gg_vec)");
 #define GV_THREADS 1024
 
 template <int NV>

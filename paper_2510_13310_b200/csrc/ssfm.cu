@@ -598,6 +598,8 @@ static int setup_gp_pcg_op(ssfm_handle* h, cudaStream_t st) {
   // 250k observations on single-rank handles; SSFM_GP_GRAPH=1 / 0 forces either
   const char* ge = getenv("SSFM_GP_GRAPH");
   h->graph_state = (ge ? ge[0] == '1' : h->topo.N >= 250000) ? 0 : -1;
+  // kernel attributes are set here, never while a graph is being captured
+  if (GV_CL > 8) CU(cudaFuncSetAttribute((const void*)k_gg_vec, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   return SSFM_OK;
 }
 
@@ -626,6 +628,8 @@ static int setup_ba_pcg(ssfm_handle* h, cudaStream_t st) {
       if (!(le && le[0] == '0')) DALLOC(d.Rpm, 4ll * d.Npad);
     }
   }
+  // kernel attributes are set here, never while a graph is being captured
+  if (GV_CL > 8) CU(cudaFuncSetAttribute((const void*)k_g_vec, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   const char* ge = getenv("SSFM_PCG_GRAPH");
   // two-pass operator from 250k observations: the graph wins well below C5
   // (3000 cameras / 800k obs: 0.067 vs 0.116 ms per CG iteration)
@@ -1313,7 +1317,6 @@ static void capture_ba_pcg_body(ssfm_handle* h, cudaStream_t cs, cudaGraphCondit
   const char* gv = getenv("SSFM_GVEC");
   const bool cluster = !(gv && gv[0] == '0');
   if (cluster) {
-    if (GV_CL > 8) cudaFuncSetAttribute((const void*)k_g_vec, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     k_g_vec<<<GV_CL, GV_THREADS, 0, cs>>>(d, h->fz, g, h->cm, hc);
   } else {
     k_g_q<<<CGV_BLOCKS, 256, 0, cs>>>(d, h->fz, g, h->cm);
@@ -1387,7 +1390,6 @@ static void capture_gp_pcg_body(ssfm_handle* h, cudaStream_t cs, cudaGraphCondit
   const char* gv = getenv("SSFM_GVEC");
   const bool cluster = !(gv && gv[0] == '0');
   if (cluster) {   // the vector phases as one thread-block cluster kernel
-    if (GV_CL > 8) cudaFuncSetAttribute((const void*)k_gg_vec, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     k_gg_vec<<<GV_CL, GV_THREADS, 0, cs>>>(d, g, hc);
   } else {
     k_gg_q<<<CGV_BLOCKS, 256, 0, cs>>>(d, g);
