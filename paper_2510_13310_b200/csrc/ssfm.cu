@@ -598,8 +598,6 @@ static int setup_gp_pcg_op(ssfm_handle* h, cudaStream_t st) {
   // 250k observations on single-rank handles; SSFM_GP_GRAPH=1 / 0 forces either
   const char* ge = getenv("SSFM_GP_GRAPH");
   h->graph_state = (ge ? ge[0] == '1' : h->topo.N >= 250000) ? 0 : -1;
-  // kernel attributes are set here, never while a graph is being captured
-  if (GV_CL > 8) CU(cudaFuncSetAttribute((const void*)k_gg_vec, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   return SSFM_OK;
 }
 
@@ -628,8 +626,6 @@ static int setup_ba_pcg(ssfm_handle* h, cudaStream_t st) {
       if (!(le && le[0] == '0')) DALLOC(d.Rpm, 4ll * d.Npad);
     }
   }
-  // kernel attributes are set here, never while a graph is being captured
-  if (GV_CL > 8) CU(cudaFuncSetAttribute((const void*)k_g_vec, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   const char* ge = getenv("SSFM_PCG_GRAPH");
   // two-pass operator from 250k observations: the graph wins well below C5
   // (3000 cameras / 800k obs: 0.067 vs 0.116 ms per CG iteration)
